@@ -1,0 +1,124 @@
+/*
+ * occ.h -- C ABI of the B200-native fast edge-aware occlusion detection
+ * (arXiv 2408.14050, §3 "Edge-aware Occlusion Detection", Eqs. 1-6).
+ *
+ * One call marks, for each peripheral camera of an array, the pixels of the
+ * fused centre-camera disparity map that the camera cannot see:
+ *
+ *   occ_detect(D [batch][H][W] fp32, device)  ->  M [batch][V][H][W] uint8 {0,1}
+ *
+ * The operation is the paper's detector with N = infinity (SURVEY.md §8.0
+ * S1-S9; readings Q1-Q21 in DESIGN.md §2):
+ *   PAPER.md:92-101  Eq. 1  E_x, E_y forward differences (f = (-1, 1)^T)
+ *   PAPER.md:103           E = sqrt(E_x^2 + E_y^2), Theta = angle of (E_x, E_y)
+ *   PAPER.md:105-109 Eq. 2  candidates: E > t_edge and |Theta - phi| < pi/2
+ *   PAPER.md:113-116 Eq. 3  L = ceil(2 s (max D - min D)), s = ||b||_inf
+ *   PAPER.md:117-129 Eq. 4  scan lines of length L along the baseline, W = G + s V
+ *   PAPER.md:131-144 Eq. 5  neighbours with |W_i - W_j| < t_dist and larger
+ *                           disparity (by more than t_disp) occlude
+ *   PAPER.md:145-151 Eq. 6  M = 1 where the occlusion count is positive
+ * Every step runs in the library's own sm_100a CUDA kernels; there is no CPU
+ * fallback.  The result is bit-identical to the test oracle (oracle/).
+ *
+ * Conventions
+ *   - D is row-major fp32, x rightward, y downward, contiguous,
+ *     device memory owned by the caller; frames are [H][W] back to back.
+ *   - A baseline b = (bx, by) is the offset of a peripheral camera from the
+ *     centre camera in units of the grid spacing; that camera sees centre
+ *     pixel p at p - D(p) b.  |bx|, |by| <= 8, b != (0, 0).
+ *   - masks is caller-owned device memory, [batch][n_views][H][W] uint8;
+ *     every byte is written (0 or 1).  masks must not alias disparity.
+ *   - Stream ordered: occ_detect enqueues work on the given cudaStream_t and
+ *     returns without synchronising.  Argument errors are returned
+ *     synchronously; data errors (non-finite input) are reported per frame
+ *     by occ_status, and that frame's masks are all zero.
+ *   - A context must not be used concurrently from two host threads/streams.
+ */
+#ifndef OCC_H
+#define OCC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct occ_ctx occ_ctx;                       /* opaque; owns device scratch */
+
+typedef struct { int32_t bx, by; } occ_baseline;       /* peripheral camera offset */
+
+/* PAPER.md:187 (§4.1): t_e = 1.0, t_dist = 2.0, t_disp = 0.5; SPEC.md:153 cap 4096.
+ * Valid ranges: t_edge > 0 finite; t_dist in [2^-12, 2^16];
+ * t_disp in [0, 2^16]; max_scan in [1, 65536]. */
+typedef struct { float t_edge, t_dist, t_disp; int32_t max_scan; } occ_params;
+
+enum {
+    OCC_OK = 0,
+    OCC_ERR_INVALID_ARG = -1,   /* bad sizes, pointers, params or baselines */
+    OCC_ERR_CUDA = -2,          /* a CUDA runtime call failed */
+    OCC_ERR_OOM = -3,           /* device allocation failed */
+    OCC_ERR_NONFINITE = -4,     /* per-frame status: NaN/Inf in the input */
+    OCC_ERR_UNSUPPORTED = -5    /* |bx| or |by| > 8, or too many views */
+};
+
+/* Paths (occ_set_path): AUTO picks the tiled sweep kernel and falls back to
+ * the direct per-pixel kernel for frames whose scan half-length exceeds the
+ * tile halo.  DIRECT forces the per-pixel kernel (debug / cross-check). */
+enum { OCC_PATH_AUTO = 0, OCC_PATH_TILED = 1, OCC_PATH_DIRECT = 2 };
+
+/* Fills the paper's defaults. */
+void occ_default_params(occ_params *p);
+
+/* Creates a context for H x W maps and n_views baselines (copied).
+ * params == NULL selects the defaults.  max_batch bounds occ_detect's batch.
+ * Allocates only small per-frame scratch (O(max_batch) bytes).  Requires a
+ * current CUDA device with compute capability 10.0 (sm_100a).
+ * Errors: OCC_ERR_INVALID_ARG (H < 2, W < 2, H or W > 32768, n_views < 1,
+ * b == (0,0), params out of range, max_batch < 1, out == NULL),
+ * OCC_ERR_UNSUPPORTED (|b| component > 8 or n_views > 64), OCC_ERR_CUDA,
+ * OCC_ERR_OOM. */
+int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_views,
+               const occ_params *params, int32_t max_batch, occ_ctx **out);
+
+/* Enqueues detection for `batch` frames.  disparity: device [batch][H][W]
+ * fp32; masks: device [batch][n_views][H][W] uint8.  cuda_stream is a
+ * cudaStream_t (NULL = legacy default stream).  Returns OCC_OK or
+ * OCC_ERR_INVALID_ARG (null pointers, batch < 1 or > max_batch) /
+ * OCC_ERR_CUDA (launch failure). */
+int occ_detect(occ_ctx *ctx, const float *disparity, uint8_t *masks, int32_t batch,
+               void *cuda_stream);
+
+/* Same operation on HOST buffers (pageable or pinned): copies D to the
+ * context's device staging buffer, detects, copies the masks back, and
+ * synchronises the stream before returning.  Staging buffers are allocated
+ * on first use (max_batch frames).  Used for end-to-end timing. */
+int occ_detect_host(occ_ctx *ctx, const float *disparity_host, uint8_t *masks_host,
+                    int32_t batch, void *cuda_stream);
+
+/* Synchronises the stream of the last occ_detect and writes one status per
+ * frame of that call (OCC_OK or OCC_ERR_NONFINITE) to host memory
+ * frame_status[batch].  Returns OCC_OK or OCC_ERR_CUDA. */
+int occ_status(occ_ctx *ctx, int32_t *frame_status);
+
+/* Synchronises and reports the per-frame statistics of the last call:
+ * dmin/dmax (exact, S1) and the scan half-length h of every view (S5);
+ * h_per_view has n_views entries.  Any output pointer may be NULL. */
+int occ_frame_info(occ_ctx *ctx, int32_t frame, float *dmin, float *dmax, int32_t *h_per_view);
+
+/* Selects the kernel path for subsequent calls (OCC_PATH_*). */
+int occ_set_path(occ_ctx *ctx, int32_t path);
+
+/* Number of kernel launches the last occ_detect enqueued. */
+int32_t occ_last_launches(const occ_ctx *ctx);
+
+/* Releases the context and its device scratch (synchronises first). */
+int occ_destroy(occ_ctx *ctx);
+
+const char *occ_strerror(int code);
+
+/* ABI version (major*10000 + minor*100 + patch). */
+int32_t occ_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

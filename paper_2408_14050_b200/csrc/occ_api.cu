@@ -1,0 +1,333 @@
+// occ_api.cu -- host side of libocc: the C ABI of include/occ.h.
+//
+// Owns validation, the view/family descriptors (digital-line geometry of
+// SURVEY §8.0 S6), the exact fp32 thresholds of the Eq. 5 test, per-frame
+// scratch, and launch sequencing on the caller's stream.  All arithmetic of
+// the method runs in the kernels (k_stats.cu, k_tile.cu, k_direct.cu).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "occ_internal.h"
+
+using namespace occ;
+
+struct occ_ctx {
+    int32_t H = 0, W = 0, V = 0, nfam = 0, max_batch = 0, device = 0;
+    int32_t path = OCC_PATH_AUTO;
+    Params params{};
+    std::vector<ViewDesc> views;
+    std::vector<FamilyDesc> fams;
+    ViewDesc *d_views = nullptr;
+    FamilyDesc *d_fams = nullptr;
+    FrameStats *d_stats = nullptr;
+    uint32_t *d_cand = nullptr;          // direct path scratch (lazy)
+    int64_t cand_frames = 0;
+    float *d_stage_D = nullptr;          // occ_detect_host staging (lazy)
+    uint8_t *d_stage_M = nullptr;
+    cudaStream_t last_stream = nullptr;
+    int32_t last_batch = 0;
+    int32_t last_launches = 0;
+};
+
+namespace {
+
+int32_t igcd(int32_t a, int32_t b) {
+    a = std::abs(a); b = std::abs(b);
+    while (b) { int32_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+// Largest fp32 f with s*f <= A (A exact in binary64): delta > A/s <=> delta > f
+float rd_div(double A, int32_t s) {
+    float f = (float)(A / s);
+    while ((double)s * (double)f > A) f = std::nextafter(f, -INFINITY);
+    for (;;) {
+        float n = std::nextafter(f, INFINITY);
+        if ((double)s * (double)n <= A) f = n; else break;
+    }
+    return f;
+}
+
+// Smallest fp32 f with s*f >= B: delta < B/s <=> delta < f
+float ru_div(double B, int32_t s) {
+    float f = (float)(B / s);
+    while ((double)s * (double)f < B) f = std::nextafter(f, INFINITY);
+    for (;;) {
+        float n = std::nextafter(f, -INFINITY);
+        if ((double)s * (double)n >= B) f = n; else break;
+    }
+    return f;
+}
+
+// Largest fp32 x >= 0 with sqrt_rn(x) <= t: sqrt_rn is monotone, so
+// sqrt_rn(e2) > t  <=>  e2 > x   (exact rewrite of PAPER.md:103's E > t_e).
+float sqrt_thresh(float t) {
+    double t2 = (double)t * (double)t;
+    float x = t2 > 3.0e38 ? 3.4028234663852886e38f : (float)t2;
+    while (x > 0.0f && std::sqrt(x) > t) x = std::nextafter(x, 0.0f);
+    for (;;) {
+        float n = std::nextafter(x, INFINITY);
+        if (std::isfinite(n) && std::sqrt(n) <= t) x = n; else break;
+    }
+    return x;
+}
+
+int validate(int32_t H, int32_t W, const occ_baseline *b, int32_t V, const occ_params &p) {
+    if (H < 2 || W < 2 || H > 32768 || W > 32768) return OCC_ERR_INVALID_ARG;
+    if (V < 1 || b == nullptr) return OCC_ERR_INVALID_ARG;
+    if (V > kMaxViews) return OCC_ERR_UNSUPPORTED;
+    if (!(std::isfinite(p.t_edge) && p.t_edge > 0.0f)) return OCC_ERR_INVALID_ARG;
+    if (!(p.t_dist >= 0x1p-12f && p.t_dist <= 0x1p16f)) return OCC_ERR_INVALID_ARG;
+    if (!(p.t_disp >= 0.0f && p.t_disp <= 0x1p16f)) return OCC_ERR_INVALID_ARG;
+    if (p.max_scan < 1 || p.max_scan > 65536) return OCC_ERR_INVALID_ARG;
+    for (int32_t i = 0; i < V; ++i) {
+        if (b[i].bx == 0 && b[i].by == 0) return OCC_ERR_INVALID_ARG;
+        if (std::abs(b[i].bx) > 8 || std::abs(b[i].by) > 8) return OCC_ERR_UNSUPPORTED;
+    }
+    return OCC_OK;
+}
+
+// Near/far split of the Eq. 5 offsets for one view:
+// backward offsets j >= jstar satisfy delta > t_disp automatically
+// (s delta > j - t_dist >= s t_disp); forward offsets need f < t_dist - s t_disp.
+void near_far(ViewDesc &vd, const occ_params &p) {
+    const double t = p.t_dist, sd = (double)vd.s * (double)p.t_disp;
+    int32_t j = 1;
+    while ((double)j - t < sd) ++j;
+    vd.jstar = j;
+    vd.nback = j - 1;
+    int32_t f = 0;
+    while ((double)(f + 1) < t - sd) ++f;
+    vd.nfwd = f;
+    for (int32_t i = 0; i < kMaxNear; ++i) {
+        vd.back_lo[i] = vd.back_hi[i] = vd.fwd_lo[i] = vd.fwd_hi[i] = 0.0f;
+    }
+    // delta in (lo, hi) <=> delta > t_disp and -t < dk + s delta < t   (S7)
+    for (int32_t i = 0; i < vd.nback && i < kMaxNear; ++i) {
+        const double dk = -(double)(i + 1);
+        vd.back_lo[i] = std::fmax(p.t_disp, rd_div(-t - dk, vd.s));
+        vd.back_hi[i] = ru_div(t - dk, vd.s);
+    }
+    for (int32_t i = 0; i < vd.nfwd && i < kMaxNear; ++i) {
+        const double dk = (double)(i + 1);
+        vd.fwd_lo[i] = std::fmax(p.t_disp, rd_div(-t - dk, vd.s));
+        vd.fwd_hi[i] = ru_div(t - dk, vd.s);
+    }
+}
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return OCC_ERR_CUDA; } while (0)
+
+int ensure_cand(occ_ctx *c, int32_t frames) {
+    if (c->d_cand && c->cand_frames >= frames) return OCC_OK;
+    if (c->d_cand) { cudaFree(c->d_cand); c->d_cand = nullptr; }
+    size_t bytes = (size_t)frames * c->H * c->W * sizeof(uint32_t);
+    if (cudaMalloc(&c->d_cand, bytes) != cudaSuccess) { cudaGetLastError(); return OCC_ERR_OOM; }
+    c->cand_frames = frames;
+    return OCC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void occ_default_params(occ_params *p) {
+    if (!p) return;
+    p->t_edge = 1.0f;
+    p->t_dist = 2.0f;
+    p->t_disp = 0.5f;
+    p->max_scan = 4096;
+}
+
+int32_t occ_version(void) { return 10000; }
+
+const char *occ_strerror(int code) {
+    switch (code) {
+        case OCC_OK: return "ok";
+        case OCC_ERR_INVALID_ARG: return "invalid argument";
+        case OCC_ERR_CUDA: return "CUDA runtime error";
+        case OCC_ERR_OOM: return "out of device memory";
+        case OCC_ERR_NONFINITE: return "non-finite disparity in frame";
+        case OCC_ERR_UNSUPPORTED: return "unsupported baseline or view count";
+        default: return "unknown error";
+    }
+}
+
+int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_views,
+               const occ_params *params, int32_t max_batch, occ_ctx **out) {
+    if (!out) return OCC_ERR_INVALID_ARG;
+    *out = nullptr;
+    occ_params p;
+    occ_default_params(&p);
+    if (params) p = *params;
+    int rc = validate(H, W, baselines, n_views, p);
+    if (rc != OCC_OK) return rc;
+    if (max_batch < 1) return OCC_ERR_INVALID_ARG;
+
+    occ_ctx *c = new (std::nothrow) occ_ctx();
+    if (!c) return OCC_ERR_OOM;
+    c->H = H; c->W = W; c->V = n_views; c->max_batch = max_batch;
+    c->params.t_edge = p.t_edge;
+    c->params.t_dist = p.t_dist;
+    c->params.t_disp = p.t_disp;
+    c->params.max_scan = p.max_scan;
+    c->params.e2_thresh = sqrt_thresh(p.t_edge);
+
+    // families: lines shared by +-m b0 (S6); b0 reduced with positive major
+    for (int32_t i = 0; i < n_views; ++i) {
+        ViewDesc vd{};
+        vd.bx = baselines[i].bx; vd.by = baselines[i].by;
+        vd.s = std::max(std::abs(vd.bx), std::abs(vd.by));
+        vd.xmajor = std::abs(vd.bx) >= std::abs(vd.by) ? 1 : 0;
+        const int32_t g = igcd(vd.bx, vd.by);
+        int32_t b0x = vd.bx / g, b0y = vd.by / g;
+        const int32_t major = vd.xmajor ? b0x : b0y;
+        vd.sg = major > 0 ? 1 : -1;
+        if (vd.sg < 0) { b0x = -b0x; b0y = -b0y; }
+        if (vd.xmajor) { vd.num = b0y; vd.den = b0x; }
+        else { vd.num = b0x; vd.den = b0y; }
+        int32_t fam = -1;
+        for (size_t k = 0; k < c->fams.size(); ++k)
+            if (c->fams[k].b0x == b0x && c->fams[k].b0y == b0y) fam = (int32_t)k;
+        if (fam < 0) {
+            if ((int32_t)c->fams.size() >= kMaxFamilies) { delete c; return OCC_ERR_UNSUPPORTED; }
+            FamilyDesc fd{};
+            fd.b0x = b0x; fd.b0y = b0y; fd.xmajor = vd.xmajor; fd.num = vd.num; fd.den = vd.den;
+            fd.nviews = 0;
+            c->fams.push_back(fd);
+            fam = (int32_t)c->fams.size() - 1;
+        }
+        FamilyDesc &fd = c->fams[fam];
+        fd.view[fd.nviews++] = i;
+        vd.fam = fam;
+        vd.candbit = 2 * fam + (vd.sg < 0 ? 1 : 0);
+        near_far(vd, p);
+        c->views.push_back(vd);
+    }
+    c->nfam = (int32_t)c->fams.size();
+
+    if (cudaGetDevice(&c->device) != cudaSuccess) { cudaGetLastError(); delete c; return OCC_ERR_CUDA; }
+    if (cudaMalloc(&c->d_views, sizeof(ViewDesc) * c->views.size()) != cudaSuccess ||
+        cudaMalloc(&c->d_fams, sizeof(FamilyDesc) * c->fams.size()) != cudaSuccess ||
+        cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess) {
+        cudaGetLastError();
+        occ_destroy(c);
+        return OCC_ERR_OOM;
+    }
+    if (cudaMemcpy(c->d_views, c->views.data(), sizeof(ViewDesc) * c->views.size(),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_fams, c->fams.data(), sizeof(FamilyDesc) * c->fams.size(),
+                   cudaMemcpyHostToDevice) != cudaSuccess) {
+        occ_destroy(c);
+        return OCC_ERR_CUDA;
+    }
+    *out = c;
+    return OCC_OK;
+}
+
+int occ_set_path(occ_ctx *c, int32_t path) {
+    if (!c || path < OCC_PATH_AUTO || path > OCC_PATH_DIRECT) return OCC_ERR_INVALID_ARG;
+    c->path = path;
+    return OCC_OK;
+}
+
+int32_t occ_last_launches(const occ_ctx *c) { return c ? c->last_launches : -1; }
+
+int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stream) {
+    if (!c || !D || !M || batch < 1 || batch > c->max_batch) return OCC_ERR_INVALID_ARG;
+    const int64_t HW = (int64_t)c->H * c->W;
+    {   // masks must not alias the input
+        const char *d0 = (const char *)D, *d1 = d0 + (size_t)batch * HW * sizeof(float);
+        const char *m0 = (const char *)M, *m1 = m0 + (size_t)batch * c->V * HW;
+        if (m0 < d1 && d0 < m1) return OCC_ERR_INVALID_ARG;
+    }
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    int launches = 0;
+    CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
+    CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
+    {
+        int rc = ensure_cand(c, batch);
+        if (rc != OCC_OK) return rc;
+        CK(launch_cand(D, c->H, c->W, batch, c->d_fams, c->nfam, c->params, c->d_cand, s)); ++launches;
+        CK(launch_direct(D, c->d_cand, c->H, c->W, batch, c->d_views, c->V, c->d_stats,
+                         c->params, M, s)); ++launches;
+    }
+    c->last_stream = s;
+    c->last_batch = batch;
+    c->last_launches = launches;
+    return OCC_OK;
+}
+
+int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, void *stream) {
+    if (!c || !Dh || !Mh || batch < 1 || batch > c->max_batch) return OCC_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    const size_t HW = (size_t)c->H * c->W;
+    if (!c->d_stage_D) {
+        if (cudaMalloc(&c->d_stage_D, (size_t)c->max_batch * HW * sizeof(float)) != cudaSuccess ||
+            cudaMalloc(&c->d_stage_M, (size_t)c->max_batch * c->V * HW) != cudaSuccess) {
+            cudaGetLastError();
+            return OCC_ERR_OOM;
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(c->d_stage_D, Dh, (size_t)batch * HW * sizeof(float),
+                       cudaMemcpyHostToDevice, s));
+    int rc = occ_detect(c, c->d_stage_D, c->d_stage_M, batch, stream);
+    if (rc != OCC_OK) return rc;
+    CK(cudaMemcpyAsync(Mh, c->d_stage_M, (size_t)batch * c->V * HW, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return OCC_OK;
+}
+
+int occ_status(occ_ctx *c, int32_t *frame_status) {
+    if (!c || !frame_status) return OCC_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->last_stream));
+    std::vector<FrameStats> st((size_t)c->last_batch);
+    if (c->last_batch > 0)
+        CK(cudaMemcpy(st.data(), c->d_stats, sizeof(FrameStats) * st.size(), cudaMemcpyDeviceToHost));
+    for (int32_t i = 0; i < c->last_batch; ++i)
+        frame_status[i] = st[(size_t)i].nonfinite ? OCC_ERR_NONFINITE : OCC_OK;
+    return OCC_OK;
+}
+
+int occ_frame_info(occ_ctx *c, int32_t frame, float *dmin, float *dmax, int32_t *h_per_view) {
+    if (!c || frame < 0 || frame >= c->last_batch) return OCC_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->last_stream));
+    FrameStats fs;
+    CK(cudaMemcpy(&fs, c->d_stats + frame, sizeof(fs), cudaMemcpyDeviceToHost));
+    const float lo = key_float(fs.minkey), hi = key_float(fs.maxkey);
+    if (dmin) *dmin = lo;
+    if (dmax) *dmax = hi;
+    if (h_per_view) {
+        const float R = hi - lo;
+        for (int32_t v = 0; v < c->V; ++v) {
+            double L = std::ceil(2.0 * (double)c->views[v].s * (double)R);
+            if (!(L <= (double)c->params.max_scan)) L = c->params.max_scan;
+            h_per_view[v] = fs.nonfinite ? 0 : ((int32_t)L) / 2;
+        }
+    }
+    return OCC_OK;
+}
+
+int occ_destroy(occ_ctx *c) {
+    if (!c) return OCC_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    if (c->last_stream || c->last_batch) cudaStreamSynchronize(c->last_stream);
+    cudaFree(c->d_views);
+    cudaFree(c->d_fams);
+    cudaFree(c->d_stats);
+    cudaFree(c->d_cand);
+    cudaFree(c->d_stage_D);
+    cudaFree(c->d_stage_M);
+    delete c;
+    return OCC_OK;
+}
+
+}  // extern "C"

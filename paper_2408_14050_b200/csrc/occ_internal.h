@@ -1,0 +1,91 @@
+// occ_internal.h -- device-side descriptors shared by the host library and
+// the sm_100a kernels of libocc.  Product code only (never includes oracle/).
+#pragma once
+#include <cstdint>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "../../include/occ.h"
+
+namespace occ {
+
+constexpr int kMaxViews = 64;
+constexpr int kMaxFamilies = 16;
+constexpr int kMaxNear = 8;        // near partners handled by fp32 thresholds
+
+// One peripheral view (baseline b).  Geometry of its digital epipolar lines
+// (SURVEY §8.0 S6): x-major when |bx| >= |by|: pos = x, line = y - floor(x num/den);
+// y-major: pos = y, line = x - floor(y num/den).  u = sg * pos increases toward
+// the "backward" partners (the side the occluders of this view come from).
+struct ViewDesc {
+    int32_t bx, by;
+    int32_t s;          // ||b||_inf (Eq. 3 / W scaling, readings Q6, Q9)
+    int32_t xmajor;     // 1: pos = x
+    int32_t sg;         // sign of the major component of b (+1 / -1)
+    int32_t num, den;   // reduced slope of the family (den > 0)
+    int32_t fam;        // family index (lines shared by +-m b0)
+    int32_t candbit;    // bit of the per-pixel candidate code: 2*fam + (sg < 0)
+    int32_t jstar;      // first backward offset whose Eq. 5 test implies delta > t_disp
+    int32_t nback;      // near backward offsets j = 1..nback (nback = jstar-1)
+    int32_t nfwd;       // near forward offsets f = 1..nfwd
+    // exact fp32 thresholds: delta in (lo, hi) <=> Eq. 5 test holds
+    float back_lo[kMaxNear], back_hi[kMaxNear];   // dk = -j, j = 1..nback
+    float fwd_lo[kMaxNear], fwd_hi[kMaxNear];     // dk = +f, f = 1..nfwd
+};
+
+struct FamilyDesc {
+    int32_t b0x, b0y;   // reduced base direction, major component > 0
+    int32_t xmajor, num, den;
+    int32_t nviews;
+    int32_t view[kMaxViews];   // indices into ViewDesc[]
+};
+
+struct Params {
+    float t_edge, t_dist, t_disp;
+    int32_t max_scan;
+    float e2_thresh;    // largest fp32 x with sqrt_rn(x) <= t_edge: E > t_e <=> e2 > e2_thresh
+};
+
+// Per-frame statistics written by k_stats (S1) -- ordered-int keys so that
+// atomicMin/atomicMax give the exact fp32 min/max.
+struct FrameStats {
+    int32_t minkey, maxkey;
+    uint32_t nonfinite;
+    int32_t pad;
+};
+
+__host__ __device__ inline int32_t float_key(float f) {
+#ifdef __CUDA_ARCH__
+    int32_t b = __float_as_int(f);
+#else
+    int32_t b; memcpy(&b, &f, 4);
+#endif
+    return b >= 0 ? b : (b ^ 0x7FFFFFFF);
+}
+__host__ __device__ inline float key_float(int32_t k) {
+    int32_t b = k >= 0 ? k : (k ^ 0x7FFFFFFF);
+#ifdef __CUDA_ARCH__
+    return __int_as_float(b);
+#else
+    float f; memcpy(&f, &b, 4); return f;
+#endif
+}
+
+__host__ __device__ inline int32_t floordiv(int32_t a, int32_t d) {   // d > 0
+    int32_t q = a / d;
+    if ((a % d) != 0 && a < 0) q -= 1;
+    return q;
+}
+
+// Launchers (k_*.cu)
+cudaError_t launch_stats_init(FrameStats *st, int32_t batch, cudaStream_t s);
+cudaError_t launch_stats(const float *D, int64_t HW, int32_t batch, FrameStats *st, cudaStream_t s);
+cudaError_t launch_cand(const float *D, int32_t H, int32_t W, int32_t batch,
+                        const FamilyDesc *fams, int32_t nfam, const Params &p,
+                        uint32_t *cand, cudaStream_t s);
+cudaError_t launch_direct(const float *D, const uint32_t *cand, int32_t H, int32_t W,
+                          int32_t batch, const ViewDesc *views, int32_t nviews,
+                          const FrameStats *st, const Params &p, uint8_t *masks,
+                          cudaStream_t s);
+
+}  // namespace occ

@@ -1,0 +1,216 @@
+"""Thin Python binding of libocc's C ABI (include/occ.h) -- marshalling only.
+
+Every step of the detector runs in libocc's sm_100a CUDA kernels; this module
+only passes pointers, sizes and the current torch CUDA stream.  There is no
+CPU or PyTorch fallback: if ``libocc.so`` is missing or cannot be loaded the
+import of :class:`Detector` fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libocc.so")
+
+OCC_OK = 0
+OCC_ERR_INVALID_ARG = -1
+OCC_ERR_CUDA = -2
+OCC_ERR_OOM = -3
+OCC_ERR_NONFINITE = -4
+OCC_ERR_UNSUPPORTED = -5
+PATHS = {"auto": 0, "tiled": 1, "direct": 2}
+
+# every function include/occ.h declares (checked against the header by tests)
+EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", "occ_status",
+           "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
+           "occ_version"]
+
+
+class occ_baseline(ctypes.Structure):
+    _fields_ = [("bx", ctypes.c_int32), ("by", ctypes.c_int32)]
+
+
+class occ_params(ctypes.Structure):
+    _fields_ = [("t_edge", ctypes.c_float), ("t_dist", ctypes.c_float),
+                ("t_disp", ctypes.c_float), ("max_scan", ctypes.c_int32)]
+
+
+class OccError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {strerror(code)} ({code})")
+        self.code = code
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libocc.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libocc.so not found at {LIB_PATH}: run `python -c "
+                               f"'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32 = ctypes.c_void_p, ctypes.c_int32
+        L.occ_default_params.argtypes = [ctypes.POINTER(occ_params)]
+        L.occ_default_params.restype = None
+        L.occ_create.argtypes = [i32, i32, ctypes.POINTER(occ_baseline), i32,
+                                 ctypes.POINTER(occ_params), i32, ctypes.POINTER(vp)]
+        L.occ_create.restype = ctypes.c_int
+        L.occ_detect.argtypes = [vp, vp, vp, i32, vp]
+        L.occ_detect.restype = ctypes.c_int
+        L.occ_detect_host.argtypes = [vp, vp, vp, i32, vp]
+        L.occ_detect_host.restype = ctypes.c_int
+        L.occ_status.argtypes = [vp, ctypes.POINTER(i32)]
+        L.occ_status.restype = ctypes.c_int
+        L.occ_frame_info.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_float),
+                                     ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
+        L.occ_frame_info.restype = ctypes.c_int
+        L.occ_set_path.argtypes = [vp, i32]
+        L.occ_set_path.restype = ctypes.c_int
+        L.occ_last_launches.argtypes = [vp]
+        L.occ_last_launches.restype = i32
+        L.occ_destroy.argtypes = [vp]
+        L.occ_destroy.restype = ctypes.c_int
+        L.occ_strerror.argtypes = [ctypes.c_int]
+        L.occ_strerror.restype = ctypes.c_char_p
+        L.occ_version.argtypes = []
+        L.occ_version.restype = i32
+        _lib = L
+    return _lib
+
+
+def strerror(code: int) -> str:
+    try:
+        return lib().occ_strerror(code).decode()
+    except Exception:  # pragma: no cover - message formatting only
+        return str(code)
+
+
+def default_params() -> occ_params:
+    p = occ_params()
+    lib().occ_default_params(ctypes.byref(p))
+    return p
+
+
+def create_raw(H: int, W: int, baselines: Sequence[Tuple[int, int]], params: Optional[occ_params],
+               max_batch: int = 1) -> Tuple[int, Optional[int]]:
+    """Call occ_create; returns (rc, handle or None).  Used by ABI tests."""
+    arr = (occ_baseline * max(1, len(baselines)))(*[occ_baseline(int(a), int(b)) for a, b in baselines])
+    h = ctypes.c_void_p()
+    rc = lib().occ_create(int(H), int(W), arr if len(baselines) else None, len(baselines),
+                          ctypes.byref(params) if params is not None else None, int(max_batch),
+                          ctypes.byref(h))
+    return rc, (h.value if rc == OCC_OK else None)
+
+
+class Detector:
+    """``Detector(H, W, baselines).detect(D)`` -> uint8 masks [B, V, H, W].
+
+    D: torch.float32 CUDA tensor [B, H, W] (or [H, W]), contiguous.  The call
+    is enqueued on the current torch CUDA stream and does not synchronise.
+    """
+
+    def __init__(self, H: int, W: int, baselines: Sequence[Tuple[int, int]], t_edge: float = 1.0,
+                 t_dist: float = 2.0, t_disp: float = 0.5, max_scan: int = 4096, max_batch: int = 1,
+                 path: str = "auto"):
+        self.H, self.W = int(H), int(W)
+        self.baselines: List[Tuple[int, int]] = [(int(a), int(b)) for a, b in baselines]
+        self.V = len(self.baselines)
+        self.max_batch = int(max_batch)
+        p = occ_params(t_edge, t_dist, t_disp, max_scan)
+        rc, h = create_raw(self.H, self.W, self.baselines, p, self.max_batch)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_create")
+        self._h = h
+        self._last_batch = 0
+        self.set_path(path)
+
+    def set_path(self, path: str) -> None:
+        rc = lib().occ_set_path(self._h, PATHS[path])
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_set_path")
+
+    def detect(self, D, out=None, stream=None):
+        import torch
+        if D.dim() == 2:
+            D = D.unsqueeze(0)
+        if D.dtype != torch.float32 or not D.is_cuda or not D.is_contiguous():
+            raise ValueError("D must be a contiguous float32 CUDA tensor [B, H, W]")
+        B = D.shape[0]
+        if tuple(D.shape[1:]) != (self.H, self.W):
+            raise ValueError(f"expected [B, {self.H}, {self.W}], got {tuple(D.shape)}")
+        if out is None:
+            out = torch.empty((B, self.V, self.H, self.W), dtype=torch.uint8, device=D.device)
+        elif out.dtype != torch.uint8 or not out.is_contiguous() or out.numel() < B * self.V * self.H * self.W:
+            raise ValueError("out must be a contiguous uint8 CUDA tensor [B, V, H, W]")
+        s = stream if stream is not None else torch.cuda.current_stream(D.device)
+        rc = lib().occ_detect(self._h, D.data_ptr(), out.data_ptr(), B, s.cuda_stream)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_detect")
+        self._last_batch = B
+        return out
+
+    def detect_host(self, D: np.ndarray, out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
+        """Host buffers in, host masks out; copies and synchronisation inside."""
+        D = np.ascontiguousarray(D, dtype=np.float32)
+        if D.ndim == 2:
+            D = D[None]
+        B = D.shape[0]
+        if out is None:
+            out = np.empty((B, self.V, self.H, self.W), dtype=np.uint8)
+        sp = 0
+        if stream is not None:
+            sp = stream.cuda_stream
+        else:
+            try:
+                import torch
+                sp = torch.cuda.current_stream().cuda_stream
+            except Exception:
+                sp = 0
+        rc = lib().occ_detect_host(self._h, D.ctypes.data, out.ctypes.data, B, sp)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_detect_host")
+        self._last_batch = B
+        return out
+
+    def detect_host_ptr(self, d_ptr: int, m_ptr: int, batch: int, stream_ptr: int = 0) -> None:
+        rc = lib().occ_detect_host(self._h, d_ptr, m_ptr, batch, stream_ptr)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_detect_host")
+        self._last_batch = batch
+
+    def status(self) -> List[int]:
+        st = (ctypes.c_int32 * max(1, self._last_batch))()
+        rc = lib().occ_status(self._h, st)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_status")
+        return list(st)[: self._last_batch]
+
+    def frame_info(self, frame: int = 0):
+        lo, hi = ctypes.c_float(), ctypes.c_float()
+        hv = (ctypes.c_int32 * self.V)()
+        rc = lib().occ_frame_info(self._h, frame, ctypes.byref(lo), ctypes.byref(hi), hv)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_frame_info")
+        return lo.value, hi.value, list(hv)
+
+    @property
+    def last_launches(self) -> int:
+        return int(lib().occ_last_launches(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().occ_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

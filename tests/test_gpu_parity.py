@@ -1,0 +1,213 @@
+"""GPU parity: libocc's CUDA masks vs the CPU oracle, element by element.
+
+The bar is bit-exact (uint8 masks; north_star: "GPU masks must match the
+oracle bit-exactly on the same seeded inputs").  Covered: all five
+BASELINE.json configs (C5 in the bench's launch configuration: one call over
+all 256 frames, sampled frames vs the oracle, every frame vs its single-frame
+result), random tiny maps (integer, half-integer, noisy, uniform) with all
+24 baselines up to (+-2, +-2) plus longer ones, parameter variations, ragged
+and degenerate sizes, non-finite frames, the large-h fallback, both kernel
+paths, and the host-buffer entry point.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2408_14050_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (run with -m 'not gpu' on CPU)")
+    from paper_2408_14050_b200 import build
+    build.build()
+    return torch
+
+
+def run_gpu(torch, D, views, path="auto", max_batch=None, **kw):
+    from paper_2408_14050_b200.occ import Detector
+    D = np.ascontiguousarray(D, np.float32)
+    if D.ndim == 2:
+        D = D[None]
+    B, H, W = D.shape
+    det = Detector(H, W, views, max_batch=max_batch or B, path=path, **kw)
+    d = torch.from_numpy(D).cuda()
+    m = det.detect(d)
+    torch.cuda.synchronize()
+    st = det.status()
+    out = m.cpu().numpy()
+    det.close()
+    return out, st
+
+
+def assert_same(g, o, what=""):
+    if not (g == o).all():
+        diff = np.argwhere(g != o)
+        raise AssertionError(f"{what}: {len(diff)} mismatches, first {diff[:5].tolist()}, "
+                             f"gpu sum {int(g.sum())} oracle sum {int(o.sum())}")
+
+
+@pytest.mark.parametrize("path", ["auto", "direct"])
+def test_c1(torch_cuda, path):
+    D = scenes.make_scene(1)
+    g, st = run_gpu(torch_cuda, D, [(1, 0)], path=path)
+    o = oracle.detect(D, [(1, 0)])
+    assert_same(g[0], o, "C1")
+    assert int(g.sum()) == 112 and st == [0]
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_config_full_frame(torch_cuda, cfg):
+    D = scenes.make_scene(cfg)
+    views = scenes.config_views(cfg)
+    g, st = run_gpu(torch_cuda, D, views)
+    o = oracle.detect(D, views)
+    for i, b in enumerate(views):
+        assert_same(g[0, i], o[i], f"C{cfg} view {b}")
+
+
+def test_config4_full_frame(torch_cuda):
+    D = scenes.make_scene(4)
+    views = scenes.config_views(4)
+    g, st = run_gpu(torch_cuda, D, views)
+    o = oracle.detect(D, views)
+    for i, b in enumerate(views):
+        assert_same(g[0, i], o[i], f"C4 view {b}")
+
+
+def test_config5_batch(torch_cuda):
+    torch = torch_cuda
+    from paper_2408_14050_b200.occ import Detector
+    frames = 256
+    D = scenes.make_batch(5, frames)
+    views = scenes.config_views(5)
+    det = Detector(1080, 1920, views, max_batch=frames)
+    d = torch.from_numpy(D).cuda()
+    m = det.detect(d)                       # the bench's launch configuration
+    torch.cuda.synchronize()
+    assert det.status() == [0] * frames
+    for f in (0, 97, 255):                  # sampled frames vs the oracle
+        o = oracle.detect(D[f], views)
+        g = m[f].cpu().numpy()
+        for i, b in enumerate(views):
+            assert_same(g[i], o[i], f"C5 frame {f} view {b}")
+    # every frame of the batch equals its single-frame result (batch independence)
+    one = torch.empty((1, len(views), 1080, 1920), dtype=torch.uint8, device="cuda")
+    for f in range(frames):
+        det.detect(d[f:f + 1], out=one)
+        assert torch.equal(one[0], m[f]), f
+    det.close()
+
+
+MODES = ["int", "half", "noisy", "uniform"]
+SIZES = [(2, 2), (2, 9), (4, 4), (5, 7), (16, 16), (24, 17), (13, 31), (33, 65), (70, 3), (40, 130)]
+
+
+@pytest.mark.parametrize("H,W", SIZES)
+def test_random_tiny_maps(torch_cuda, H, W):
+    rng = scenes.SplitMix64(901, H, W)
+    views = scenes.all_small_baselines(2) + [(3, 1), (-1, 4), (5, -2), (8, 8), (0, -7)]
+    B = 24
+    D = np.stack([scenes.random_tiny_map(rng, H, W, MODES[i % 4]) for i in range(B)])
+    g, st = run_gpu(torch_cuda, D, views)
+    for f in range(B):
+        o = oracle.detect(D[f], views)
+        assert_same(g[f], o, f"frame {f} ({MODES[f % 4]}) {H}x{W}")
+
+
+@pytest.mark.parametrize("kw", [dict(t_edge=0.5), dict(t_dist=1.0), dict(t_dist=3.5, t_disp=0.25),
+                                dict(t_disp=0.0), dict(max_scan=7), dict(t_dist=1.7, t_disp=0.3),
+                                dict(t_dist=0.5, t_edge=2.0)])
+def test_params(torch_cuda, kw):
+    rng = scenes.SplitMix64(902, len(kw))
+    views = scenes.all_small_baselines(2)
+    D = np.stack([scenes.random_tiny_map(rng, 20, 28, MODES[i % 4]) for i in range(8)])
+    g, _ = run_gpu(torch_cuda, D, views, **kw)
+    for f in range(len(D)):
+        assert_same(g[f], oracle.detect(D[f], views, **kw), f"{kw} frame {f}")
+
+
+def test_noisy_c3_crop_with_params(torch_cuda):
+    D = scenes.make_scene(3)[300:560, 700:1100].copy()
+    views = scenes.VIEWS_3X3
+    for kw in ({}, dict(t_dist=1.0), dict(t_disp=0.25)):
+        g, _ = run_gpu(torch_cuda, D, views, **kw)
+        assert_same(g[0], oracle.detect(D, views, **kw), str(kw))
+
+
+def test_large_h_fallback(torch_cuda):
+    # range 0..300 -> h = 300 (s=1) / 600 (s=2): larger than any tile halo
+    rng = scenes.SplitMix64(903)
+    D = (scenes.random_tiny_map(rng, 48, 96, "int") * 30.0).astype(np.float32)
+    views = [(1, 0), (-2, 0), (0, 1), (1, -1), (2, 1)]
+    g, _ = run_gpu(torch_cuda, D, views)
+    assert_same(g[0], oracle.detect(D, views), "large h")
+
+
+def test_nonfinite_frames(torch_cuda):
+    D = scenes.make_batch(2, 3)
+    D[1, 10, 20] = np.nan
+    D[2, 0, 0] = np.inf
+    views = scenes.VIEWS_3X3
+    g, st = run_gpu(torch_cuda, D, views)
+    assert st == [0, -4, -4]
+    assert not g[1].any() and not g[2].any()
+    assert_same(g[0], oracle.detect(D[0], views), "finite frame")
+
+
+def test_views_subset_and_order(torch_cuda):
+    D = scenes.make_scene(2)
+    allv = scenes.VIEWS_3X3
+    g_all, _ = run_gpu(torch_cuda, D, allv)
+    sub = [allv[5], allv[0], allv[3]]
+    g_sub, _ = run_gpu(torch_cuda, D, sub)
+    for i, b in enumerate(sub):
+        assert (g_sub[0, i] == g_all[0, allv.index(b)]).all()
+
+
+def test_paths_agree(torch_cuda):
+    D = scenes.make_batch(3, 2)
+    views = scenes.VIEWS_3X3
+    a, _ = run_gpu(torch_cuda, D, views, path="auto")
+    b, _ = run_gpu(torch_cuda, D, views, path="direct")
+    assert (a == b).all()
+
+
+def test_host_entry_point(torch_cuda):
+    from paper_2408_14050_b200.occ import Detector
+    D = scenes.make_batch(2, 2)
+    views = scenes.VIEWS_3X3
+    det = Detector(480, 640, views, max_batch=2)
+    mh = det.detect_host(D)
+    dev, _ = run_gpu(torch_cuda, D, views)
+    assert (mh == dev).all()
+    det.close()
+
+
+def test_constant_and_planar(torch_cuda):
+    D = np.full((3, 50, 70), 4.0, np.float32)
+    D[1] = 2.5
+    D[2] = np.fromfunction(lambda y, x: 1.0 + 0.1 * x + 0.05 * y, (50, 70)).astype(np.float32)
+    g, _ = run_gpu(torch_cuda, D, scenes.all_small_baselines(2))
+    assert not g.any()
+
+
+def test_transpose_equivariance_gpu(torch_cuda):
+    D = scenes.make_scene(2)
+    views = scenes.VIEWS_3X3
+    a, _ = run_gpu(torch_cuda, D, views)
+    b, _ = run_gpu(torch_cuda, np.ascontiguousarray(D.T), [(by, bx) for bx, by in views])
+    assert (a[0] == b[0].transpose(0, 2, 1)).all()
+
+
+def test_deterministic_hash(torch_cuda):
+    D = scenes.make_scene(3)
+    a, _ = run_gpu(torch_cuda, D, scenes.VIEWS_3X3)
+    b, _ = run_gpu(torch_cuda, D, scenes.VIEWS_3X3)
+    assert hashlib.sha256(a.tobytes()).hexdigest() == hashlib.sha256(b.tobytes()).hexdigest()
