@@ -110,6 +110,16 @@ int occ_set_path(occ_ctx *ctx, int32_t path);
 /* Number of kernel launches the last occ_detect enqueued. */
 int32_t occ_last_launches(const occ_ctx *ctx);
 
+/* Kernel timing (benchmarks): while enabled, every kernel launch is
+ * bracketed by CUDA events recorded on its launch stream.  occ_profile
+ * enables/disables and resets the accumulators; occ_profile_read
+ * synchronises and returns, for one kernel kind, the summed device time in
+ * milliseconds and the number of launches since the last reset. */
+enum { OCC_KERNEL_INIT = 0, OCC_KERNEL_STATS = 1, OCC_KERNEL_TILE = 2, OCC_KERNEL_DIRECT = 3,
+       OCC_KERNEL_CAND = 4, OCC_KERNEL_KINDS = 5 };
+int occ_profile(occ_ctx *ctx, int32_t enable);
+int occ_profile_read(occ_ctx *ctx, int32_t kind, double *total_ms, int32_t *launches);
+
 /* Releases the context and its device scratch (synchronises first). */
 int occ_destroy(occ_ctx *ctx);
 

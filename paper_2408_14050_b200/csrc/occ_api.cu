@@ -32,6 +32,10 @@ struct occ_ctx {
     cudaStream_t last_stream = nullptr;
     int32_t last_batch = 0;
     int32_t last_launches = 0;
+    // kernel timing (occ_profile)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev[OCC_KERNEL_KINDS];   // start/end pairs
+    size_t ev_used[OCC_KERNEL_KINDS] = {0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -121,6 +125,30 @@ void near_far(ViewDesc &vd, const occ_params &p) {
 }
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return OCC_ERR_CUDA; } while (0)
+
+// Brackets one launch with events when profiling; returns a CUDA error.
+struct ProfScope {
+    occ_ctx *c; int kind; cudaStream_t s; bool on;
+    ProfScope(occ_ctx *c_, int kind_, cudaStream_t s_) : c(c_), kind(kind_), s(s_), on(c_->profiling) {
+        if (!on) return;
+        auto &v = c->ev[kind];
+        size_t &u = c->ev_used[kind];
+        while (v.size() < u + 2) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) { on = false; return; }
+            v.push_back(e);
+        }
+        cudaEventRecord(v[u], s);
+    }
+    void end() {
+        if (!on) return;
+        auto &v = c->ev[kind];
+        size_t &u = c->ev_used[kind];
+        cudaEventRecord(v[u + 1], s);
+        u += 2;
+        on = false;
+    }
+};
 
 int ensure_cand(occ_ctx *c, int32_t frames) {
     if (c->d_cand && c->cand_frames >= frames) return OCC_OK;
@@ -248,14 +276,26 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
     CK(cudaSetDevice(c->device));
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
-    CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
-    CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
+    {
+        ProfScope ps(c, OCC_KERNEL_INIT, s);
+        CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
+        ps.end();
+    }
+    {
+        ProfScope ps(c, OCC_KERNEL_STATS, s);
+        CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
+        ps.end();
+    }
     {
         int rc = ensure_cand(c, batch);
         if (rc != OCC_OK) return rc;
+        ProfScope pc(c, OCC_KERNEL_CAND, s);
         CK(launch_cand(D, c->H, c->W, batch, c->d_fams, c->nfam, c->params, c->d_cand, s)); ++launches;
+        pc.end();
+        ProfScope pd(c, OCC_KERNEL_DIRECT, s);
         CK(launch_direct(D, c->d_cand, c->H, c->W, batch, c->d_views, c->V, c->d_stats,
                          c->params, M, s)); ++launches;
+        pd.end();
     }
     c->last_stream = s;
     c->last_batch = batch;
@@ -316,6 +356,29 @@ int occ_frame_info(occ_ctx *c, int32_t frame, float *dmin, float *dmax, int32_t 
     return OCC_OK;
 }
 
+int occ_profile(occ_ctx *c, int32_t enable) {
+    if (!c) return OCC_ERR_INVALID_ARG;
+    c->profiling = enable != 0;
+    for (int k = 0; k < OCC_KERNEL_KINDS; ++k) c->ev_used[k] = 0;
+    return OCC_OK;
+}
+
+int occ_profile_read(occ_ctx *c, int32_t kind, double *total_ms, int32_t *launches) {
+    if (!c || kind < 0 || kind >= OCC_KERNEL_KINDS) return OCC_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    double tot = 0.0;
+    const size_t n = c->ev_used[kind];
+    for (size_t i = 0; i + 1 < n; i += 2) {
+        CK(cudaEventSynchronize(c->ev[kind][i + 1]));
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, c->ev[kind][i], c->ev[kind][i + 1]));
+        tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = (int32_t)(n / 2);
+    return OCC_OK;
+}
+
 int occ_destroy(occ_ctx *c) {
     if (!c) return OCC_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
@@ -326,6 +389,8 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_cand);
     cudaFree(c->d_stage_D);
     cudaFree(c->d_stage_M);
+    for (int k = 0; k < OCC_KERNEL_KINDS; ++k)
+        for (cudaEvent_t e : c->ev[k]) cudaEventDestroy(e);
     delete c;
     return OCC_OK;
 }

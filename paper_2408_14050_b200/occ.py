@@ -27,7 +27,8 @@ PATHS = {"auto": 0, "tiled": 1, "direct": 2}
 # every function include/occ.h declares (checked against the header by tests)
 EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", "occ_status",
            "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
-           "occ_version"]
+           "occ_version", "occ_profile", "occ_profile_read"]
+KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4}
 
 
 class occ_baseline(ctypes.Structure):
@@ -79,6 +80,10 @@ def lib() -> ctypes.CDLL:
         L.occ_destroy.restype = ctypes.c_int
         L.occ_strerror.argtypes = [ctypes.c_int]
         L.occ_strerror.restype = ctypes.c_char_p
+        L.occ_profile.argtypes = [vp, i32]
+        L.occ_profile.restype = ctypes.c_int
+        L.occ_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)]
+        L.occ_profile_read.restype = ctypes.c_int
         L.occ_version.argtypes = []
         L.occ_version.restype = i32
         _lib = L
@@ -199,6 +204,22 @@ class Detector:
         if rc != OCC_OK:
             raise OccError(rc, "occ_frame_info")
         return lo.value, hi.value, list(hv)
+
+    def profile(self, enable: bool) -> None:
+        rc = lib().occ_profile(self._h, 1 if enable else 0)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_profile")
+
+    def profile_read(self) -> dict:
+        """{kind: (total_ms, launches)} since the last occ_profile call (syncs)."""
+        out = {}
+        for name, k in KERNEL_KINDS.items():
+            ms, n = ctypes.c_double(), ctypes.c_int32()
+            rc = lib().occ_profile_read(self._h, k, ctypes.byref(ms), ctypes.byref(n))
+            if rc != OCC_OK:
+                raise OccError(rc, "occ_profile_read")
+            out[name] = (ms.value, n.value)
+        return out
 
     @property
     def last_launches(self) -> int:
