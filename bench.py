@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the occlusion-detection hot path on B200.
+
+Metric (BASELINE.json): occlusion-mask megapixel-views per second
+(frames x H x W x views / time / 1e6), per B200 and per box, plus the HBM
+roofline fraction of the dominant kernel.
+
+Workload (config.workload): BASELINE.json configs[4] "C5" -- 256 frames of
+1920x1080 fp32 disparity per GPU, 3x3 camera array (8 views), each frame a
+layered synthetic scene with N(0, 0.25^2) noise generated from seed + frame
+(paper_2408_14050_b200/scenes.py).  C5 is the config the metric's per-box
+scaling is quoted on; it fits one GPU (2.1 GB in + 4.2 GB out).  One step =
+one occ_detect call over the GPU's 256 frames (stats + all 8 views).  Weak
+scaling: every rank processes its own 256 frames (seed + rank * 256 + f);
+value = all ranks' pixel-views / max-over-ranks time.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+        torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import json
+import multiprocessing as mp
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "occlusion-mask megapixel-views/sec per B200 and per box; % of HBM roofline"
+CFG = 5
+H, W = 1080, 1920
+FRAMES_PER_GPU = 256
+
+
+def _gen(args):
+    cfg, seed, first, n = args
+    from paper_2408_14050_b200 import scenes
+    return scenes.make_batch(cfg, n, seed=seed, first_frame=first)
+
+
+def make_frames(n: int, first: int, workers: int = 0) -> np.ndarray:
+    """[n, H, W] fp32 C5 frames first..first+n-1 (parallel host generation)."""
+    workers = workers or min(32, os.cpu_count() or 1, n)
+    out = np.empty((n, H, W), np.float32)
+    chunk = max(1, (n + workers - 1) // workers)
+    jobs = [(CFG, 0, first + i, min(chunk, n - i)) for i in range(0, n, chunk)]
+    if workers <= 1:
+        for (c, s, f, k) in jobs:
+            out[f - first:f - first + k] = _gen((c, s, f, k))
+        return out
+    ctx = mp.get_context("fork")
+    with cf.ProcessPoolExecutor(max_workers=workers, mp_context=ctx) as ex:
+        for (c, s, f, k), arr in zip(jobs, ex.map(_gen, jobs)):
+            out[f - first:f - first + k] = arr
+    return out
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _sample(self):
+        mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples.append(mhz)
+        for bit, name in self.REASONS.items():
+            if r & bit and bit != 0x1:
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy_ test)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def cpu_oracle_sample(frames: np.ndarray, views, budget_s: float):
+    """Time the oracle (single thread) on whole frames until budget_s elapses."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    n = 0
+    for f in range(len(frames)):
+        oracle.detect(frames[f], views)
+        n += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    pv = n * H * W * len(views)
+    return pv / dt / 1e6, n, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (the tier's reference arm), rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2408_14050_b200 import scenes
+    views = scenes.config_views(CFG)
+    frames = make_frames(max(1, args.ref_frames), 0)
+    import oracle
+    oracle.build()
+    for i in range(args.warmup):
+        oracle.detect(frames[i % len(frames)], views)
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.detect(frames[i % len(frames)], views)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    pv = args.steps * H * W * len(views)
+    val = pv / tot / 1e6
+    sample = (f"1 C5 frame ({W}x{H}, 8 views) per step, frames 0..{len(frames) - 1} cycled; "
+              f"single-threaded C oracle (oracle/occ_oracle.c)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "MPV/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": workload_config(world),
+        "cpu_baseline": {"value": val, "unit": "MPV/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "MPV/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(world):
+    return {"workload": "C5: 256 frames/GPU of 1920x1080 fp32 layered synthetic disparity "
+                        "(50 shapes, disparities U[1,64], N(0,0.25^2) noise), 3x3 array, 8 views",
+            "frames_per_gpu": FRAMES_PER_GPU, "H": H, "W": W, "views": 8,
+            "params": {"t_edge": 1.0, "t_dist": 2.0, "t_disp": 0.5, "max_scan": 4096},
+            "l2": "no flush: each step reads 2.1 GB and writes 4.2 GB per GPU (>> 126 MB L2)",
+            "parallelism": f"frame-sharded x{world} (no data-path collective)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--frames", type=int, default=FRAMES_PER_GPU)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 3)")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle timing")
+    ap.add_argument("--ref-frames", type=int, default=2)
+    ap.add_argument("--path", default="auto", choices=["auto", "tiled", "direct"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    from paper_2408_14050_b200 import scenes
+    from paper_2408_14050_b200.occ import Detector
+    views = scenes.config_views(CFG)
+    V = len(views)
+    nf = args.frames
+    frames = make_frames(nf, rank * nf)
+    d = torch.from_numpy(frames).to(dev)
+    masks = torch.empty((nf, V, H, W), dtype=torch.uint8, device=dev)
+    det = Detector(H, W, views, max_batch=nf, path=args.path)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        det.detect(d, out=masks)
+    torch.cuda.synchronize()
+    st = det.status()
+    assert all(s == 0 for s in st), st
+
+    # ---------------- timed region: K steps, inputs resident in HBM ----------------
+    det.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            det.detect(d, out=masks)
+            launches += det.last_launches
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    kt = det.profile_read()
+    det.profile(False)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    pv_step = world * nf * H * W * V
+    value = pv_step / (ms_step / 1e3) / 1e6
+
+    # dominant kernel: the largest summed device time inside the timed region
+    dom_name, (dom_ms, dom_n) = max(kt.items(), key=lambda kv: kv[1][0])
+    per_launch_ms = dom_ms / max(1, dom_n)
+    alg_bytes = nf * H * W * (4 + V)           # 4 B read + V B written per pixel
+    peak, peak_src = load_peaks()
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    tr = load_traffic()
+    traffic = None
+    if tr and tr.get("kernel") == dom_name and tr.get("frames") == nf:
+        traffic = tr.get("bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
+                "kernel_ms_per_launch": per_launch_ms, "kernel_share_of_step": dom_ms / ms if ms else None,
+                "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                "kernels_ms": {k: v[0] / args.steps for k, v in kt.items() if v[1]}}
+
+    # ---------------- end to end: host buffers through the C ABI ----------------
+    e2e_steps = args.e2e_steps or min(args.steps, 3)
+    hbuf = torch.from_numpy(frames).pin_memory()
+    mbuf = torch.empty((nf, V, H, W), dtype=torch.uint8).pin_memory()
+    det.detect_host_ptr(hbuf.data_ptr(), mbuf.data_ptr(), nf, stream.cuda_stream)   # warm staging
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        det.detect_host_ptr(hbuf.data_ptr(), mbuf.data_ptr(), nf, stream.cuda_stream)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": pv_step / e2e_s / 1e6, "unit": "MPV/s", "h2d_bytes_per_step": int(frames.nbytes),
+           "d2h_bytes_per_step": int(nf * V * H * W), "ms_per_step": e2e_s * 1e3,
+           "note": "occ_detect_host: pinned H2D of D, detect, D2H of all masks, stream sync"}
+    assert torch.equal(mbuf[:1].to(dev), masks[:1])
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        val, n, dt = cpu_oracle_sample(frames, views, args.cpu_budget)
+        cpu = {"value": val, "unit": "MPV/s", "cores": 1, "kind": "oracle",
+               "sample": f"{n} whole C5 frame(s) x 8 views in {dt:.1f} s, single-threaded C oracle"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "MPV/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+        "gpu_launches": launches, "path": args.path,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
