@@ -1,0 +1,397 @@
+// k_tile.cu -- K1, the tiled sweep kernel: Eqs. 1-6 for one line family.
+//
+// One CTA = one (tile, frame): 32 consecutive digital epipolar lines of one
+// family x up to 256 output positions along them, for a
+// group of <= 2 views of that family.  Layout "lane = line": every thread of
+// a warp owns one line, a warp owns 32 consecutive positions, so all shared
+// memory accesses of the compute phase are conflict-free and the per-line
+// work is a sequential sweep (the cheapest possible scan).
+//
+//  1. stage   D along the 32 lines into smem [pos][lane] with a halo of
+//             HALO >= max(h, reach) positions per side (coalesced row runs),
+//             candidate bits (Eqs. 1-2) per line as 32-bit words.
+//  2. per view:
+//     a. dcov(p) = U(p) - u_p, U(p) = pc(u_p + h) + h: a pair (p, q) shares
+//        one candidate's scan window (Eq. 4) iff u_q - u_p <= dcov(p).
+//     b. near pairs (|dk| <= jstar-1): exact fp32 interval tests of
+//        delta = fl(v_q - v_p) (host-precomputed thresholds, S7).
+//     c. far pairs (dk <= -jstar, delta > t_disp implied): conservative
+//        suffix-max filter on B = s v - u along the sweep; survivors are
+//        resolved exactly (binary64 predicate), first at the offset that
+//        resolved the previous survivor of the line, else by a bounded scan.
+//  3. store   mask bytes through smem, row-contiguous streaming stores.
+// Views whose halo does not fit (huge disparity ranges) are computed by the
+// exact per-pixel routine (direct_pixel) inside the same CTA.
+#include "occ_device.cuh"
+
+namespace occ {
+
+namespace {
+constexpr int TP = kTilePositions;     // output positions per tile
+constexpr int NT = 256;                // threads (8 warps)
+constexpr int HMAX = kTileHaloMax;     // max staged halo per side
+constexpr int NPMAX = TP + 2 * HMAX;   // staged positions
+constexpr int NB = NPMAX / 32;         // 32-position blocks
+constexpr int VPITCH = 33;             // floats per staged position (32 lanes + pad)
+constexpr int OPITCH = 36;             // bytes per output position (32 lanes + pad)
+constexpr int DC = TP + 2 * kMaxNear;  // dcov entries (outputs +- near reach)
+constexpr int16_t NONE_LO = -30000, NONE_HI = 30000;
+
+constexpr size_t OFF_V = 0;
+constexpr size_t OFF_CW = OFF_V + sizeof(float) * NPMAX * VPITCH;
+constexpr size_t OFF_LAST = OFF_CW + sizeof(uint32_t) * 2 * NB * 32;
+constexpr size_t OFF_NEXT = OFF_LAST + sizeof(int16_t) * 2 * NB * 32;
+constexpr size_t OFF_DCOV = OFF_NEXT + sizeof(int16_t) * 2 * NB * 32;
+constexpr size_t OFF_AGG = OFF_DCOV + sizeof(int16_t) * DC * 32;
+constexpr size_t OFF_OUT = OFF_AGG + sizeof(float) * 2 * NB * 32;
+constexpr size_t SMEM = OFF_OUT + (size_t)kGroupViews * TP * OPITCH;
+}  // namespace
+
+size_t tile_smem_bytes() { return SMEM; }
+
+// floor(a / den) for den > 0, shifts for the common powers of two
+__device__ __forceinline__ int32_t fdiv(int32_t a, int32_t den) {
+    if (den == 1) return a;
+    if (den == 2) return a >> 1;
+    if (den == 4) return a >> 2;
+    if (den == 8) return a >> 3;
+    return floordiv(a, den);
+}
+__device__ __forceinline__ int32_t cdiv(int32_t a, int32_t den) { return -fdiv(-a, den); }
+
+// x-range of image row y covered by lanes [0, 32) of an x-major tile:
+// l = y - l0 - floor(x num / den) in [0, 31].
+__device__ __forceinline__ void row_run(int32_t y, int32_t l0, int32_t num, int32_t den,
+                                        int32_t lo, int32_t hi, int32_t &xa, int32_t &xb) {
+    const int32_t A = y - l0 - 31, B = y - l0;
+    if (num == 0) {
+        if (B < 0 || B > 31) { xa = 1; xb = 0; return; }
+        xa = lo; xb = hi;
+    } else if (num > 0) {
+        xa = cdiv(A * den, num);
+        xb = cdiv((B + 1) * den, num) - 1;
+    } else {
+        const int32_t n = -num;
+        xa = floordiv(-(B + 1) * den, n) + 1;
+        xb = floordiv(-A * den, n);
+    }
+    xa = max(xa, lo);
+    xb = min(xb, hi);
+}
+
+struct ViewRegs {
+    int32_t s, sg, h, jstar, nback, nfwd, vid;
+    float T;              // far-filter margin t_dist + eps
+    bool staged;
+};
+
+__global__ void __launch_bounds__(NT, 2)
+k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__restrict__ tiles,
+       const GroupDesc *__restrict__ groups, const ViewDesc *__restrict__ views, int32_t nviews,
+       const FamilyDesc *__restrict__ fams, const FrameStats *__restrict__ st, Params p,
+       uint8_t *__restrict__ masks) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sv = reinterpret_cast<float *>(smem + OFF_V);
+    uint32_t *scw = reinterpret_cast<uint32_t *>(smem + OFF_CW);
+    int16_t *slast = reinterpret_cast<int16_t *>(smem + OFF_LAST);
+    int16_t *snext = reinterpret_cast<int16_t *>(smem + OFF_NEXT);
+    int16_t *sdcov = reinterpret_cast<int16_t *>(smem + OFF_DCOV);
+    float *sagg = reinterpret_cast<float *>(smem + OFF_AGG);
+    uint8_t *sout = smem + OFF_OUT;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const TileDesc td = tiles[blockIdx.x];
+    const int f = blockIdx.y;
+    const GroupDesc gd = groups[td.group];
+    const FamilyDesc fd = fams[gd.fam];
+    const FrameStats fs = st[f];
+    const int64_t HW = (int64_t)H * W;
+    const float *Df = D + (int64_t)f * HW;
+    const int32_t l0 = td.l0, P0 = td.p0, P1 = td.p1, TPe = P1 - P0;
+    const int32_t num = fd.num, den = fd.den;
+    const bool xm = fd.xmajor != 0;
+
+    // ------------------------------------------------ per-view parameters
+    const float R = frame_range(fs);
+    const float M = fmaxf(fabsf(key_float(fs.minkey)), fabsf(key_float(fs.maxkey)));
+    ViewRegs vr[kGroupViews];
+    int32_t halo = 0;
+    bool any_staged = false;
+#pragma unroll
+    for (int g = 0; g < kGroupViews; ++g) {
+        vr[g].staged = false;
+        if (g >= gd.nv) continue;
+        const ViewDesc &vd = views[gd.view[g]];
+        vr[g].vid = gd.view[g];
+        vr[g].s = vd.s; vr[g].sg = vd.sg; vr[g].jstar = vd.jstar;
+        vr[g].nback = vd.nback; vr[g].nfwd = vd.nfwd;
+        vr[g].h = view_h(R, vd.s, p.max_scan);
+        // reach: a valid partner has |dk| < t_dist + s R (delta <= R) and <= 2h
+        const int32_t jr = (int32_t)floor(__dadd_rn((double)p.t_dist,
+                                                    __dmul_rn((double)vd.s, (double)R))) + 1;
+        // staged halo: far partners (min(2h, reach)), candidates within h of a
+        // forward neighbour (h + nfwd), near partners (nback)
+        int32_t need = max(vr[g].h + vd.nfwd, min(2 * vr[g].h, jr));
+        need = max(need, vd.nback);
+        // filter margin: bounds the fp32 rounding of B = s v - u (|u| < 2^12)
+        const double eps = ldexp(1.0, -19) * ((double)vd.s * (double)M + 4096.0 + (double)p.t_dist);
+        vr[g].T = __double2float_ru(__dadd_rn((double)p.t_dist, eps));
+        vr[g].staged = !fs.nonfinite && need <= HMAX && vd.nback <= kMaxNear &&
+                       vd.nfwd <= kMaxNear && vd.jstar <= 32;
+        if (vr[g].staged) { halo = max(halo, need); any_staged = true; }
+    }
+    const int32_t HALO32 = (halo + 31) & ~31;
+    const int32_t L0 = HALO32;                     // local index of P0
+    const int32_t base = P0 - HALO32;              // position of local index 0
+    const int32_t NP32 = ((TPe + 31) & ~31) + 2 * HALO32;
+    const int32_t NB32 = NP32 >> 5;
+
+    if (any_staged) {
+        // ------------------------------------------------ 1. stage
+        for (int k = tid; k < NP32 * 32; k += NT) sv[(k >> 5) * VPITCH + (k & 31)] = __int_as_float(0x7fc00000);
+        for (int k = tid; k < 2 * NB * 32; k += NT) scw[k] = 0u;
+        __syncthreads();
+        if (!xm) {
+            // y-major: pos = y, lane -> x = l0 + lane + floor(y num / den): rows are positions
+            for (int i = warp; i < NP32; i += NT / 32) {
+                const int32_t y = base + i;
+                if (y < 0 || y >= H) continue;
+                const int32_t x = l0 + lane + fdiv(y * num, den);
+                if (x < 0 || x >= W) continue;
+                sv[i * VPITCH + lane] = __ldg(Df + (int64_t)y * W + x);
+                const uint32_t c = cand_dirs<false>(Df, H, W, x, y, fd.b0x, fd.b0y, p.e2_thresh, p.t_edge);
+                if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
+                if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
+            }
+        } else {
+            // x-major: pos = x, lane = y - l0 - floor(x num / den); walk image rows
+            const int32_t xs = max(base, 0), xe = min(base + NP32, W) - 1;
+            if (xs <= xe) {
+                const int32_t fa = fdiv(xs * num, den), fb = fdiv(xe * num, den);
+                const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
+                for (int32_t y = ylo + warp; y <= yhi; y += NT / 32) {
+                    int32_t xa, xb;
+                    row_run(y, l0, num, den, xs, xe, xa, xb);
+                    for (int32_t x = xa + lane; x <= xb; x += 32) {
+                        const int32_t l = y - l0 - fdiv(x * num, den);
+                        const int32_t i = x - base;
+                        sv[i * VPITCH + l] = __ldg(Df + (int64_t)y * W + x);
+                        const uint32_t c = cand_dirs<false>(Df, H, W, x, y, fd.b0x, fd.b0y, p.e2_thresh, p.t_edge);
+                        if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
+                        if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // candidate prefix/suffix summaries per word (for O(1) prev/next candidate)
+        if (tid < 64) {
+            const int d = tid >> 5;
+            int16_t last = NONE_LO;
+            for (int w = 0; w < NB32; ++w) {
+                const uint32_t m = scw[(d * NB + w) * 32 + lane];
+                if (m) last = (int16_t)(32 * w + 31 - __clz(m));
+                slast[(d * NB + w) * 32 + lane] = last;
+            }
+            int16_t nxt = NONE_HI;
+            for (int w = NB32 - 1; w >= 0; --w) {
+                const uint32_t m = scw[(d * NB + w) * 32 + lane];
+                if (m) nxt = (int16_t)(32 * w + __ffs(m) - 1);
+                snext[(d * NB + w) * 32 + lane] = nxt;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ------------------------------------------------ 2. per view
+#pragma unroll 1
+    for (int g = 0; g < gd.nv; ++g) {
+        const ViewRegs cv = g == 0 ? vr[0] : vr[kGroupViews - 1];   // static register selection
+        uint8_t *so = sout + (size_t)g * TP * OPITCH;
+        if (fs.nonfinite) {            // reject the frame, masks all zero
+            for (int k = tid; k < TP * 32; k += NT) so[(k >> 5) * OPITCH + (k & 31)] = 0;
+            continue;
+        }
+        if (!cv.staged) {           // halo too large: exact per-pixel routine
+            const ViewDesc vd = views[cv.vid];
+            for (int k = tid; k < TPe * 32; k += NT) {
+                const int32_t pos = P0 + (k >> 5), l = k & 31, ln = l0 + l;
+                int32_t x, y;
+                if (xm) { x = pos; y = ln + fdiv(pos * num, den); }
+                else { y = pos; x = ln + fdiv(pos * num, den); }
+                bool m = false;
+                if (x >= 0 && x < W && y >= 0 && y < H)
+                    m = direct_pixel<false>(Df, H, W, vd, fd, p, cv.h, x, y);
+                so[(k >> 5) * OPITCH + l] = (uint8_t)m;
+            }
+            continue;
+        }
+        const int32_t s = cv.s, sg = cv.sg, h = cv.h, jstar = cv.jstar;
+        const int d = sg > 0 ? 0 : 1;
+        const float fs_ = (float)s;
+        const float T = cv.T;
+        // exact fp32 interval bounds of the near offsets (host-precomputed, S7)
+        float blo[kMaxNear], bhi[kMaxNear], flo[kMaxNear], fhi[kMaxNear];
+        {
+            const ViewDesc &vd = views[cv.vid];
+#pragma unroll
+            for (int j = 0; j < kMaxNear; ++j) {
+                blo[j] = vd.back_lo[j]; bhi[j] = vd.back_hi[j];
+                flo[j] = vd.fwd_lo[j]; fhi[j] = vd.fwd_hi[j];
+            }
+        }
+        // a. dcov for local positions [L0 - kMaxNear, L0 + TPe + kMaxNear)
+        const int32_t D0 = L0 - kMaxNear;
+        for (int k = warp; k < TPe + 2 * kMaxNear; k += NT / 32) {
+            const int32_t i = D0 + k;
+            int32_t dc = -1;
+            if (i >= 0 && i < NP32) {
+                if (sg > 0) {
+                    const int32_t xq = min(i + h, NP32 - 1);
+                    const int32_t w = xq >> 5;
+                    const uint32_t m = scw[(d * NB + w) * 32 + lane] & (0xffffffffu >> (31 - (xq & 31)));
+                    const int32_t pc = m ? 32 * w + 31 - __clz(m)
+                                         : (w > 0 ? slast[(d * NB + w - 1) * 32 + lane] : NONE_LO);
+                    if (pc != NONE_LO && pc >= i - h) dc = pc + h - i;
+                } else {
+                    const int32_t xq = max(i - h, 0);
+                    const int32_t w = xq >> 5;
+                    const uint32_t m = scw[(d * NB + w) * 32 + lane] & (0xffffffffu << (xq & 31));
+                    const int32_t nc = m ? 32 * w + __ffs(m) - 1
+                                         : (w + 1 < NB32 ? snext[(d * NB + w + 1) * 32 + lane] : NONE_HI);
+                    if (nc != NONE_HI && nc <= i + h) dc = i + h - nc;
+                }
+            }
+            sdcov[k * 32 + lane] = (int16_t)dc;
+        }
+        // b. block aggregates of B = s v - u for the far filter (u = sg (i - L0))
+        for (int b = warp; b < NB32; b += NT / 32) {
+            float A = -INFINITY, Ap = -INFINITY;
+            for (int r = 0; r < 32; ++r) {
+                const int32_t i = 32 * b + r;
+                const float Bv = __fsub_rn(__fmul_rn(fs_, sv[i * VPITCH + lane]), (float)(sg * (i - L0)));
+                A = fmaxf(A, Bv);
+                const bool excl = sg > 0 ? (r < jstar - 1) : (r > 32 - jstar);
+                if (!excl) Ap = fmaxf(Ap, Bv);
+            }
+            sagg[(0 * NB + b) * 32 + lane] = A;
+            sagg[(1 * NB + b) * 32 + lane] = Ap;
+        }
+        __syncthreads();
+        // c. sweep: warp w owns output block L0/32 + w, moving toward lower u
+        const int32_t nob = (TPe + 31) >> 5;
+        for (int ob = warp; ob < nob; ob += NT / 32) {
+            const int32_t b = (L0 >> 5) + ob;
+            float SX = -INFINITY;
+            if (sg > 0) {
+                if (b + 1 < NB32) SX = sagg[(1 * NB + b + 1) * 32 + lane];
+                for (int bb = b + 2; bb < NB32; ++bb) SX = fmaxf(SX, sagg[(0 * NB + bb) * 32 + lane]);
+            } else {
+                if (b - 1 >= 0) SX = sagg[(1 * NB + b - 1) * 32 + lane];
+                for (int bb = 0; bb <= b - 2; ++bb) SX = fmaxf(SX, sagg[(0 * NB + bb) * 32 + lane]);
+            }
+            int32_t jl = 0;
+            for (int r = 0; r < 32; ++r) {
+                const int32_t i = sg > 0 ? 32 * b + 31 - r : 32 * b + r;
+                {   // fold position i + sg*jstar into the suffix max
+                    const int32_t qf = i + sg * jstar;
+                    if (qf >= 0 && qf < NP32)
+                        SX = fmaxf(SX, __fsub_rn(__fmul_rn(fs_, sv[qf * VPITCH + lane]),
+                                                 (float)(sg * (qf - L0))));
+                }
+                const int32_t k = i - L0;          // output index
+                if (k < 0 || k >= TPe) continue;
+                const float vp = sv[i * VPITCH + lane];
+                bool m = false;
+                if (!isnan(vp)) {
+                    const int32_t dc = sdcov[(i - D0) * 32 + lane];
+#pragma unroll
+                    for (int j = 1; j <= kMaxNear; ++j) {
+                        if (j > cv.nback) break;
+                        const int32_t q = i + sg * j;
+                        const float vq = (q >= 0 && q < NP32) ? sv[q * VPITCH + lane] : __int_as_float(0x7fc00000);
+                        const float dl = __fsub_rn(vq, vp);
+                        m |= (dl > blo[j - 1]) & (dl < bhi[j - 1]) & (j <= dc);
+                    }
+#pragma unroll
+                    for (int fo = 1; fo <= kMaxNear; ++fo) {
+                        if (fo > cv.nfwd) break;
+                        const int32_t q = i - sg * fo;
+                        const float vq = (q >= 0 && q < NP32) ? sv[q * VPITCH + lane] : __int_as_float(0x7fc00000);
+                        const float dl = __fsub_rn(vq, vp);
+                        const int32_t dq = sdcov[(q - D0) * 32 + lane];
+                        m |= (dl > flo[fo - 1]) & (dl < fhi[fo - 1]) & (dq >= fo);
+                    }
+                    if (!m) {
+                        const float Bp = __fsub_rn(__fmul_rn(fs_, vp), (float)(sg * (i - L0)));
+                        if (SX > __fsub_rn(Bp, T)) {
+                            // exact resolution over backward offsets j in [jstar, jmax]
+                            const int32_t lim = sg > 0 ? NP32 - 1 - i : i;
+                            const int32_t jmax = min(min(dc, 2 * h), lim);
+                            if (jmax >= jstar) {
+                                if (jl >= jstar) {
+#pragma unroll
+                                    for (int dj = 0; dj < 3 && !m; ++dj) {
+                                        const int32_t j = jl + (dj == 0 ? 0 : (dj == 1 ? -1 : 1));
+                                        if (j < jstar || j > jmax) continue;
+                                        if (pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s,
+                                                       p.t_dist, p.t_disp)) { m = true; jl = j; }
+                                    }
+                                }
+                                for (int32_t j = jstar; j <= jmax && !m; ++j) {
+                                    if (pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s,
+                                                   p.t_dist, p.t_disp)) { m = true; jl = j; }
+                                }
+                            }
+                        }
+                    }
+                }
+                so[k * OPITCH + lane] = (uint8_t)m;
+            }
+        }
+        __syncthreads();    // sdcov / sagg reused by the next view
+    }
+    __syncthreads();
+
+    // ------------------------------------------------ 3. store (row-contiguous)
+#pragma unroll 1
+    for (int g = 0; g < gd.nv; ++g) {
+        const uint8_t *so = sout + (size_t)g * TP * OPITCH;
+        uint8_t *Mv = masks + ((int64_t)f * nviews + gd.view[g]) * HW;
+        if (!xm) {
+            for (int k = warp; k < TPe; k += NT / 32) {
+                const int32_t y = P0 + k;
+                if (y < 0 || y >= H) continue;
+                const int32_t x = l0 + lane + fdiv(y * num, den);
+                if (x < 0 || x >= W) continue;
+                __stcs(Mv + (int64_t)y * W + x, so[k * OPITCH + lane]);
+            }
+        } else {
+            const int32_t xs = max(P0, 0), xe = min(P1, W) - 1;
+            if (xs > xe) continue;
+            const int32_t fa = fdiv(xs * num, den), fb = fdiv(xe * num, den);
+            const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
+            for (int32_t y = ylo + warp; y <= yhi; y += NT / 32) {
+                int32_t xa, xb;
+                row_run(y, l0, num, den, xs, xe, xa, xb);
+                for (int32_t x = xa + lane; x <= xb; x += 32) {
+                    const int32_t l = y - l0 - fdiv(x * num, den);
+                    __stcs(Mv + (int64_t)y * W + x, so[(x - P0) * OPITCH + l]);
+                }
+            }
+        }
+    }
+}
+
+cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
+                        const TileDesc *tiles, int32_t ntiles, const GroupDesc *groups,
+                        const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
+                        const FrameStats *st, const Params &p, uint8_t *masks, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)ntiles, (unsigned)batch);
+    k_tile<<<grid, NT, SMEM, s>>>(D, H, W, tiles, groups, views, nviews, fams, st, p, masks);
+    return cudaGetLastError();
+}
+
+}  // namespace occ

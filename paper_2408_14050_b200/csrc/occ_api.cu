@@ -25,8 +25,10 @@ struct occ_ctx {
     ViewDesc *d_views = nullptr;
     FamilyDesc *d_fams = nullptr;
     FrameStats *d_stats = nullptr;
-    uint32_t *d_cand = nullptr;          // direct path scratch (lazy)
-    int64_t cand_frames = 0;
+    std::vector<GroupDesc> groups;
+    std::vector<TileDesc> tiles;
+    GroupDesc *d_groups = nullptr;
+    TileDesc *d_tiles = nullptr;
     float *d_stage_D = nullptr;          // occ_detect_host staging (lazy)
     uint8_t *d_stage_M = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -150,13 +152,49 @@ struct ProfScope {
     }
 };
 
-int ensure_cand(occ_ctx *c, int32_t frames) {
-    if (c->d_cand && c->cand_frames >= frames) return OCC_OK;
-    if (c->d_cand) { cudaFree(c->d_cand); c->d_cand = nullptr; }
-    size_t bytes = (size_t)frames * c->H * c->W * sizeof(uint32_t);
-    if (cudaMalloc(&c->d_cand, bytes) != cudaSuccess) { cudaGetLastError(); return OCC_ERR_OOM; }
-    c->cand_frames = frames;
-    return OCC_OK;
+// View groups (<= 2 views of one family, +-b pairs of equal s first) and the
+// static tile list: for every group, blocks of 32 consecutive lines and
+// segments of kTilePositions positions covering the lines' in-image extent.
+// Pure integer geometry of the digital lines (S6); independent of the data.
+void build_tiles(occ_ctx *c) {
+    for (int32_t fam = 0; fam < c->nfam; ++fam) {
+        const FamilyDesc &fd = c->fams[fam];
+        std::vector<int32_t> vs(fd.view, fd.view + fd.nviews);
+        std::stable_sort(vs.begin(), vs.end(), [&](int32_t a, int32_t b) {
+            if (c->views[a].s != c->views[b].s) return c->views[a].s < c->views[b].s;
+            return c->views[a].sg > c->views[b].sg;
+        });
+        for (size_t k = 0; k < vs.size(); k += kGroupViews) {
+            GroupDesc g{};
+            g.fam = fam;
+            g.nv = 0;
+            for (size_t j = k; j < vs.size() && j < k + kGroupViews; ++j) g.view[g.nv++] = vs[j];
+            c->groups.push_back(g);
+        }
+    }
+    const int32_t H = c->H, W = c->W;
+    for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi) {
+        const FamilyDesc &fd = c->fams[c->groups[gi].fam];
+        const int32_t num = fd.num, den = fd.den;
+        const int32_t PM = fd.xmajor ? W : H;      // positions
+        const int32_t QM = fd.xmajor ? H : W;      // the other axis
+        auto fdv = [&](int32_t a) { return floordiv(a * num, den); };
+        const int32_t f0 = fdv(0), f1 = fdv(PM - 1);
+        const int32_t lmin = 0 - std::max(f0, f1), lmax = QM - 1 - std::min(f0, f1);
+        for (int32_t l0 = lmin; l0 <= lmax; l0 += 32) {
+            int32_t plo = INT32_MAX, phi = -1;
+            for (int32_t pos = 0; pos < PM; ++pos) {
+                const int32_t q0 = l0 + fdv(pos);
+                if (q0 <= QM - 1 && q0 + 31 >= 0) { plo = std::min(plo, pos); phi = pos; }
+            }
+            if (phi < 0) continue;
+            for (int32_t p0 = plo; p0 <= phi; p0 += kTilePositions) {
+                TileDesc t{};
+                t.group = gi; t.l0 = l0; t.p0 = p0; t.p1 = std::min(p0 + kTilePositions, phi + 1);
+                c->tiles.push_back(t);
+            }
+        }
+    }
 }
 
 }  // namespace
@@ -237,10 +275,13 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
         c->views.push_back(vd);
     }
     c->nfam = (int32_t)c->fams.size();
+    build_tiles(c);
 
     if (cudaGetDevice(&c->device) != cudaSuccess) { cudaGetLastError(); delete c; return OCC_ERR_CUDA; }
     if (cudaMalloc(&c->d_views, sizeof(ViewDesc) * c->views.size()) != cudaSuccess ||
         cudaMalloc(&c->d_fams, sizeof(FamilyDesc) * c->fams.size()) != cudaSuccess ||
+        cudaMalloc(&c->d_groups, sizeof(GroupDesc) * c->groups.size()) != cudaSuccess ||
+        cudaMalloc(&c->d_tiles, sizeof(TileDesc) * c->tiles.size()) != cudaSuccess ||
         cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess) {
         cudaGetLastError();
         occ_destroy(c);
@@ -249,6 +290,10 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
     if (cudaMemcpy(c->d_views, c->views.data(), sizeof(ViewDesc) * c->views.size(),
                    cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(c->d_fams, c->fams.data(), sizeof(FamilyDesc) * c->fams.size(),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_groups, c->groups.data(), sizeof(GroupDesc) * c->groups.size(),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_tiles, c->tiles.data(), sizeof(TileDesc) * c->tiles.size(),
                    cudaMemcpyHostToDevice) != cudaSuccess) {
         occ_destroy(c);
         return OCC_ERR_CUDA;
@@ -286,16 +331,16 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
         CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
         ps.end();
     }
-    {
-        int rc = ensure_cand(c, batch);
-        if (rc != OCC_OK) return rc;
-        ProfScope pc(c, OCC_KERNEL_CAND, s);
-        CK(launch_cand(D, c->H, c->W, batch, c->d_fams, c->nfam, c->params, c->d_cand, s)); ++launches;
-        pc.end();
+    if (c->path == OCC_PATH_DIRECT) {
         ProfScope pd(c, OCC_KERNEL_DIRECT, s);
-        CK(launch_direct(D, c->d_cand, c->H, c->W, batch, c->d_views, c->V, c->d_stats,
+        CK(launch_direct(D, c->H, c->W, batch, c->d_views, c->V, c->d_fams, c->d_stats,
                          c->params, M, s)); ++launches;
         pd.end();
+    } else {
+        ProfScope pt(c, OCC_KERNEL_TILE, s);
+        CK(launch_tile(D, c->H, c->W, batch, c->d_tiles, (int32_t)c->tiles.size(), c->d_groups,
+                       c->d_views, c->V, c->d_fams, c->d_stats, c->params, M, s)); ++launches;
+        pt.end();
     }
     c->last_stream = s;
     c->last_batch = batch;
@@ -386,7 +431,8 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_views);
     cudaFree(c->d_fams);
     cudaFree(c->d_stats);
-    cudaFree(c->d_cand);
+    cudaFree(c->d_groups);
+    cudaFree(c->d_tiles);
     cudaFree(c->d_stage_D);
     cudaFree(c->d_stage_M);
     for (int k = 0; k < OCC_KERNEL_KINDS; ++k)

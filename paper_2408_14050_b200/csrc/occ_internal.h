@@ -40,6 +40,17 @@ struct FamilyDesc {
     int32_t view[kMaxViews];   // indices into ViewDesc[]
 };
 
+// Tiled kernel work decomposition (k_tile.cu): a group is <= 2 views of one
+// family sharing staged data; a tile is 32 consecutive lines x TP positions.
+constexpr int kGroupViews = 2;
+struct GroupDesc {
+    int32_t fam, nv;
+    int32_t view[kGroupViews];
+};
+struct TileDesc {
+    int32_t group, l0, p0, p1;   // lines [l0, l0+32), output positions [p0, p1)
+};
+
 struct Params {
     float t_edge, t_dist, t_disp;
     int32_t max_scan;
@@ -80,12 +91,15 @@ __host__ __device__ inline int32_t floordiv(int32_t a, int32_t d) {   // d > 0
 // Launchers (k_*.cu)
 cudaError_t launch_stats_init(FrameStats *st, int32_t batch, cudaStream_t s);
 cudaError_t launch_stats(const float *D, int64_t HW, int32_t batch, FrameStats *st, cudaStream_t s);
-cudaError_t launch_cand(const float *D, int32_t H, int32_t W, int32_t batch,
-                        const FamilyDesc *fams, int32_t nfam, const Params &p,
-                        uint32_t *cand, cudaStream_t s);
-cudaError_t launch_direct(const float *D, const uint32_t *cand, int32_t H, int32_t W,
-                          int32_t batch, const ViewDesc *views, int32_t nviews,
-                          const FrameStats *st, const Params &p, uint8_t *masks,
-                          cudaStream_t s);
+cudaError_t launch_direct(const float *D, int32_t H, int32_t W, int32_t batch,
+                          const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
+                          const FrameStats *st, const Params &p, uint8_t *masks, cudaStream_t s);
+size_t tile_smem_bytes();
+constexpr int kTilePositions = 256;    // TP
+constexpr int kTileHaloMax = 96;       // staged halo per side (multiple of 32)
+cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
+                        const TileDesc *tiles, int32_t ntiles, const GroupDesc *groups,
+                        const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
+                        const FrameStats *st, const Params &p, uint8_t *masks, cudaStream_t s);
 
 }  // namespace occ
