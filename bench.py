@@ -191,10 +191,10 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(world):
-    return {"workload": "C5: 256 frames/GPU of 1920x1080 fp32 layered synthetic disparity "
+def workload_config(world, nf=FRAMES_PER_GPU):
+    return {"workload": f"C5: {nf} frames/GPU of 1920x1080 fp32 layered synthetic disparity "
                         "(50 shapes, disparities U[1,64], N(0,0.25^2) noise), 3x3 array, 8 views",
-            "frames_per_gpu": FRAMES_PER_GPU, "H": H, "W": W, "views": 8,
+            "frames_per_gpu": nf, "H": H, "W": W, "views": 8,
             "params": {"t_edge": 1.0, "t_dist": 2.0, "t_disp": 0.5, "max_scan": 4096},
             "l2": "no flush: each step reads 2.1 GB and writes 4.2 GB per GPU (>> 126 MB L2)",
             "parallelism": f"frame-sharded x{world} (no data-path collective)"}
@@ -321,7 +321,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "MPV/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world),
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world, nf),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
         "gpu_launches": launches, "path": args.path,
     }

@@ -72,15 +72,118 @@ __device__ __forceinline__ void row_run(int32_t y, int32_t l0, int32_t num, int3
         xb = cdiv((B + 1) * den, num) - 1;
     } else {
         const int32_t n = -num;
-        xa = floordiv(-(B + 1) * den, n) + 1;
-        xb = floordiv(-A * den, n);
+        xa = fdiv(-(B + 1) * den, n) + 1;
+        xb = fdiv(-A * den, n);
     }
     xa = max(xa, lo);
     xb = min(xb, hi);
 }
 
+// previous / next candidate of a line (local index), from the bit words and
+// their per-word summaries; NONE_LO / NONE_HI when there is none
+__device__ __forceinline__ int32_t prevcand(const uint32_t *cw, const int16_t *last, int32_t x,
+                                            int32_t lane) {
+    const int32_t w = x >> 5;
+    const uint32_t m = cw[w * 32 + lane] & (0xffffffffu >> (31 - (x & 31)));
+    return m ? 32 * w + 31 - __clz(m) : (w > 0 ? (int32_t)last[(w - 1) * 32 + lane] : (int32_t)NONE_LO);
+}
+__device__ __forceinline__ int32_t nextcand(const uint32_t *cw, const int16_t *next, int32_t x,
+                                            int32_t nb, int32_t lane) {
+    const int32_t w = x >> 5;
+    const uint32_t m = cw[w * 32 + lane] & (0xffffffffu << (x & 31));
+    return m ? 32 * w + __ffs(m) - 1 : (w + 1 < nb ? (int32_t)next[(w + 1) * 32 + lane] : (int32_t)NONE_HI);
+}
+
+// Fast sweep for the default split (near backward j = 1, 2; far j >= 3;
+// NFWD near forward offsets in {0, 1}): one thread = one line, 32 output
+// positions walked toward lower u with a register window, incremental
+// coverage state and the far filter's suffix maximum carried in a register.
+// No shared scratch beyond the staged data, no barrier.
+template <int NFWD>
+__device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const uint32_t *cw,
+                                           const int16_t *last, const int16_t *next,
+                                           uint8_t *so, int lane, int32_t b, int32_t L0,
+                                           int32_t TPe, int32_t NP32, int32_t NB32, int32_t h,
+                                           int32_t s, int32_t sg, float T, int32_t Jr,
+                                           float blo0, float bhi0, float blo1, float bhi1,
+                                           float flo0, float fhi0, float t_dist, float t_disp) {
+    const float NaN = __int_as_float(0x7fc00000);
+    const float fs_ = (float)s;
+    auto V = [&](int32_t i) -> float { return (i >= 0 && i < NP32) ? sv[i * VPITCH + lane] : NaN; };
+    const int32_t i0 = sg > 0 ? 32 * b + 31 : 32 * b;       // first (highest-u) position
+    float uf = (float)(sg * (i0 - L0));                     // u of the current position
+    // suffix max of B = s v - u over positions i0 + sg*[4, Jr]  (partners of any
+    // position of the block lie within Jr; a superset keeps the filter sound)
+    float SX = -INFINITY;
+    for (int32_t j = 4; j <= Jr; ++j) {
+        const int32_t q = i0 + sg * j;
+        if (q < 0 || q >= NP32) break;
+        SX = fmaxf(SX, __fmaf_rn(fs_, sv[q * VPITCH + lane], -(uf + (float)j)));
+    }
+    float vp = V(i0), v1 = V(i0 + sg), v2 = V(i0 + 2 * sg), v3 = V(i0 + 3 * sg);
+    // coverage state: sg > 0 tracks pc(x) for x = i + h (x decreasing),
+    // sg < 0 tracks nc(x) for x = i - h (x increasing)
+    auto cover_init = [&](int32_t i) -> int32_t {
+        if (sg > 0) return prevcand(cw, last, min(i + h, NP32 - 1), lane);
+        return nextcand(cw, next, max(i - h, 0), NB32, lane);
+    };
+    int32_t cst = cover_init(i0);
+    auto dcov_of = [&](int32_t i) -> int32_t {
+        if (sg > 0) {
+            const int32_t x = min(i + h, NP32 - 1);
+            if (cst > x) cst = prevcand(cw, last, x, lane);
+            return (cst != NONE_LO && cst >= i - h) ? cst + h - i : -1;
+        }
+        const int32_t x = max(i - h, 0);
+        if (cst < x) cst = nextcand(cw, next, x, NB32, lane);
+        return (cst != NONE_HI && cst <= i + h) ? i + h - cst : -1;
+    };
+    int32_t dc = dcov_of(i0);
+    int32_t jl = 0;
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+        const int32_t i = i0 - sg * r;
+        const float vf = V(i - sg);                          // forward neighbour
+        SX = fmaxf(SX, __fmaf_rn(fs_, v3, -(uf + 3.0f)));   // fold position i + 3 sg
+        const int32_t dcn = dcov_of(i - sg);
+        const float d1 = __fsub_rn(v1, vp), d2 = __fsub_rn(v2, vp);
+        bool m = ((d1 > blo0) & (d1 < bhi0) & (dc >= 1)) | ((d2 > blo1) & (d2 < bhi1) & (dc >= 2));
+        if (NFWD) {
+            const float df = __fsub_rn(vf, vp);
+            m |= (df > flo0) & (df < fhi0) & (dcn >= 1);
+        }
+        if (!m && SX > __fsub_rn(__fmaf_rn(fs_, vp, -uf), T)) {
+            // exact resolution over backward offsets j in [3, jmax]
+            const int32_t lim = sg > 0 ? NP32 - 1 - i : i;
+            const int32_t jmax = min(min(dc, 2 * h), lim);
+            if (jmax >= 3) {
+                if (jl >= 3) {
+#pragma unroll
+                    for (int dj = 0; dj < 3 && !m; ++dj) {
+                        const int32_t j = jl + (dj == 0 ? 0 : (dj == 1 ? -1 : 1));
+                        if (j < 3 || j > jmax) continue;
+                        if (pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s, t_dist, t_disp)) {
+                            m = true; jl = j;
+                        }
+                    }
+                }
+                for (int32_t j = 3; j <= jmax && !m; ++j) {
+                    if (pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s, t_dist, t_disp)) {
+                        m = true; jl = j;
+                    }
+                }
+            }
+        }
+        const int32_t k = i - L0;
+        if (k >= 0 && k < TPe) so[k * OPITCH + lane] = (uint8_t)m;
+        v3 = v2; v2 = v1; v1 = vp; vp = vf;
+        dc = dcn;
+        uf -= 1.0f;
+    }
+}
+
 struct ViewRegs {
-    int32_t s, sg, h, jstar, nback, nfwd, vid;
+    int32_t s, sg, h, jstar, nback, nfwd, vid, jr;
     float T;              // far-filter margin t_dist + eps
     bool staged;
 };
@@ -131,7 +234,8 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
                                                     __dmul_rn((double)vd.s, (double)R))) + 1;
         // staged halo: far partners (min(2h, reach)), candidates within h of a
         // forward neighbour (h + nfwd), near partners (nback)
-        int32_t need = max(vr[g].h + vd.nfwd, min(2 * vr[g].h, jr));
+        vr[g].jr = min(2 * vr[g].h, jr);
+        int32_t need = max(vr[g].h + vd.nfwd, vr[g].jr);
         need = max(need, vd.nback);
         // filter margin: bounds the fp32 rounding of B = s v - u (|u| < 2^12)
         const double eps = ldexp(1.0, -19) * ((double)vd.s * (double)M + 4096.0 + (double)p.t_dist);
@@ -151,21 +255,24 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
         for (int k = tid; k < NP32 * 32; k += NT) sv[(k >> 5) * VPITCH + (k & 31)] = __int_as_float(0x7fc00000);
         for (int k = tid; k < 2 * NB * 32; k += NT) scw[k] = 0u;
         __syncthreads();
+        // only [L0 - halo, L0 + TPe + halo) is ever read; the rest stays NaN
+        const int32_t lo_i = L0 - halo, hi_i = L0 + TPe + halo;
         if (!xm) {
             // y-major: pos = y, lane -> x = l0 + lane + floor(y num / den): rows are positions
-            for (int i = warp; i < NP32; i += NT / 32) {
+            for (int i = lo_i + warp; i < hi_i; i += NT / 32) {
                 const int32_t y = base + i;
                 if (y < 0 || y >= H) continue;
                 const int32_t x = l0 + lane + fdiv(y * num, den);
                 if (x < 0 || x >= W) continue;
-                sv[i * VPITCH + lane] = __ldg(Df + (int64_t)y * W + x);
-                const uint32_t c = cand_dirs<false>(Df, H, W, x, y, fd.b0x, fd.b0y, p.e2_thresh, p.t_edge);
+                const float c0 = __ldg(Df + (int64_t)y * W + x);
+                sv[i * VPITCH + lane] = c0;
+                const uint32_t c = cand_dirs_v(Df, H, W, x, y, c0, fd.b0x, fd.b0y, p.e2_thresh);
                 if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
                 if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
             }
         } else {
             // x-major: pos = x, lane = y - l0 - floor(x num / den); walk image rows
-            const int32_t xs = max(base, 0), xe = min(base + NP32, W) - 1;
+            const int32_t xs = max(base + lo_i, 0), xe = min(base + hi_i, W) - 1;
             if (xs <= xe) {
                 const int32_t fa = fdiv(xs * num, den), fb = fdiv(xe * num, den);
                 const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
@@ -175,8 +282,9 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
                     for (int32_t x = xa + lane; x <= xb; x += 32) {
                         const int32_t l = y - l0 - fdiv(x * num, den);
                         const int32_t i = x - base;
-                        sv[i * VPITCH + l] = __ldg(Df + (int64_t)y * W + x);
-                        const uint32_t c = cand_dirs<false>(Df, H, W, x, y, fd.b0x, fd.b0y, p.e2_thresh, p.t_edge);
+                        const float c0 = __ldg(Df + (int64_t)y * W + x);
+                        sv[i * VPITCH + l] = c0;
+                        const uint32_t c = cand_dirs_v(Df, H, W, x, y, c0, fd.b0x, fd.b0y, p.e2_thresh);
                         if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
                         if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
                     }
@@ -239,6 +347,22 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
                 blo[j] = vd.back_lo[j]; bhi[j] = vd.back_hi[j];
                 flo[j] = vd.fwd_lo[j]; fhi[j] = vd.fwd_hi[j];
             }
+        }
+        if (cv.nback == 2 && cv.jstar == 3 && cv.nfwd <= 1) {
+            // default thresholds: barrier-free register sweep
+            const int32_t nob = (TPe + 31) >> 5;
+            for (int ob = warp; ob < nob; ob += NT / 32) {
+                const int32_t b = (L0 >> 5) + ob;
+                if (cv.nfwd)
+                    sweep_fast<1>(sv, scw + d * NB * 32, slast + d * NB * 32, snext + d * NB * 32, so,
+                                  lane, b, L0, TPe, NP32, NB32, h, s, sg, T, cv.jr, blo[0], bhi[0],
+                                  blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
+                else
+                    sweep_fast<0>(sv, scw + d * NB * 32, slast + d * NB * 32, snext + d * NB * 32, so,
+                                  lane, b, L0, TPe, NP32, NB32, h, s, sg, T, cv.jr, blo[0], bhi[0],
+                                  blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
+            }
+            continue;
         }
         // a. dcov for local positions [L0 - kMaxNear, L0 + TPe + kMaxNear)
         const int32_t D0 = L0 - kMaxNear;

@@ -54,6 +54,20 @@ __device__ __forceinline__ uint32_t cand_dirs(const float *__restrict__ Df, int3
     return (dot > 0.0 ? 1u : 0u) | (dot < 0.0 ? 2u : 0u);
 }
 
+// cand_dirs with the centre value already loaded (tiled kernel's staging);
+// squared-threshold form of E > t_e.
+__device__ __forceinline__ uint32_t cand_dirs_v(const float *__restrict__ Df, int32_t H, int32_t W,
+                                                int32_t x, int32_t y, float c, int32_t b0x,
+                                                int32_t b0y, float e2_thresh) {
+    const int64_t i = (int64_t)y * W + x;
+    const float ex = (x + 1 < W) ? __fsub_rn(__ldg(Df + i + 1), c) : 0.0f;
+    const float ey = (y + 1 < H) ? __fsub_rn(__ldg(Df + i + W), c) : 0.0f;
+    const float e2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+    if (!(e2 > e2_thresh)) return 0u;
+    const double dot = __dadd_rn(__dmul_rn((double)b0x, (double)ex), __dmul_rn((double)b0y, (double)ey));
+    return (dot > 0.0 ? 1u : 0u) | (dot < 0.0 ? 2u : 0u);
+}
+
 // The digital epipolar line through a pixel (S6) and its samples by u.
 struct LineGeom {
     int32_t H, W, line, xmajor, num, den, sg;
