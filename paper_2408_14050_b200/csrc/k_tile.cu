@@ -114,11 +114,14 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
     float uf = (float)(sg * (i0 - L0));                     // u of the current position
     // suffix max of B = s v - u over positions i0 + sg*[4, Jr]  (partners of any
     // position of the block lie within Jr; a superset keeps the filter sound)
+    // SA = position where SX is attained (the witness used to guess partners)
     float SX = -INFINITY;
+    int32_t SA = i0;
     for (int32_t j = 4; j <= Jr; ++j) {
         const int32_t q = i0 + sg * j;
         if (q < 0 || q >= NP32) break;
-        SX = fmaxf(SX, __fmaf_rn(fs_, sv[q * VPITCH + lane], -(uf + (float)j)));
+        const float Bq = __fmaf_rn(fs_, sv[q * VPITCH + lane], -(uf + (float)j));
+        if (Bq > SX) { SX = Bq; SA = q; }
     }
     float vp = V(i0), v1 = V(i0 + sg), v2 = V(i0 + 2 * sg), v3 = V(i0 + 3 * sg);
     // coverage state: sg > 0 tracks pc(x) for x = i + h (x decreasing),
@@ -144,7 +147,10 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
     for (int r = 0; r < 32; ++r) {
         const int32_t i = i0 - sg * r;
         const float vf = V(i - sg);                          // forward neighbour
-        SX = fmaxf(SX, __fmaf_rn(fs_, v3, -(uf + 3.0f)));   // fold position i + 3 sg
+        {   // fold position i + 3 sg into the suffix max
+            const float B3 = __fmaf_rn(fs_, v3, -(uf + 3.0f));
+            if (B3 > SX) { SX = B3; SA = i + 3 * sg; }
+        }
         const int32_t dcn = dcov_of(i - sg);
         const float d1 = __fsub_rn(v1, vp), d2 = __fsub_rn(v2, vp);
         bool m = ((d1 > blo0) & (d1 < bhi0) & (dc >= 1)) | ((d2 > blo1) & (d2 < bhi1) & (dc >= 2));
@@ -152,27 +158,44 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
             const float df = __fsub_rn(vf, vp);
             m |= (df > flo0) & (df < fhi0) & (dcn >= 1);
         }
-        if (!m && SX > __fsub_rn(__fmaf_rn(fs_, vp, -uf), T)) {
-            // exact resolution over backward offsets j in [3, jmax]
-            const int32_t lim = sg > 0 ? NP32 - 1 - i : i;
-            const int32_t jmax = min(min(dc, 2 * h), lim);
-            if (jmax >= 3) {
-                if (jl >= 3) {
+        const int32_t lim = sg > 0 ? NP32 - 1 - i : i;
+        const int32_t jmax = min(min(dc, 2 * h), lim);
+        bool need = false;
+        const float Bp = __fmaf_rn(fs_, vp, -uf);
+        if (!m && jmax >= 3 && SX > __fsub_rn(Bp, T)) {
+            // survivor: exact checks at guessed offsets first.  Past the
+            // witness SA, B falls ~1 per step on a flat occluder, so the
+            // partner sits ~(SX - Bp) beyond it; jl is the last hit's offset.
+            const int32_t ja = sg * (SA - i);
+            const int32_t jg = ja + min(max(0, __float2int_rn(__fsub_rn(SX, Bp))), 1 << 16);
+            int32_t cand[4] = {jg, jg - 1, jg + 1, jl};
 #pragma unroll
-                    for (int dj = 0; dj < 3 && !m; ++dj) {
-                        const int32_t j = jl + (dj == 0 ? 0 : (dj == 1 ? -1 : 1));
-                        if (j < 3 || j > jmax) continue;
-                        if (pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s, t_dist, t_disp)) {
-                            m = true; jl = j;
-                        }
-                    }
-                }
-                for (int32_t j = 3; j <= jmax && !m; ++j) {
-                    if (pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s, t_dist, t_disp)) {
-                        m = true; jl = j;
-                    }
+            for (int c = 0; c < 4; ++c) {
+                const int32_t j = cand[c];
+                if (!m && j >= 3 && j <= jmax &&
+                    pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s, t_dist, t_disp)) {
+                    m = true; jl = j;
                 }
             }
+            need = !m;
+        }
+        // remaining survivors: warp-cooperative exhaustive search, 32 offsets
+        // per step, one pending line at a time (all lanes share position i)
+        unsigned pend = __ballot_sync(0xffffffffu, need);
+        while (pend) {
+            const int src = __ffs(pend) - 1;
+            pend &= pend - 1;
+            const float vs = __shfl_sync(0xffffffffu, vp, src);
+            const int32_t jm = __shfl_sync(0xffffffffu, jmax, src);
+            int32_t found = -1;
+            for (int32_t j0 = 3; j0 <= jm && found < 0; j0 += 32) {
+                const int32_t j = j0 + lane;
+                const bool ok = j <= jm && pair_exact(sv[(i + sg * j) * VPITCH + src], vs, -j, s,
+                                                      t_dist, t_disp);
+                const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                if (bal) found = j0 + __ffs(bal) - 1;
+            }
+            if (lane == src && found >= 0) { m = true; jl = found; }
         }
         const int32_t k = i - L0;
         if (k >= 0 && k < TPe) so[k * OPITCH + lane] = (uint8_t)m;
@@ -212,6 +235,10 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
     const float *Df = D + (int64_t)f * HW;
     const int32_t l0 = td.l0, P0 = td.p0, P1 = td.p1, TPe = P1 - P0;
     const int32_t num = fd.num, den = fd.den;
+    // floor(a / den): a shift for the power-of-two slopes of all |b| <= 2 arrays
+    const bool dpow = (den & (den - 1)) == 0;
+    const int32_t dsh = __ffs(den) - 1;
+    auto FD = [&](int32_t a) -> int32_t { return dpow ? (a >> dsh) : floordiv(a, den); };
     const bool xm = fd.xmajor != 0;
 
     // ------------------------------------------------ per-view parameters
@@ -262,7 +289,7 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
             for (int i = lo_i + warp; i < hi_i; i += NT / 32) {
                 const int32_t y = base + i;
                 if (y < 0 || y >= H) continue;
-                const int32_t x = l0 + lane + fdiv(y * num, den);
+                const int32_t x = l0 + lane + FD(y * num);
                 if (x < 0 || x >= W) continue;
                 const float c0 = __ldg(Df + (int64_t)y * W + x);
                 sv[i * VPITCH + lane] = c0;
@@ -274,13 +301,13 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
             // x-major: pos = x, lane = y - l0 - floor(x num / den); walk image rows
             const int32_t xs = max(base + lo_i, 0), xe = min(base + hi_i, W) - 1;
             if (xs <= xe) {
-                const int32_t fa = fdiv(xs * num, den), fb = fdiv(xe * num, den);
+                const int32_t fa = FD(xs * num), fb = FD(xe * num);
                 const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
                 for (int32_t y = ylo + warp; y <= yhi; y += NT / 32) {
                     int32_t xa, xb;
                     row_run(y, l0, num, den, xs, xe, xa, xb);
                     for (int32_t x = xa + lane; x <= xb; x += 32) {
-                        const int32_t l = y - l0 - fdiv(x * num, den);
+                        const int32_t l = y - l0 - FD(x * num);
                         const int32_t i = x - base;
                         const float c0 = __ldg(Df + (int64_t)y * W + x);
                         sv[i * VPITCH + l] = c0;
@@ -482,24 +509,58 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
     for (int g = 0; g < gd.nv; ++g) {
         const uint8_t *so = sout + (size_t)g * TP * OPITCH;
         uint8_t *Mv = masks + ((int64_t)f * nviews + gd.view[g]) * HW;
+        const bool al4 = ((W & 3) == 0) && ((l0 & 3) == 0) && ((P0 & 3) == 0) && num == 0;
+        if (!xm && al4) {
+            // columns: each output row is 32 contiguous bytes -> 8 x 4-byte stores
+            for (int k = warp * 4 + (lane >> 3); k < TPe; k += NT / 8) {
+                const int32_t y = P0 + k, x = l0 + 4 * (lane & 7);
+                if (y >= H || x >= W) continue;
+                const uint8_t *src = so + k * OPITCH + 4 * (lane & 7);
+                if (x + 3 < W) {
+                    __stcs(reinterpret_cast<uint32_t *>(Mv + (int64_t)y * W + x),
+                           *reinterpret_cast<const uint32_t *>(src));
+                } else {
+                    for (int e = 0; e < 4 && x + e < W; ++e) Mv[(int64_t)y * W + x + e] = src[e];
+                }
+            }
+            continue;
+        }
+        if (xm && al4) {
+            // rows: row l0 + l, positions [P0, P1) -> 4-byte packed stores
+            const int32_t nq = (TPe + 3) >> 2;
+            for (int t = tid; t < 32 * nq; t += NT) {
+                const int32_t l = t / nq, q = t - l * nq;
+                const int32_t y = l0 + l, x = P0 + 4 * q;
+                if (y >= H) continue;
+                const uint8_t *src = so + (4 * q) * OPITCH + l;
+                if (x + 3 < P1) {
+                    const uint32_t w = (uint32_t)src[0] | ((uint32_t)src[OPITCH] << 8) |
+                                       ((uint32_t)src[2 * OPITCH] << 16) | ((uint32_t)src[3 * OPITCH] << 24);
+                    __stcs(reinterpret_cast<uint32_t *>(Mv + (int64_t)y * W + x), w);
+                } else {
+                    for (int e = 0; e < 4 && x + e < P1; ++e) Mv[(int64_t)y * W + x + e] = src[e * OPITCH];
+                }
+            }
+            continue;
+        }
         if (!xm) {
             for (int k = warp; k < TPe; k += NT / 32) {
                 const int32_t y = P0 + k;
                 if (y < 0 || y >= H) continue;
-                const int32_t x = l0 + lane + fdiv(y * num, den);
+                const int32_t x = l0 + lane + FD(y * num);
                 if (x < 0 || x >= W) continue;
                 __stcs(Mv + (int64_t)y * W + x, so[k * OPITCH + lane]);
             }
         } else {
             const int32_t xs = max(P0, 0), xe = min(P1, W) - 1;
             if (xs > xe) continue;
-            const int32_t fa = fdiv(xs * num, den), fb = fdiv(xe * num, den);
+            const int32_t fa = FD(xs * num), fb = FD(xe * num);
             const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
             for (int32_t y = ylo + warp; y <= yhi; y += NT / 32) {
                 int32_t xa, xb;
                 row_run(y, l0, num, den, xs, xe, xa, xb);
                 for (int32_t x = xa + lane; x <= xb; x += 32) {
-                    const int32_t l = y - l0 - fdiv(x * num, den);
+                    const int32_t l = y - l0 - FD(x * num);
                     __stcs(Mv + (int64_t)y * W + x, so[(x - P0) * OPITCH + l]);
                 }
             }
