@@ -1,0 +1,141 @@
+// k_prologue.cu -- K0 of the tiled path: one streaming pass over a chunk of
+// frames computing
+//   * the exact per-frame min / max / non-finite count (S1; PAPER.md:113-115,
+//     Eq. 3 "minimum and maximum occurring disparity"), and
+//   * a per-pixel candidate code: for every line family f, bit 2f = pixel is
+//     a candidate of +b0_f, bit 2f+1 = candidate of -b0_f (Eqs. 1-2,
+//     E > t_e and |Theta - phi| < pi/2).
+// The edge test runs once per pixel here instead of once per family in K1.
+// D is read once from HBM (16-byte loads); the row below is an L2 hit (the
+// neighbouring block reads it at the same time); codes stay L2-resident for
+// K1, which runs on the same chunk right after.
+#include "occ_internal.h"
+
+namespace occ {
+
+struct FamDirs {
+    int32_t n;
+    int32_t bx[kMaxFamilies], by[kMaxFamilies];
+};
+
+template <typename CodeT>
+__device__ __forceinline__ CodeT pixel_code(float c, float right, float below, bool has_r, bool has_b,
+                                            const FamDirs &fd, float e2_thresh) {
+    // Eq. 1 forward differences (0 on the last column / row), E^2 vs the exact
+    // squared threshold of E > t_e (sqrt_rn is monotone)
+    const float ex = has_r ? __fsub_rn(right, c) : 0.0f;
+    const float ey = has_b ? __fsub_rn(below, c) : 0.0f;
+    const float e2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+    uint32_t code = 0;
+    if (e2 > e2_thresh) {
+        for (int k = 0; k < fd.n; ++k) {
+            // Eq. 2 <=> b0 . (E_x, E_y) > 0, exact sign in binary64
+            const double dot = __dadd_rn(__dmul_rn((double)fd.bx[k], (double)ex),
+                                         __dmul_rn((double)fd.by[k], (double)ey));
+            code |= ((dot > 0.0) ? 1u : 0u) << (2 * k);
+            code |= ((dot < 0.0) ? 1u : 0u) << (2 * k + 1);
+        }
+    }
+    return (CodeT)code;
+}
+
+// four consecutive codes in one vector store (dst is 4-code aligned)
+__device__ __forceinline__ void store4(uint8_t *dst, uint8_t a, uint8_t b, uint8_t c, uint8_t d) {
+    *reinterpret_cast<uint32_t *>(dst) = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)c << 16) | ((uint32_t)d << 24);
+}
+__device__ __forceinline__ void store4(uint16_t *dst, uint16_t a, uint16_t b, uint16_t c, uint16_t d) {
+    *reinterpret_cast<uint2 *>(dst) = make_uint2((uint32_t)a | ((uint32_t)b << 16), (uint32_t)c | ((uint32_t)d << 16));
+}
+__device__ __forceinline__ void store4(uint32_t *dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(a, b, c, d);
+}
+
+__device__ __forceinline__ void stat_acc(float d, int32_t &lo, int32_t &hi, uint32_t &bad) {
+    if (isfinite(d)) {
+        const int32_t k = float_key(d);
+        lo = min(lo, k);
+        hi = max(hi, k);
+    } else {
+        ++bad;
+    }
+}
+
+// grid: (blocks per frame, frames); block 256
+template <typename CodeT>
+__global__ void __launch_bounds__(256) k_prologue(const float *__restrict__ D, int32_t H, int32_t W,
+                                                  FamDirs fd, float e2_thresh, FrameStats *st,
+                                                  CodeT *__restrict__ codes) {
+    const int f = blockIdx.y;
+    const int64_t HW = (int64_t)H * W;
+    const float *Df = D + (int64_t)f * HW;
+    CodeT *Cf = codes + (int64_t)f * HW;
+    int32_t lo = 0x7FFFFFFF, hi = (int32_t)0x80000000;
+    uint32_t bad = 0;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    if ((W & 3) == 0 && (reinterpret_cast<uintptr_t>(Df) & 15) == 0) {
+        const float4 *D4 = reinterpret_cast<const float4 *>(Df);
+        const int32_t W4 = W >> 2;
+        const int64_t n4 = HW >> 2;
+        for (int64_t t = tid; t < n4; t += nth) {
+            const int32_t y = (int32_t)(t / W4), x = (int32_t)(t - (int64_t)y * W4) * 4;
+            const float4 c = __ldg(D4 + t);
+            const bool has_b = y + 1 < H;
+            const float4 b = has_b ? __ldg(D4 + t + W4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const bool has_r4 = x + 4 < W;
+            const float r4 = has_r4 ? __ldg(Df + (int64_t)y * W + x + 4) : 0.0f;
+            stat_acc(c.x, lo, hi, bad);
+            stat_acc(c.y, lo, hi, bad);
+            stat_acc(c.z, lo, hi, bad);
+            stat_acc(c.w, lo, hi, bad);
+            CodeT k0 = pixel_code<CodeT>(c.x, c.y, b.x, true, has_b, fd, e2_thresh);
+            CodeT k1 = pixel_code<CodeT>(c.y, c.z, b.y, true, has_b, fd, e2_thresh);
+            CodeT k2 = pixel_code<CodeT>(c.z, c.w, b.z, true, has_b, fd, e2_thresh);
+            CodeT k3 = pixel_code<CodeT>(c.w, r4, b.w, has_r4, has_b, fd, e2_thresh);
+            store4(Cf + (int64_t)t * 4, k0, k1, k2, k3);
+        }
+    } else {
+        for (int64_t i = tid; i < HW; i += nth) {
+            const int32_t y = (int32_t)(i / W), x = (int32_t)(i - (int64_t)y * W);
+            const float c = Df[i];
+            stat_acc(c, lo, hi, bad);
+            const bool has_r = x + 1 < W, has_b = y + 1 < H;
+            Cf[i] = pixel_code<CodeT>(c, has_r ? Df[i + 1] : 0.0f, has_b ? Df[i + W] : 0.0f, has_r,
+                                      has_b, fd, e2_thresh);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&st[f].minkey, lo);
+        atomicMax(&st[f].maxkey, hi);
+        if (bad) atomicAdd(&st[f].nonfinite, bad);
+    }
+}
+
+cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
+                            const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
+                            FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s) {
+    FamDirs fd{};
+    fd.n = nfam;
+    for (int k = 0; k < nfam; ++k) { fd.bx[k] = fams_host[k].b0x; fd.by[k] = fams_host[k].b0y; }
+    const int64_t HW = (int64_t)H * W;
+    const int64_t per_block = 256 * 4 * 4;
+    int bx = (int)((HW + per_block - 1) / per_block);
+    if (bx < 1) bx = 1;
+    if (bx > 2048) bx = 2048;
+    dim3 grid(bx, frames);
+    if (code_bytes == 1)
+        k_prologue<uint8_t><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
+    else if (code_bytes == 2)
+        k_prologue<uint16_t><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint16_t *)codes);
+    else
+        k_prologue<uint32_t><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint32_t *)codes);
+    return cudaGetLastError();
+}
+
+}  // namespace occ

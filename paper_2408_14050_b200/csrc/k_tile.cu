@@ -36,6 +36,7 @@ constexpr int VPITCH = 33;             // floats per staged position (32 lanes +
 constexpr int OPITCH = 36;             // bytes per output position (32 lanes + pad)
 constexpr int DC = TP + 2 * kMaxNear;  // dcov entries (outputs +- near reach)
 constexpr int16_t NONE_LO = -30000, NONE_HI = 30000;
+constexpr int kQueueCap = 128;          // survivor queue entries per warp
 
 constexpr size_t OFF_V = 0;
 constexpr size_t OFF_CW = OFF_V + sizeof(float) * NPMAX * VPITCH;
@@ -44,7 +45,8 @@ constexpr size_t OFF_NEXT = OFF_LAST + sizeof(int16_t) * 2 * NB * 32;
 constexpr size_t OFF_DCOV = OFF_NEXT + sizeof(int16_t) * 2 * NB * 32;
 constexpr size_t OFF_AGG = OFF_DCOV + sizeof(int16_t) * DC * 32;
 constexpr size_t OFF_OUT = OFF_AGG + sizeof(float) * 2 * NB * 32;
-constexpr size_t SMEM = OFF_OUT + (size_t)kGroupViews * TP * OPITCH;
+constexpr size_t OFF_Q = OFF_OUT + (size_t)kGroupViews * TP * OPITCH;
+constexpr size_t SMEM = OFF_Q + sizeof(uint32_t) * (NT / 32) * kQueueCap;
 }  // namespace
 
 size_t tile_smem_bytes() { return SMEM; }
@@ -102,51 +104,94 @@ __device__ __forceinline__ int32_t nextcand(const uint32_t *cw, const int16_t *n
 template <int NFWD>
 __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const uint32_t *cw,
                                            const int16_t *last, const int16_t *next,
-                                           uint8_t *so, int lane, int32_t b, int32_t L0,
-                                           int32_t TPe, int32_t NP32, int32_t NB32, int32_t h,
-                                           int32_t s, int32_t sg, float T, int32_t Jr,
+                                           uint8_t *so, uint32_t *queue, int lane, int32_t b,
+                                           int32_t L0, int32_t TPe, int32_t NP32, int32_t NB32,
+                                           int32_t h, int32_t s, int32_t sg, float T, int32_t Jr,
                                            float blo0, float bhi0, float blo1, float bhi1,
                                            float flo0, float fhi0, float t_dist, float t_disp) {
-    const float NaN = __int_as_float(0x7fc00000);
     const float fs_ = (float)s;
-    auto V = [&](int32_t i) -> float { return (i >= 0 && i < NP32) ? sv[i * VPITCH + lane] : NaN; };
     const int32_t i0 = sg > 0 ? 32 * b + 31 : 32 * b;       // first (highest-u) position
     float uf = (float)(sg * (i0 - L0));                     // u of the current position
     // suffix max of B = s v - u over positions i0 + sg*[4, Jr]  (partners of any
-    // position of the block lie within Jr; a superset keeps the filter sound)
+    // position of the block lie within Jr; a superset keeps the filter sound);
     // SA = position where SX is attained (the witness used to guess partners)
     float SX = -INFINITY;
     int32_t SA = i0;
-    for (int32_t j = 4; j <= Jr; ++j) {
-        const int32_t q = i0 + sg * j;
-        if (q < 0 || q >= NP32) break;
-        const float Bq = __fmaf_rn(fs_, sv[q * VPITCH + lane], -(uf + (float)j));
-        if (Bq > SX) { SX = Bq; SA = q; }
+    {
+        const int32_t jend = min(Jr, sg > 0 ? NP32 - 1 - i0 : i0);
+        for (int32_t j = 4; j <= jend; ++j) {
+            const int32_t q = i0 + sg * j;
+            const float Bq = __fmaf_rn(fs_, sv[q * VPITCH + lane], -(uf + (float)j));
+            if (Bq > SX) { SX = Bq; SA = q; }
+        }
     }
-    float vp = V(i0), v1 = V(i0 + sg), v2 = V(i0 + 2 * sg), v3 = V(i0 + 3 * sg);
+    // the staged range has >= 32 NaN-padded positions beyond every output block
+    float vp = sv[i0 * VPITCH + lane], v1 = sv[(i0 + sg) * VPITCH + lane];
+    float v2 = sv[(i0 + 2 * sg) * VPITCH + lane], v3 = sv[(i0 + 3 * sg) * VPITCH + lane];
     // coverage state: sg > 0 tracks pc(x) for x = i + h (x decreasing),
     // sg < 0 tracks nc(x) for x = i - h (x increasing)
-    auto cover_init = [&](int32_t i) -> int32_t {
-        if (sg > 0) return prevcand(cw, last, min(i + h, NP32 - 1), lane);
-        return nextcand(cw, next, max(i - h, 0), NB32, lane);
-    };
-    int32_t cst = cover_init(i0);
+    int32_t cst = sg > 0 ? prevcand(cw, last, i0 + h, lane) : nextcand(cw, next, i0 - h, NB32, lane);
     auto dcov_of = [&](int32_t i) -> int32_t {
         if (sg > 0) {
-            const int32_t x = min(i + h, NP32 - 1);
+            const int32_t x = i + h;
             if (cst > x) cst = prevcand(cw, last, x, lane);
             return (cst != NONE_LO && cst >= i - h) ? cst + h - i : -1;
         }
-        const int32_t x = max(i - h, 0);
+        const int32_t x = i - h;
         if (cst < x) cst = nextcand(cw, next, x, NB32, lane);
         return (cst != NONE_HI && cst <= i + h) ? i + h - cst : -1;
     };
     int32_t dc = dcov_of(i0);
-    int32_t jl = 0;
+    int32_t qn = 0;                                         // warp-uniform queue length
+    // exact resolution of queued survivors, one per lane, at guessed offsets;
+    // misses go to a warp-cooperative exhaustive search (32 offsets per step)
+    auto flush = [&]() {
+        __syncwarp();
+        for (int32_t e0 = 0; e0 < qn; e0 += 32) {
+            const int32_t e = e0 + lane;
+            bool miss = false;
+            uint32_t ent = 0;
+            if (e < qn) {
+                ent = queue[e];
+                const int32_t r = ent & 31, ln = (ent >> 5) & 31, jg = (ent >> 10) & 2047, jm = ent >> 21;
+                const int32_t i = i0 - sg * r;
+                const float vq0 = sv[i * VPITCH + ln];
+                bool hit = false;
+#pragma unroll
+                for (int c = 0; c < 5; ++c) {
+                    const int32_t j = jg + (c == 0 ? 0 : (c == 1 ? -1 : (c == 2 ? 1 : (c == 3 ? -2 : 2))));
+                    if (!hit && j >= 3 && j <= jm &&
+                        pair_exact(sv[(i + sg * j) * VPITCH + ln], vq0, -j, s, t_dist, t_disp)) hit = true;
+                }
+                if (hit) so[(i - L0) * OPITCH + ln] = 1;
+                miss = !hit;
+            }
+            unsigned pend = __ballot_sync(0xffffffffu, miss);
+            while (pend) {
+                const int src = __ffs(pend) - 1;
+                pend &= pend - 1;
+                const uint32_t en = __shfl_sync(0xffffffffu, ent, src);
+                const int32_t r = en & 31, ln = (en >> 5) & 31, jm = en >> 21;
+                const int32_t i = i0 - sg * r;
+                const float vs = sv[i * VPITCH + ln];
+                bool found = false;
+                for (int32_t j0 = 3; j0 <= jm && !found; j0 += 32) {
+                    const int32_t j = j0 + lane;
+                    const bool ok = j <= jm && pair_exact(sv[(i + sg * j) * VPITCH + ln], vs, -j, s,
+                                                          t_dist, t_disp);
+                    found = __ballot_sync(0xffffffffu, ok) != 0u;
+                }
+                if (found && lane == 0) so[(i - L0) * OPITCH + ln] = 1;
+            }
+        }
+        __syncwarp();
+        qn = 0;
+    };
+    const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 4
     for (int r = 0; r < 32; ++r) {
         const int32_t i = i0 - sg * r;
-        const float vf = V(i - sg);                          // forward neighbour
+        const float vf = sv[(i - sg) * VPITCH + lane];       // forward neighbour
         {   // fold position i + 3 sg into the suffix max
             const float B3 = __fmaf_rn(fs_, v3, -(uf + 3.0f));
             if (B3 > SX) { SX = B3; SA = i + 3 * sg; }
@@ -158,51 +203,28 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
             const float df = __fsub_rn(vf, vp);
             m |= (df > flo0) & (df < fhi0) & (dcn >= 1);
         }
-        const int32_t lim = sg > 0 ? NP32 - 1 - i : i;
-        const int32_t jmax = min(min(dc, 2 * h), lim);
-        bool need = false;
+        // far filter: a partner at j >= 3 needs some B_q > B_p - t_dist
         const float Bp = __fmaf_rn(fs_, vp, -uf);
-        if (!m && jmax >= 3 && SX > __fsub_rn(Bp, T)) {
-            // survivor: exact checks at guessed offsets first.  Past the
-            // witness SA, B falls ~1 per step on a flat occluder, so the
-            // partner sits ~(SX - Bp) beyond it; jl is the last hit's offset.
-            const int32_t ja = sg * (SA - i);
-            const int32_t jg = ja + min(max(0, __float2int_rn(__fsub_rn(SX, Bp))), 1 << 16);
-            int32_t cand[4] = {jg, jg - 1, jg + 1, jl};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int32_t j = cand[c];
-                if (!m && j >= 3 && j <= jmax &&
-                    pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s, t_dist, t_disp)) {
-                    m = true; jl = j;
-                }
+        const int32_t jmax = min(dc, 2 * h);
+        const bool surv = !m && jmax >= 3 && SX > __fsub_rn(Bp, T);
+        const unsigned bal = __ballot_sync(0xffffffffu, surv);
+        if (qn + __popc(bal) > kQueueCap) flush();
+        if (bal) {
+            if (surv) {
+                // guess: past the witness SA, B falls ~1 per step on a flat
+                // occluder, so the partner sits ~(SX - Bp) beyond it
+                const int32_t jg = sg * (SA - i) + min(max(0, __float2int_rn(__fsub_rn(SX, Bp))), 1023);
+                queue[qn + __popc(bal & lt)] = (uint32_t)r | ((uint32_t)lane << 5) |
+                                               ((uint32_t)min(jg, 2047) << 10) | ((uint32_t)jmax << 21);
             }
-            need = !m;
+            qn += __popc(bal);
         }
-        // remaining survivors: warp-cooperative exhaustive search, 32 offsets
-        // per step, one pending line at a time (all lanes share position i)
-        unsigned pend = __ballot_sync(0xffffffffu, need);
-        while (pend) {
-            const int src = __ffs(pend) - 1;
-            pend &= pend - 1;
-            const float vs = __shfl_sync(0xffffffffu, vp, src);
-            const int32_t jm = __shfl_sync(0xffffffffu, jmax, src);
-            int32_t found = -1;
-            for (int32_t j0 = 3; j0 <= jm && found < 0; j0 += 32) {
-                const int32_t j = j0 + lane;
-                const bool ok = j <= jm && pair_exact(sv[(i + sg * j) * VPITCH + src], vs, -j, s,
-                                                      t_dist, t_disp);
-                const unsigned bal = __ballot_sync(0xffffffffu, ok);
-                if (bal) found = j0 + __ffs(bal) - 1;
-            }
-            if (lane == src && found >= 0) { m = true; jl = found; }
-        }
-        const int32_t k = i - L0;
-        if (k >= 0 && k < TPe) so[k * OPITCH + lane] = (uint8_t)m;
+        so[(i - L0) * OPITCH + lane] = (uint8_t)m;
         v3 = v2; v2 = v1; v1 = vp; vp = vf;
         dc = dcn;
         uf -= 1.0f;
     }
+    flush();
 }
 
 struct ViewRegs {
@@ -215,8 +237,9 @@ __global__ void __launch_bounds__(NT, 2)
 k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__restrict__ tiles,
        const GroupDesc *__restrict__ groups, const ViewDesc *__restrict__ views, int32_t nviews,
        const FamilyDesc *__restrict__ fams, const FrameStats *__restrict__ st, Params p,
-       uint8_t *__restrict__ masks) {
+       uint8_t *__restrict__ masks, const void *__restrict__ codes, int32_t code_bytes) {
     extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t *squeue = reinterpret_cast<uint32_t *>(smem + OFF_Q) + (threadIdx.x >> 5) * kQueueCap;
     float *sv = reinterpret_cast<float *>(smem + OFF_V);
     uint32_t *scw = reinterpret_cast<uint32_t *>(smem + OFF_CW);
     int16_t *slast = reinterpret_cast<int16_t *>(smem + OFF_LAST);
@@ -271,7 +294,8 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
                        vd.nfwd <= kMaxNear && vd.jstar <= 32;
         if (vr[g].staged) { halo = max(halo, need); any_staged = true; }
     }
-    const int32_t HALO32 = (halo + 31) & ~31;
+    // >= 32 NaN-padded positions on each side of the output blocks
+    const int32_t HALO32 = max(32, (halo + 31) & ~31);
     const int32_t L0 = HALO32;                     // local index of P0
     const int32_t base = P0 - HALO32;              // position of local index 0
     const int32_t NP32 = ((TPe + 31) & ~31) + 2 * HALO32;
@@ -284,6 +308,17 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
         __syncthreads();
         // only [L0 - halo, L0 + TPe + halo) is ever read; the rest stays NaN
         const int32_t lo_i = L0 - halo, hi_i = L0 + TPe + halo;
+        // candidate bits of this family from K0's per-pixel codes (Eqs. 1-2)
+        const int cshift = 2 * gd.fam;
+        const unsigned char *Cb = reinterpret_cast<const unsigned char *>(codes) +
+                                  (int64_t)f * HW * code_bytes;
+        auto cand_of = [&](int64_t idx) -> uint32_t {
+            uint32_t c;
+            if (code_bytes == 1) c = __ldg(Cb + idx);
+            else if (code_bytes == 2) c = __ldg(reinterpret_cast<const uint16_t *>(Cb) + idx);
+            else c = __ldg(reinterpret_cast<const uint32_t *>(Cb) + idx);
+            return (c >> cshift) & 3u;
+        };
         if (!xm) {
             // y-major: pos = y, lane -> x = l0 + lane + floor(y num / den): rows are positions
             for (int i = lo_i + warp; i < hi_i; i += NT / 32) {
@@ -291,9 +326,9 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
                 if (y < 0 || y >= H) continue;
                 const int32_t x = l0 + lane + FD(y * num);
                 if (x < 0 || x >= W) continue;
-                const float c0 = __ldg(Df + (int64_t)y * W + x);
-                sv[i * VPITCH + lane] = c0;
-                const uint32_t c = cand_dirs_v(Df, H, W, x, y, c0, fd.b0x, fd.b0y, p.e2_thresh);
+                const int64_t idx = (int64_t)y * W + x;
+                sv[i * VPITCH + lane] = __ldg(Df + idx);
+                const uint32_t c = cand_of(idx);
                 if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
                 if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
             }
@@ -309,9 +344,9 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
                     for (int32_t x = xa + lane; x <= xb; x += 32) {
                         const int32_t l = y - l0 - FD(x * num);
                         const int32_t i = x - base;
-                        const float c0 = __ldg(Df + (int64_t)y * W + x);
-                        sv[i * VPITCH + l] = c0;
-                        const uint32_t c = cand_dirs_v(Df, H, W, x, y, c0, fd.b0x, fd.b0y, p.e2_thresh);
+                        const int64_t idx = (int64_t)y * W + x;
+                        sv[i * VPITCH + l] = __ldg(Df + idx);
+                        const uint32_t c = cand_of(idx);
                         if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
                         if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
                     }
@@ -382,11 +417,11 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
                 const int32_t b = (L0 >> 5) + ob;
                 if (cv.nfwd)
                     sweep_fast<1>(sv, scw + d * NB * 32, slast + d * NB * 32, snext + d * NB * 32, so,
-                                  lane, b, L0, TPe, NP32, NB32, h, s, sg, T, cv.jr, blo[0], bhi[0],
+                                  squeue, lane, b, L0, TPe, NP32, NB32, h, s, sg, T, cv.jr, blo[0], bhi[0],
                                   blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                 else
                     sweep_fast<0>(sv, scw + d * NB * 32, slast + d * NB * 32, snext + d * NB * 32, so,
-                                  lane, b, L0, TPe, NP32, NB32, h, s, sg, T, cv.jr, blo[0], bhi[0],
+                                  squeue, lane, b, L0, TPe, NP32, NB32, h, s, sg, T, cv.jr, blo[0], bhi[0],
                                   blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
             }
             continue;
@@ -571,11 +606,13 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
 cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
                         const TileDesc *tiles, int32_t ntiles, const GroupDesc *groups,
                         const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
-                        const FrameStats *st, const Params &p, uint8_t *masks, cudaStream_t s) {
+                        const FrameStats *st, const Params &p, uint8_t *masks, const void *codes,
+                        int32_t code_bytes, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)ntiles, (unsigned)batch);
-    k_tile<<<grid, NT, SMEM, s>>>(D, H, W, tiles, groups, views, nviews, fams, st, p, masks);
+    k_tile<<<grid, NT, SMEM, s>>>(D, H, W, tiles, groups, views, nviews, fams, st, p, masks, codes,
+                                  code_bytes);
     return cudaGetLastError();
 }
 

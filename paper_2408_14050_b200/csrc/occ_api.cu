@@ -29,6 +29,8 @@ struct occ_ctx {
     std::vector<TileDesc> tiles;
     GroupDesc *d_groups = nullptr;
     TileDesc *d_tiles = nullptr;
+    void *d_codes = nullptr;             // K0 -> K1 candidate codes, one chunk of frames
+    int32_t code_bytes = 1, chunk = 1;
     float *d_stage_D = nullptr;          // occ_detect_host staging (lazy)
     uint8_t *d_stage_M = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -276,13 +278,20 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
     }
     c->nfam = (int32_t)c->fams.size();
     build_tiles(c);
+    c->code_bytes = c->nfam <= 4 ? 1 : (c->nfam <= 8 ? 2 : 4);
+    {   // frames per K0/K1 chunk: D + codes of a chunk within ~48 MiB of L2
+        const double per = (double)H * W * (4.0 + c->code_bytes);
+        c->chunk = (int32_t)std::max(1.0, std::min(64.0, std::floor(48.0 * 1048576.0 / per)));
+        c->chunk = std::min(c->chunk, max_batch);
+    }
 
     if (cudaGetDevice(&c->device) != cudaSuccess) { cudaGetLastError(); delete c; return OCC_ERR_CUDA; }
     if (cudaMalloc(&c->d_views, sizeof(ViewDesc) * c->views.size()) != cudaSuccess ||
         cudaMalloc(&c->d_fams, sizeof(FamilyDesc) * c->fams.size()) != cudaSuccess ||
         cudaMalloc(&c->d_groups, sizeof(GroupDesc) * c->groups.size()) != cudaSuccess ||
         cudaMalloc(&c->d_tiles, sizeof(TileDesc) * c->tiles.size()) != cudaSuccess ||
-        cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess) {
+        cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess ||
+        cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess) {
         cudaGetLastError();
         occ_destroy(c);
         return OCC_ERR_OOM;
@@ -326,21 +335,34 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
         CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
         ps.end();
     }
-    {
-        ProfScope ps(c, OCC_KERNEL_STATS, s);
-        CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
-        ps.end();
-    }
     if (c->path == OCC_PATH_DIRECT) {
+        {
+            ProfScope ps(c, OCC_KERNEL_STATS, s);
+            CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
+            ps.end();
+        }
         ProfScope pd(c, OCC_KERNEL_DIRECT, s);
         CK(launch_direct(D, c->H, c->W, batch, c->d_views, c->V, c->d_fams, c->d_stats,
                          c->params, M, s)); ++launches;
         pd.end();
     } else {
-        ProfScope pt(c, OCC_KERNEL_TILE, s);
-        CK(launch_tile(D, c->H, c->W, batch, c->d_tiles, (int32_t)c->tiles.size(), c->d_groups,
-                       c->d_views, c->V, c->d_fams, c->d_stats, c->params, M, s)); ++launches;
-        pt.end();
+        // chunks of frames small enough that D and the candidate codes written
+        // by K0 are still L2-resident when K1 reads them
+        for (int32_t c0 = 0; c0 < batch; c0 += c->chunk) {
+            const int32_t n = std::min(c->chunk, batch - c0);
+            const float *Dc = D + (int64_t)c0 * HW;
+            {
+                ProfScope ps(c, OCC_KERNEL_STATS, s);
+                CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
+                                   c->d_stats + c0, c->d_codes, c->code_bytes, s)); ++launches;
+                ps.end();
+            }
+            ProfScope pt(c, OCC_KERNEL_TILE, s);
+            CK(launch_tile(Dc, c->H, c->W, n, c->d_tiles, (int32_t)c->tiles.size(), c->d_groups,
+                           c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params,
+                           M + (int64_t)c0 * c->V * HW, c->d_codes, c->code_bytes, s)); ++launches;
+            pt.end();
+        }
     }
     c->last_stream = s;
     c->last_batch = batch;
@@ -431,6 +453,7 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_views);
     cudaFree(c->d_fams);
     cudaFree(c->d_stats);
+    cudaFree(c->d_codes);
     cudaFree(c->d_groups);
     cudaFree(c->d_tiles);
     cudaFree(c->d_stage_D);

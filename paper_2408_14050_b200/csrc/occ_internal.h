@@ -100,6 +100,10 @@ constexpr int kTileHaloMax = 96;       // staged halo per side (multiple of 32)
 cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
                         const TileDesc *tiles, int32_t ntiles, const GroupDesc *groups,
                         const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
-                        const FrameStats *st, const Params &p, uint8_t *masks, cudaStream_t s);
+                        const FrameStats *st, const Params &p, uint8_t *masks, const void *codes,
+                        int32_t code_bytes, cudaStream_t s);
+cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
+                            const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
+                            FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s);
 
 }  // namespace occ
