@@ -205,7 +205,8 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
         }
         // far filter: a partner at j >= 3 needs some B_q > B_p - t_dist
         const float Bp = __fmaf_rn(fs_, vp, -uf);
-        const int32_t jmax = min(dc, 2 * h);
+        // partners lie within the staged reach (>= min(2h, t_dist + s R))
+        const int32_t jmax = min(min(dc, 2 * h), sg > 0 ? NP32 - 1 - i : i);
         const bool surv = !m && jmax >= 3 && SX > __fsub_rn(Bp, T);
         const unsigned bal = __ballot_sync(0xffffffffu, surv);
         if (qn + __popc(bal) > kQueueCap) flush();
