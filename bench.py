@@ -237,7 +237,9 @@ def main():
     views = scenes.config_views(CFG)
     V = len(views)
     nf = args.frames
-    frames = make_frames(nf, rank * nf)
+    from paper_2408_14050_b200 import shard
+    first, nf = shard.weak_shard(nf, rank)          # rank r: frames [r*nf, (r+1)*nf)
+    frames = make_frames(nf, first)
     d = torch.from_numpy(frames).to(dev)
     masks = torch.empty((nf, V, H, W), dtype=torch.uint8, device=dev)
     det = Detector(H, W, views, max_batch=nf, path=args.path)
@@ -266,11 +268,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     kt = det.profile_read()
     det.profile(False)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = shard.max_over_ranks(ms, dev)
     ms_step = ms / args.steps
     pv_step = world * nf * H * W * V
     value = pv_step / (ms_step / 1e3) / 1e6
@@ -278,18 +276,22 @@ def main():
     # dominant kernel: the largest summed device time inside the timed region
     dom_name, (dom_ms, dom_n) = max(kt.items(), key=lambda kv: kv[1][0])
     per_launch_ms = dom_ms / max(1, dom_n)
-    alg_bytes = nf * H * W * (4 + V)           # 4 B read + V B written per pixel
+    launches_per_step = max(1, dom_n // args.steps)
+    alg_step = nf * H * W * (4 + V)            # 4 B read + V B written per pixel
+    alg_bytes = alg_step / launches_per_step   # per launch of the dominant kernel (frame chunk)
     peak, peak_src = load_peaks()
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
     tr = load_traffic()
     traffic = None
-    if tr and tr.get("kernel") == dom_name and tr.get("frames") == nf:
+    if tr and tr.get("kernel") == dom_name and abs(tr.get("alg_bytes_per_launch", -1) - alg_bytes) < 1:
         traffic = tr.get("bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
-                "kernel_ms_per_launch": per_launch_ms, "kernel_share_of_step": dom_ms / ms if ms else None,
+                "kernel_ms_per_launch": per_launch_ms, "launches_per_step": launches_per_step,
+                "kernel_share_of_step": dom_ms / ms if ms else None,
                 "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-                "kernels_ms": {k: v[0] / args.steps for k, v in kt.items() if v[1]}}
+                "step_frac": alg_step / (ms_step / 1e3) / 1e9 / peak,
+                "kernels_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]}}
 
     # ---------------- end to end: host buffers through the C ABI ----------------
     e2e_steps = args.e2e_steps or min(args.steps, 3)
@@ -300,12 +302,7 @@ def main():
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         det.detect_host_ptr(hbuf.data_ptr(), mbuf.data_ptr(), nf, stream.cuda_stream)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = shard.max_over_ranks((time.perf_counter() - t0) / e2e_steps, dev)
     e2e = {"value": pv_step / e2e_s / 1e6, "unit": "MPV/s", "h2d_bytes_per_step": int(frames.nbytes),
            "d2h_bytes_per_step": int(nf * V * H * W), "ms_per_step": e2e_s * 1e3,
            "note": "occ_detect_host: pinned H2D of D, detect, D2H of all masks, stream sync"}

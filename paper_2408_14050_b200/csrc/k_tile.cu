@@ -9,19 +9,25 @@
 //
 //  1. stage   D along the 32 lines into smem [pos][lane] with a halo of
 //             HALO >= max(h, reach) positions per side (coalesced row runs),
-//             candidate bits (Eqs. 1-2) per line as 32-bit words.
+//             candidate bits (Eqs. 1-2, from K0's per-pixel codes) per line
+//             as 32-bit words.
 //  2. per view:
-//     a. dcov(p) = U(p) - u_p, U(p) = pc(u_p + h) + h: a pair (p, q) shares
-//        one candidate's scan window (Eq. 4) iff u_q - u_p <= dcov(p).
+//     a. coverage dcov(p) = U(p) - u_p, U(p) = pc(u_p + h) + h: a pair (p, q)
+//        shares one candidate's scan window (Eq. 4) iff u_q - u_p <= dcov(p).
 //     b. near pairs (|dk| <= jstar-1): exact fp32 interval tests of
 //        delta = fl(v_q - v_p) (host-precomputed thresholds, S7).
 //     c. far pairs (dk <= -jstar, delta > t_disp implied): conservative
 //        suffix-max filter on B = s v - u along the sweep; survivors are
-//        resolved exactly (binary64 predicate), first at the offset that
-//        resolved the previous survivor of the line, else by a bounded scan.
+//        resolved exactly (binary64 predicate) at guessed offsets, the rest
+//        by a warp-cooperative exhaustive search.
 //  3. store   mask bytes through smem, row-contiguous streaming stores.
 // Views whose halo does not fit (huge disparity ranges) are computed by the
 // exact per-pixel routine (direct_pixel) inside the same CTA.
+//
+// The line geometry (major axis, slope num/den), the sweep direction, the
+// near-offset split of the default thresholds and the candidate-code width
+// are compile-time parameters for the families of |b| <= 2 arrays; other
+// cases run the same code with runtime values.
 #include "occ_device.cuh"
 
 namespace occ {
@@ -29,6 +35,7 @@ namespace occ {
 namespace {
 constexpr int TP = kTilePositions;     // output positions per tile
 constexpr int NT = 256;                // threads (8 warps)
+constexpr int NWARP = NT / 32;
 constexpr int HMAX = kTileHaloMax;     // max staged halo per side
 constexpr int NPMAX = TP + 2 * HMAX;   // staged positions
 constexpr int NB = NPMAX / 32;         // 32-position blocks
@@ -36,7 +43,7 @@ constexpr int VPITCH = 33;             // floats per staged position (32 lanes +
 constexpr int OPITCH = 36;             // bytes per output position (32 lanes + pad)
 constexpr int DC = TP + 2 * kMaxNear;  // dcov entries (outputs +- near reach)
 constexpr int16_t NONE_LO = -30000, NONE_HI = 30000;
-constexpr int kQueueCap = 128;          // survivor queue entries per warp
+constexpr int kQueueCap = 128;         // survivor queue entries per warp
 
 constexpr size_t OFF_V = 0;
 constexpr size_t OFF_CW = OFF_V + sizeof(float) * NPMAX * VPITCH;
@@ -46,36 +53,59 @@ constexpr size_t OFF_DCOV = OFF_NEXT + sizeof(int16_t) * 2 * NB * 32;
 constexpr size_t OFF_AGG = OFF_DCOV + sizeof(int16_t) * DC * 32;
 constexpr size_t OFF_OUT = OFF_AGG + sizeof(float) * 2 * NB * 32;
 constexpr size_t OFF_Q = OFF_OUT + (size_t)kGroupViews * TP * OPITCH;
-constexpr size_t SMEM = OFF_Q + sizeof(uint32_t) * (NT / 32) * kQueueCap;
+constexpr size_t SMEM = OFF_Q + sizeof(uint32_t) * NWARP * kQueueCap;
 }  // namespace
 
 size_t tile_smem_bytes() { return SMEM; }
 
-// floor(a / den) for den > 0, shifts for the common powers of two
-__device__ __forceinline__ int32_t fdiv(int32_t a, int32_t den) {
-    if (den == 1) return a;
-    if (den == 2) return a >> 1;
-    if (den == 4) return a >> 2;
-    if (den == 8) return a >> 3;
-    return floordiv(a, den);
+// ------------------------------------------------------------ geometry
+// Line family geometry: x-major lines l = y - floor(x num/den) (pos = x),
+// y-major lines l = x - floor(y num/den) (pos = y).  fl(a) = floor(a num/den).
+template <bool XM, int NUM, int DEN>
+struct GeoK {
+    __device__ __forceinline__ bool xm() const { return XM; }
+    __device__ __forceinline__ int32_t num() const { return NUM; }
+    __device__ __forceinline__ int32_t den() const { return DEN; }
+    __device__ __forceinline__ int32_t fl(int32_t a) const {
+        if (NUM == 0) return 0;
+        if (DEN == 1) return a * NUM;
+        if (DEN == 2) return (a * NUM) >> 1;
+        return floordiv(a * NUM, DEN);
+    }
+};
+struct GeoR {
+    bool xm_;
+    int32_t num_, den_;
+    __device__ __forceinline__ bool xm() const { return xm_; }
+    __device__ __forceinline__ int32_t num() const { return num_; }
+    __device__ __forceinline__ int32_t den() const { return den_; }
+    __device__ __forceinline__ int32_t fl(int32_t a) const { return floordiv(a * num_, den_); }
+};
+
+// floor(a / d) for d > 0
+__device__ __forceinline__ int32_t fdivg(int32_t a, int32_t d) {
+    if (d == 1) return a;
+    if (d == 2) return a >> 1;
+    return floordiv(a, d);
 }
-__device__ __forceinline__ int32_t cdiv(int32_t a, int32_t den) { return -fdiv(-a, den); }
 
 // x-range of image row y covered by lanes [0, 32) of an x-major tile:
-// l = y - l0 - floor(x num / den) in [0, 31].
-__device__ __forceinline__ void row_run(int32_t y, int32_t l0, int32_t num, int32_t den,
-                                        int32_t lo, int32_t hi, int32_t &xa, int32_t &xb) {
+// l = y - l0 - floor(x num / den) in [0, 31], clipped to [lo, hi].
+template <class G>
+__device__ __forceinline__ void row_run(const G &geo, int32_t y, int32_t l0, int32_t lo, int32_t hi,
+                                        int32_t &xa, int32_t &xb) {
     const int32_t A = y - l0 - 31, B = y - l0;
+    const int32_t num = geo.num(), den = geo.den();
     if (num == 0) {
         if (B < 0 || B > 31) { xa = 1; xb = 0; return; }
         xa = lo; xb = hi;
     } else if (num > 0) {
-        xa = cdiv(A * den, num);
-        xb = cdiv((B + 1) * den, num) - 1;
+        xa = -fdivg(-(A * den), num);
+        xb = -fdivg(-((B + 1) * den), num) - 1;
     } else {
         const int32_t n = -num;
-        xa = fdiv(-(B + 1) * den, n) + 1;
-        xb = fdiv(-A * den, n);
+        xa = fdivg(-(B + 1) * den, n) + 1;
+        xb = fdivg(-A * den, n);
     }
     xa = max(xa, lo);
     xb = min(xb, hi);
@@ -96,53 +126,67 @@ __device__ __forceinline__ int32_t nextcand(const uint32_t *cw, const int16_t *n
     return m ? 32 * w + __ffs(m) - 1 : (w + 1 < nb ? (int32_t)next[(w + 1) * 32 + lane] : (int32_t)NONE_HI);
 }
 
-// Fast sweep for the default split (near backward j = 1, 2; far j >= 3;
-// NFWD near forward offsets in {0, 1}): one thread = one line, 32 output
-// positions walked toward lower u with a register window, incremental
-// coverage state and the far filter's suffix maximum carried in a register.
-// No shared scratch beyond the staged data, no barrier.
-template <int NFWD>
+template <int CB>
+__device__ __forceinline__ uint32_t load_code(const unsigned char *Cb, int64_t idx) {
+    if (CB == 1) return __ldg(Cb + idx);
+    if (CB == 2) return __ldg(reinterpret_cast<const uint16_t *>(Cb) + idx);
+    return __ldg(reinterpret_cast<const uint32_t *>(Cb) + idx);
+}
+
+// ------------------------------------------------------------ fast sweep
+// Default split (near backward j = 1, 2; far j >= 3; NFWD near forward
+// offsets in {0, 1}): one thread = one line, 32 output positions walked
+// toward lower u (SG = direction of u along pos) with a register window,
+// incremental coverage state and the far filter's suffix maximum carried in
+// a register.  Survivors of the filter are queued (warp-aggregated) and
+// resolved afterwards one per lane.
+template <int SG, int NFWD>
 __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const uint32_t *cw,
                                            const int16_t *last, const int16_t *next,
                                            uint8_t *so, uint32_t *queue, int lane, int32_t b,
-                                           int32_t L0, int32_t TPe, int32_t NP32, int32_t NB32,
-                                           int32_t h, int32_t s, int32_t sg, float T, int32_t Jr,
+                                           int32_t L0, int32_t NP32, int32_t NB32, int32_t h,
+                                           int32_t s, float T, int32_t Jr,
                                            float blo0, float bhi0, float blo1, float bhi1,
                                            float flo0, float fhi0, float t_dist, float t_disp) {
     const float fs_ = (float)s;
-    const int32_t i0 = sg > 0 ? 32 * b + 31 : 32 * b;       // first (highest-u) position
-    float uf = (float)(sg * (i0 - L0));                     // u of the current position
-    // suffix max of B = s v - u over positions i0 + sg*[4, Jr]  (partners of any
+    const int32_t i0 = SG > 0 ? 32 * b + 31 : 32 * b;       // first (highest-u) position
+    const float *col = sv + lane;                           // this line's column
+    float uf = (float)(SG * (i0 - L0));                     // u of the current position
+    // suffix max of B = s v - u over positions i0 + SG*[4, Jr] (partners of any
     // position of the block lie within Jr; a superset keeps the filter sound);
     // SA = position where SX is attained (the witness used to guess partners)
     float SX = -INFINITY;
     int32_t SA = i0;
     {
-        const int32_t jend = min(Jr, sg > 0 ? NP32 - 1 - i0 : i0);
+        const int32_t jend = min(Jr, SG > 0 ? NP32 - 1 - i0 : i0);
+        const float *pq = col + (i0 + 4 * SG) * VPITCH;
+        float uq = uf + 4.0f;
         for (int32_t j = 4; j <= jend; ++j) {
-            const int32_t q = i0 + sg * j;
-            const float Bq = __fmaf_rn(fs_, sv[q * VPITCH + lane], -(uf + (float)j));
-            if (Bq > SX) { SX = Bq; SA = q; }
+            const float Bq = __fmaf_rn(fs_, *pq, -uq);
+            if (Bq > SX) { SX = Bq; SA = i0 + SG * j; }
+            pq += SG * VPITCH;
+            uq += 1.0f;
         }
     }
     // the staged range has >= 32 NaN-padded positions beyond every output block
-    float vp = sv[i0 * VPITCH + lane], v1 = sv[(i0 + sg) * VPITCH + lane];
-    float v2 = sv[(i0 + 2 * sg) * VPITCH + lane], v3 = sv[(i0 + 3 * sg) * VPITCH + lane];
-    // coverage state: sg > 0 tracks pc(x) for x = i + h (x decreasing),
-    // sg < 0 tracks nc(x) for x = i - h (x increasing)
-    int32_t cst = sg > 0 ? prevcand(cw, last, i0 + h, lane) : nextcand(cw, next, i0 - h, NB32, lane);
+    const float *pc = col + i0 * VPITCH;
+    float vp = pc[0], v1 = pc[SG * VPITCH], v2 = pc[2 * SG * VPITCH], v3 = pc[3 * SG * VPITCH];
+    // coverage state: SG > 0 tracks pc(x) for x = i + h (x decreasing),
+    // SG < 0 tracks nc(x) for x = i - h (x increasing)
+    int32_t cst = SG > 0 ? prevcand(cw, last, i0 + h, lane) : nextcand(cw, next, i0 - h, NB32, lane);
     auto dcov_of = [&](int32_t i) -> int32_t {
-        if (sg > 0) {
+        if (SG > 0) {
             const int32_t x = i + h;
             if (cst > x) cst = prevcand(cw, last, x, lane);
-            return (cst != NONE_LO && cst >= i - h) ? cst + h - i : -1;
+            return (cst >= i - h) ? cst + h - i : -1;         // NONE_LO < i - h
         }
         const int32_t x = i - h;
         if (cst < x) cst = nextcand(cw, next, x, NB32, lane);
-        return (cst != NONE_HI && cst <= i + h) ? i + h - cst : -1;
+        return (cst <= i + h) ? i + h - cst : -1;             // NONE_HI > i + h
     };
     int32_t dc = dcov_of(i0);
     int32_t qn = 0;                                         // warp-uniform queue length
+    const uint32_t lt = (1u << lane) - 1u;
     // exact resolution of queued survivors, one per lane, at guessed offsets;
     // misses go to a warp-cooperative exhaustive search (32 offsets per step)
     auto flush = [&]() {
@@ -154,14 +198,14 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
             if (e < qn) {
                 ent = queue[e];
                 const int32_t r = ent & 31, ln = (ent >> 5) & 31, jg = (ent >> 10) & 2047, jm = ent >> 21;
-                const int32_t i = i0 - sg * r;
+                const int32_t i = i0 - SG * r;
                 const float vq0 = sv[i * VPITCH + ln];
                 bool hit = false;
 #pragma unroll
                 for (int c = 0; c < 5; ++c) {
                     const int32_t j = jg + (c == 0 ? 0 : (c == 1 ? -1 : (c == 2 ? 1 : (c == 3 ? -2 : 2))));
                     if (!hit && j >= 3 && j <= jm &&
-                        pair_exact(sv[(i + sg * j) * VPITCH + ln], vq0, -j, s, t_dist, t_disp)) hit = true;
+                        pair_exact(sv[(i + SG * j) * VPITCH + ln], vq0, -j, s, t_dist, t_disp)) hit = true;
                 }
                 if (hit) so[(i - L0) * OPITCH + ln] = 1;
                 miss = !hit;
@@ -172,12 +216,12 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
                 pend &= pend - 1;
                 const uint32_t en = __shfl_sync(0xffffffffu, ent, src);
                 const int32_t r = en & 31, ln = (en >> 5) & 31, jm = en >> 21;
-                const int32_t i = i0 - sg * r;
+                const int32_t i = i0 - SG * r;
                 const float vs = sv[i * VPITCH + ln];
                 bool found = false;
                 for (int32_t j0 = 3; j0 <= jm && !found; j0 += 32) {
                     const int32_t j = j0 + lane;
-                    const bool ok = j <= jm && pair_exact(sv[(i + sg * j) * VPITCH + ln], vs, -j, s,
+                    const bool ok = j <= jm && pair_exact(sv[(i + SG * j) * VPITCH + ln], vs, -j, s,
                                                           t_dist, t_disp);
                     found = __ballot_sync(0xffffffffu, ok) != 0u;
                 }
@@ -187,34 +231,34 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
         __syncwarp();
         qn = 0;
     };
-    const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll 4
+    const int32_t lim0 = SG > 0 ? NP32 - 1 - i0 : i0;       // staged extent beyond i0
+#pragma unroll 2
     for (int r = 0; r < 32; ++r) {
-        const int32_t i = i0 - sg * r;
-        const float vf = sv[(i - sg) * VPITCH + lane];       // forward neighbour
-        {   // fold position i + 3 sg into the suffix max
+        const int32_t i = i0 - SG * r;
+        const float vf = pc[-SG * VPITCH];                   // forward neighbour
+        {   // fold position i + 3 SG into the suffix max
             const float B3 = __fmaf_rn(fs_, v3, -(uf + 3.0f));
-            if (B3 > SX) { SX = B3; SA = i + 3 * sg; }
+            if (B3 > SX) { SX = B3; SA = i + 3 * SG; }
         }
-        const int32_t dcn = dcov_of(i - sg);
+        const int32_t dcn = dcov_of(i - SG);
         const float d1 = __fsub_rn(v1, vp), d2 = __fsub_rn(v2, vp);
         bool m = ((d1 > blo0) & (d1 < bhi0) & (dc >= 1)) | ((d2 > blo1) & (d2 < bhi1) & (dc >= 2));
         if (NFWD) {
             const float df = __fsub_rn(vf, vp);
             m |= (df > flo0) & (df < fhi0) & (dcn >= 1);
         }
-        // far filter: a partner at j >= 3 needs some B_q > B_p - t_dist
-        const float Bp = __fmaf_rn(fs_, vp, -uf);
+        // far filter: a partner at j >= 3 needs some B_q > B_p - t_dist;
         // partners lie within the staged reach (>= min(2h, t_dist + s R))
-        const int32_t jmax = min(min(dc, 2 * h), sg > 0 ? NP32 - 1 - i : i);
+        const float Bp = __fmaf_rn(fs_, vp, -uf);
+        const int32_t jmax = min(min(dc, 2 * h), lim0 + r);
         const bool surv = !m && jmax >= 3 && SX > __fsub_rn(Bp, T);
         const unsigned bal = __ballot_sync(0xffffffffu, surv);
-        if (qn + __popc(bal) > kQueueCap) flush();
         if (bal) {
+            if (qn + __popc(bal) > kQueueCap) flush();
             if (surv) {
                 // guess: past the witness SA, B falls ~1 per step on a flat
                 // occluder, so the partner sits ~(SX - Bp) beyond it
-                const int32_t jg = sg * (SA - i) + min(max(0, __float2int_rn(__fsub_rn(SX, Bp))), 1023);
+                const int32_t jg = SG * (SA - i) + min(max(0, __float2int_rn(__fsub_rn(SX, Bp))), 1023);
                 queue[qn + __popc(bal & lt)] = (uint32_t)r | ((uint32_t)lane << 5) |
                                                ((uint32_t)min(jg, 2047) << 10) | ((uint32_t)jmax << 21);
             }
@@ -222,24 +266,38 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
         }
         so[(i - L0) * OPITCH + lane] = (uint8_t)m;
         v3 = v2; v2 = v1; v1 = vp; vp = vf;
+        pc -= SG * VPITCH;
         dc = dcn;
         uf -= 1.0f;
     }
     flush();
 }
 
+// ------------------------------------------------------------ tile body
 struct ViewRegs {
     int32_t s, sg, h, jstar, nback, nfwd, vid, jr;
     float T;              // far-filter margin t_dist + eps
     bool staged;
 };
 
-__global__ void __launch_bounds__(NT, 2)
-k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__restrict__ tiles,
-       const GroupDesc *__restrict__ groups, const ViewDesc *__restrict__ views, int32_t nviews,
-       const FamilyDesc *__restrict__ fams, const FrameStats *__restrict__ st, Params p,
-       uint8_t *__restrict__ masks, const void *__restrict__ codes, int32_t code_bytes) {
-    extern __shared__ __align__(16) unsigned char smem[];
+struct TileArgs {
+    const float *D;
+    int32_t H, W;
+    const TileDesc *tiles;
+    const GroupDesc *groups;
+    const ViewDesc *views;
+    int32_t nviews;
+    const FamilyDesc *fams;
+    const FrameStats *st;
+    Params p;
+    uint8_t *masks;
+    const void *codes;
+};
+
+template <class G, int CB>
+__device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const TileDesc &td,
+                                          const GroupDesc &gd, const FamilyDesc &fd,
+                                          unsigned char *smem) {
     uint32_t *squeue = reinterpret_cast<uint32_t *>(smem + OFF_Q) + (threadIdx.x >> 5) * kQueueCap;
     float *sv = reinterpret_cast<float *>(smem + OFF_V);
     uint32_t *scw = reinterpret_cast<uint32_t *>(smem + OFF_CW);
@@ -248,22 +306,16 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
     int16_t *sdcov = reinterpret_cast<int16_t *>(smem + OFF_DCOV);
     float *sagg = reinterpret_cast<float *>(smem + OFF_AGG);
     uint8_t *sout = smem + OFF_OUT;
+    const Params &p = a.p;
+    const int32_t H = a.H, W = a.W;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const TileDesc td = tiles[blockIdx.x];
     const int f = blockIdx.y;
-    const GroupDesc gd = groups[td.group];
-    const FamilyDesc fd = fams[gd.fam];
-    const FrameStats fs = st[f];
+    const FrameStats fs = a.st[f];
     const int64_t HW = (int64_t)H * W;
-    const float *Df = D + (int64_t)f * HW;
+    const float *Df = a.D + (int64_t)f * HW;
     const int32_t l0 = td.l0, P0 = td.p0, P1 = td.p1, TPe = P1 - P0;
-    const int32_t num = fd.num, den = fd.den;
-    // floor(a / den): a shift for the power-of-two slopes of all |b| <= 2 arrays
-    const bool dpow = (den & (den - 1)) == 0;
-    const int32_t dsh = __ffs(den) - 1;
-    auto FD = [&](int32_t a) -> int32_t { return dpow ? (a >> dsh) : floordiv(a, den); };
-    const bool xm = fd.xmajor != 0;
+    const bool xm = geo.xm();
 
     // ------------------------------------------------ per-view parameters
     const float R = frame_range(fs);
@@ -275,7 +327,7 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
     for (int g = 0; g < kGroupViews; ++g) {
         vr[g].staged = false;
         if (g >= gd.nv) continue;
-        const ViewDesc &vd = views[gd.view[g]];
+        const ViewDesc &vd = a.views[gd.view[g]];
         vr[g].vid = gd.view[g];
         vr[g].s = vd.s; vr[g].sg = vd.sg; vr[g].jstar = vd.jstar;
         vr[g].nback = vd.nback; vr[g].nfwd = vd.nfwd;
@@ -311,45 +363,72 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
         const int32_t lo_i = L0 - halo, hi_i = L0 + TPe + halo;
         // candidate bits of this family from K0's per-pixel codes (Eqs. 1-2)
         const int cshift = 2 * gd.fam;
-        const unsigned char *Cb = reinterpret_cast<const unsigned char *>(codes) +
-                                  (int64_t)f * HW * code_bytes;
-        auto cand_of = [&](int64_t idx) -> uint32_t {
-            uint32_t c;
-            if (code_bytes == 1) c = __ldg(Cb + idx);
-            else if (code_bytes == 2) c = __ldg(reinterpret_cast<const uint16_t *>(Cb) + idx);
-            else c = __ldg(reinterpret_cast<const uint32_t *>(Cb) + idx);
-            return (c >> cshift) & 3u;
-        };
+        const unsigned char *Cb = reinterpret_cast<const unsigned char *>(a.codes) + (int64_t)f * HW * CB;
         if (!xm) {
-            // y-major: pos = y, lane -> x = l0 + lane + floor(y num / den): rows are positions
-            for (int i = lo_i + warp; i < hi_i; i += NT / 32) {
-                const int32_t y = base + i;
-                if (y < 0 || y >= H) continue;
-                const int32_t x = l0 + lane + FD(y * num);
-                if (x < 0 || x >= W) continue;
-                const int64_t idx = (int64_t)y * W + x;
-                sv[i * VPITCH + lane] = __ldg(Df + idx);
-                const uint32_t c = cand_of(idx);
-                if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
-                if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
+            // y-major: pos = y, lane -> x = l0 + lane + fl(y).  A warp owns whole
+            // 32-position blocks, so each lane builds its line's words in registers.
+            for (int blk = (lo_i >> 5) + warp; blk <= ((hi_i - 1) >> 5); blk += NWARP) {
+                uint32_t w0 = 0u, w1 = 0u;
+                for (int r = 0; r < 32; ++r) {
+                    const int32_t i = 32 * blk + r;
+                    if (i < lo_i || i >= hi_i) continue;
+                    const int32_t y = base + i;
+                    if (y < 0 || y >= H) continue;
+                    const int32_t x = l0 + lane + geo.fl(y);
+                    if (x < 0 || x >= W) continue;
+                    const int64_t idx = (int64_t)y * W + x;
+                    sv[i * VPITCH + lane] = __ldg(Df + idx);
+                    const uint32_t c = load_code<CB>(Cb, idx) >> cshift;
+                    w0 |= (c & 1u) << r;
+                    w1 |= ((c >> 1) & 1u) << r;
+                }
+                scw[(0 * NB + blk) * 32 + lane] = w0;
+                scw[(1 * NB + blk) * 32 + lane] = w1;
             }
         } else {
-            // x-major: pos = x, lane = y - l0 - floor(x num / den); walk image rows
+            // x-major: pos = x, lane = y - l0 - fl(x); walk image rows
             const int32_t xs = max(base + lo_i, 0), xe = min(base + hi_i, W) - 1;
             if (xs <= xe) {
-                const int32_t fa = FD(xs * num), fb = FD(xe * num);
+                const int32_t fa = geo.fl(xs), fb = geo.fl(xe);
                 const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
-                for (int32_t y = ylo + warp; y <= yhi; y += NT / 32) {
+                for (int32_t y = ylo + warp; y <= yhi; y += NWARP) {
                     int32_t xa, xb;
-                    row_run(y, l0, num, den, xs, xe, xa, xb);
-                    for (int32_t x = xa + lane; x <= xb; x += 32) {
-                        const int32_t l = y - l0 - FD(x * num);
-                        const int32_t i = x - base;
-                        const int64_t idx = (int64_t)y * W + x;
-                        sv[i * VPITCH + l] = __ldg(Df + idx);
-                        const uint32_t c = cand_of(idx);
-                        if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
-                        if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
+                    row_run(geo, y, l0, xs, xe, xa, xb);
+                    const float *Drow = Df + (int64_t)y * W;
+                    if (geo.num() == 0) {
+                        // rows: the whole run is one line owned by this warp ->
+                        // ballot the candidate bits into its words (no atomics)
+                        const int32_t l = y - l0;
+                        for (int32_t x0 = xa; x0 <= xb; x0 += 32) {
+                            const int32_t x = x0 + lane;
+                            const bool ok = x <= xb;
+                            const int32_t i = x - base;
+                            uint32_t c = 0u;
+                            if (ok) {
+                                sv[i * VPITCH + l] = __ldg(Drow + x);
+                                c = load_code<CB>(Cb, (int64_t)y * W + x) >> cshift;
+                            }
+                            const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u);
+                            const uint32_t b1 = __ballot_sync(0xffffffffu, (c >> 1) & 1u);
+                            if (lane == 0 && (b0 | b1)) {
+                                const int32_t i0 = x0 - base, sh = i0 & 31, w = i0 >> 5;
+                                scw[(0 * NB + w) * 32 + l] |= b0 << sh;
+                                scw[(1 * NB + w) * 32 + l] |= b1 << sh;
+                                if (sh) {
+                                    scw[(0 * NB + w + 1) * 32 + l] |= b0 >> (32 - sh);
+                                    scw[(1 * NB + w + 1) * 32 + l] |= b1 >> (32 - sh);
+                                }
+                            }
+                        }
+                    } else {
+                        for (int32_t x = xa + lane; x <= xb; x += 32) {
+                            const int32_t l = y - l0 - geo.fl(x);
+                            const int32_t i = x - base;
+                            sv[i * VPITCH + l] = __ldg(Drow + x);
+                            const uint32_t c = load_code<CB>(Cb, (int64_t)y * W + x) >> cshift;
+                            if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
+                            if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
+                        }
                     }
                 }
             }
@@ -384,12 +463,12 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
             continue;
         }
         if (!cv.staged) {           // halo too large: exact per-pixel routine
-            const ViewDesc vd = views[cv.vid];
+            const ViewDesc vd = a.views[cv.vid];
             for (int k = tid; k < TPe * 32; k += NT) {
                 const int32_t pos = P0 + (k >> 5), l = k & 31, ln = l0 + l;
                 int32_t x, y;
-                if (xm) { x = pos; y = ln + fdiv(pos * num, den); }
-                else { y = pos; x = ln + fdiv(pos * num, den); }
+                if (xm) { x = pos; y = ln + geo.fl(pos); }
+                else { y = pos; x = ln + geo.fl(pos); }
                 bool m = false;
                 if (x >= 0 && x < W && y >= 0 && y < H)
                     m = direct_pixel<false>(Df, H, W, vd, fd, p, cv.h, x, y);
@@ -404,7 +483,7 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
         // exact fp32 interval bounds of the near offsets (host-precomputed, S7)
         float blo[kMaxNear], bhi[kMaxNear], flo[kMaxNear], fhi[kMaxNear];
         {
-            const ViewDesc &vd = views[cv.vid];
+            const ViewDesc &vd = a.views[cv.vid];
 #pragma unroll
             for (int j = 0; j < kMaxNear; ++j) {
                 blo[j] = vd.back_lo[j]; bhi[j] = vd.back_hi[j];
@@ -414,45 +493,47 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
         if (cv.nback == 2 && cv.jstar == 3 && cv.nfwd <= 1) {
             // default thresholds: barrier-free register sweep
             const int32_t nob = (TPe + 31) >> 5;
-            for (int ob = warp; ob < nob; ob += NT / 32) {
+            const uint32_t *cwd = scw + d * NB * 32;
+            const int16_t *ld = slast + d * NB * 32, *nd = snext + d * NB * 32;
+            for (int ob = warp; ob < nob; ob += NWARP) {
                 const int32_t b = (L0 >> 5) + ob;
-                if (cv.nfwd)
-                    sweep_fast<1>(sv, scw + d * NB * 32, slast + d * NB * 32, snext + d * NB * 32, so,
-                                  squeue, lane, b, L0, TPe, NP32, NB32, h, s, sg, T, cv.jr, blo[0], bhi[0],
-                                  blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
-                else
-                    sweep_fast<0>(sv, scw + d * NB * 32, slast + d * NB * 32, snext + d * NB * 32, so,
-                                  squeue, lane, b, L0, TPe, NP32, NB32, h, s, sg, T, cv.jr, blo[0], bhi[0],
-                                  blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
+                if (sg > 0) {
+                    if (cv.nfwd)
+                        sweep_fast<1, 1>(sv, cwd, ld, nd, so, squeue, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                                         blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
+                    else
+                        sweep_fast<1, 0>(sv, cwd, ld, nd, so, squeue, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                                         blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
+                } else {
+                    if (cv.nfwd)
+                        sweep_fast<-1, 1>(sv, cwd, ld, nd, so, squeue, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                                          blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
+                    else
+                        sweep_fast<-1, 0>(sv, cwd, ld, nd, so, squeue, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                                          blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
+                }
             }
             continue;
         }
+        // ---- generic thresholds: dcov table, block aggregates, per-position sweep
         // a. dcov for local positions [L0 - kMaxNear, L0 + TPe + kMaxNear)
         const int32_t D0 = L0 - kMaxNear;
-        for (int k = warp; k < TPe + 2 * kMaxNear; k += NT / 32) {
+        for (int k = warp; k < TPe + 2 * kMaxNear; k += NWARP) {
             const int32_t i = D0 + k;
             int32_t dc = -1;
             if (i >= 0 && i < NP32) {
                 if (sg > 0) {
-                    const int32_t xq = min(i + h, NP32 - 1);
-                    const int32_t w = xq >> 5;
-                    const uint32_t m = scw[(d * NB + w) * 32 + lane] & (0xffffffffu >> (31 - (xq & 31)));
-                    const int32_t pc = m ? 32 * w + 31 - __clz(m)
-                                         : (w > 0 ? slast[(d * NB + w - 1) * 32 + lane] : NONE_LO);
-                    if (pc != NONE_LO && pc >= i - h) dc = pc + h - i;
+                    const int32_t pcv = prevcand(scw + d * NB * 32, slast + d * NB * 32, min(i + h, NP32 - 1), lane);
+                    if (pcv != NONE_LO && pcv >= i - h) dc = pcv + h - i;
                 } else {
-                    const int32_t xq = max(i - h, 0);
-                    const int32_t w = xq >> 5;
-                    const uint32_t m = scw[(d * NB + w) * 32 + lane] & (0xffffffffu << (xq & 31));
-                    const int32_t nc = m ? 32 * w + __ffs(m) - 1
-                                         : (w + 1 < NB32 ? snext[(d * NB + w + 1) * 32 + lane] : NONE_HI);
-                    if (nc != NONE_HI && nc <= i + h) dc = i + h - nc;
+                    const int32_t ncv = nextcand(scw + d * NB * 32, snext + d * NB * 32, max(i - h, 0), NB32, lane);
+                    if (ncv != NONE_HI && ncv <= i + h) dc = i + h - ncv;
                 }
             }
             sdcov[k * 32 + lane] = (int16_t)dc;
         }
         // b. block aggregates of B = s v - u for the far filter (u = sg (i - L0))
-        for (int b = warp; b < NB32; b += NT / 32) {
+        for (int b = warp; b < NB32; b += NWARP) {
             float A = -INFINITY, Ap = -INFINITY;
             for (int r = 0; r < 32; ++r) {
                 const int32_t i = 32 * b + r;
@@ -467,7 +548,7 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
         __syncthreads();
         // c. sweep: warp w owns output block L0/32 + w, moving toward lower u
         const int32_t nob = (TPe + 31) >> 5;
-        for (int ob = warp; ob < nob; ob += NT / 32) {
+        for (int ob = warp; ob < nob; ob += NWARP) {
             const int32_t b = (L0 >> 5) + ob;
             float SX = -INFINITY;
             if (sg > 0) {
@@ -544,8 +625,8 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
 #pragma unroll 1
     for (int g = 0; g < gd.nv; ++g) {
         const uint8_t *so = sout + (size_t)g * TP * OPITCH;
-        uint8_t *Mv = masks + ((int64_t)f * nviews + gd.view[g]) * HW;
-        const bool al4 = ((W & 3) == 0) && ((l0 & 3) == 0) && ((P0 & 3) == 0) && num == 0;
+        uint8_t *Mv = a.masks + ((int64_t)f * a.nviews + gd.view[g]) * HW;
+        const bool al4 = ((W & 3) == 0) && ((l0 & 3) == 0) && ((P0 & 3) == 0) && geo.num() == 0;
         if (!xm && al4) {
             // columns: each output row is 32 contiguous bytes -> 8 x 4-byte stores
             for (int k = warp * 4 + (lane >> 3); k < TPe; k += NT / 8) {
@@ -580,26 +661,51 @@ k_tile(const float *__restrict__ D, int32_t H, int32_t W, const TileDesc *__rest
             continue;
         }
         if (!xm) {
-            for (int k = warp; k < TPe; k += NT / 32) {
+            for (int k = warp; k < TPe; k += NWARP) {
                 const int32_t y = P0 + k;
                 if (y < 0 || y >= H) continue;
-                const int32_t x = l0 + lane + FD(y * num);
+                const int32_t x = l0 + lane + geo.fl(y);
                 if (x < 0 || x >= W) continue;
                 __stcs(Mv + (int64_t)y * W + x, so[k * OPITCH + lane]);
             }
         } else {
             const int32_t xs = max(P0, 0), xe = min(P1, W) - 1;
             if (xs > xe) continue;
-            const int32_t fa = FD(xs * num), fb = FD(xe * num);
+            const int32_t fa = geo.fl(xs), fb = geo.fl(xe);
             const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
-            for (int32_t y = ylo + warp; y <= yhi; y += NT / 32) {
+            for (int32_t y = ylo + warp; y <= yhi; y += NWARP) {
                 int32_t xa, xb;
-                row_run(y, l0, num, den, xs, xe, xa, xb);
+                row_run(geo, y, l0, xs, xe, xa, xb);
                 for (int32_t x = xa + lane; x <= xb; x += 32) {
-                    const int32_t l = y - l0 - FD(x * num);
+                    const int32_t l = y - l0 - geo.fl(x);
                     __stcs(Mv + (int64_t)y * W + x, so[(x - P0) * OPITCH + l]);
                 }
             }
+        }
+    }
+}
+
+// Family kinds with compile-time geometry (FamilyDesc::kind, set by the host):
+// 0 rows, 1 columns, 2 diagonal, 3 anti-diagonal, 4/5 x-major knight +-1/2,
+// 6/7 y-major knight +-1/2, 8 any other slope (runtime geometry).
+template <int CB>
+__global__ void __launch_bounds__(NT, 2) k_tile(TileArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const TileDesc td = a.tiles[blockIdx.x];
+    const GroupDesc gd = a.groups[td.group];
+    const FamilyDesc fd = a.fams[gd.fam];
+    switch (fd.kind) {
+        case 0: tile_body<GeoK<true, 0, 1>, CB>(a, GeoK<true, 0, 1>(), td, gd, fd, smem); break;
+        case 1: tile_body<GeoK<false, 0, 1>, CB>(a, GeoK<false, 0, 1>(), td, gd, fd, smem); break;
+        case 2: tile_body<GeoK<true, 1, 1>, CB>(a, GeoK<true, 1, 1>(), td, gd, fd, smem); break;
+        case 3: tile_body<GeoK<true, -1, 1>, CB>(a, GeoK<true, -1, 1>(), td, gd, fd, smem); break;
+        case 4: tile_body<GeoK<true, 1, 2>, CB>(a, GeoK<true, 1, 2>(), td, gd, fd, smem); break;
+        case 5: tile_body<GeoK<true, -1, 2>, CB>(a, GeoK<true, -1, 2>(), td, gd, fd, smem); break;
+        case 6: tile_body<GeoK<false, 1, 2>, CB>(a, GeoK<false, 1, 2>(), td, gd, fd, smem); break;
+        case 7: tile_body<GeoK<false, -1, 2>, CB>(a, GeoK<false, -1, 2>(), td, gd, fd, smem); break;
+        default: {
+            GeoR g{fd.xmajor != 0, fd.num, fd.den};
+            tile_body<GeoR, CB>(a, g, td, gd, fd, smem);
         }
     }
 }
@@ -609,11 +715,22 @@ cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
                         const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
                         const FrameStats *st, const Params &p, uint8_t *masks, const void *codes,
                         int32_t code_bytes, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    if (e != cudaSuccess) return e;
+    TileArgs a{D, H, W, tiles, groups, views, nviews, fams, st, p, masks, codes};
     dim3 grid((unsigned)ntiles, (unsigned)batch);
-    k_tile<<<grid, NT, SMEM, s>>>(D, H, W, tiles, groups, views, nviews, fams, st, p, masks, codes,
-                                  code_bytes);
+    cudaError_t e;
+    if (code_bytes == 1) {
+        e = cudaFuncSetAttribute(k_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        if (e != cudaSuccess) return e;
+        k_tile<1><<<grid, NT, SMEM, s>>>(a);
+    } else if (code_bytes == 2) {
+        e = cudaFuncSetAttribute(k_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        if (e != cudaSuccess) return e;
+        k_tile<2><<<grid, NT, SMEM, s>>>(a);
+    } else {
+        e = cudaFuncSetAttribute(k_tile<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        if (e != cudaSuccess) return e;
+        k_tile<4><<<grid, NT, SMEM, s>>>(a);
+    }
     return cudaGetLastError();
 }
 

@@ -266,6 +266,12 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
             FamilyDesc fd{};
             fd.b0x = b0x; fd.b0y = b0y; fd.xmajor = vd.xmajor; fd.num = vd.num; fd.den = vd.den;
             fd.nviews = 0;
+            // k_tile's compile-time geometry variants (rows, columns, diagonals, knights)
+            const int32_t X = fd.xmajor, n = fd.num, dd = fd.den;
+            fd.kind = (X && n == 0) ? 0 : (!X && n == 0) ? 1 : (X && n == 1 && dd == 1) ? 2
+                    : (X && n == -1 && dd == 1) ? 3 : (X && n == 1 && dd == 2) ? 4
+                    : (X && n == -1 && dd == 2) ? 5 : (!X && n == 1 && dd == 2) ? 6
+                    : (!X && n == -1 && dd == 2) ? 7 : 8;
             c->fams.push_back(fd);
             fam = (int32_t)c->fams.size() - 1;
         }

@@ -36,6 +36,7 @@ struct ViewDesc {
 struct FamilyDesc {
     int32_t b0x, b0y;   // reduced base direction, major component > 0
     int32_t xmajor, num, den;
+    int32_t kind;       // compile-time geometry variant of k_tile (8 = runtime)
     int32_t nviews;
     int32_t view[kMaxViews];   // indices into ViewDesc[]
 };
