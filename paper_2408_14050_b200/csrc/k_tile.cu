@@ -273,6 +273,184 @@ __device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const u
     flush();
 }
 
+// ------------------------------------------------------------ bit-sliced sweep
+// Smallest float > x (x finite): the exact rewrite x > a <=> x >= nextup(a).
+__device__ __forceinline__ float nextup(float a) {
+    const int32_t b = __float_as_int(a);
+    if (a == 0.0f) return __int_as_float(1);                  // +-0 -> smallest denormal
+    return __int_as_float(a > 0.0f ? b + 1 : b - 1);
+}
+// Appends the sign bit of a float / int to a word: (w << 1) | sign(x).
+// The sign of fl(x - c) is the exact sign of x - c, so fl(x - nextup(a)) < 0
+// <=> !(x > a) and fl(x - b) < 0 <=> x < b; a NaN operand gives a positive
+// canonical NaN (sign 0) and therefore fails every "x < b" test.
+__device__ __forceinline__ uint32_t pushf(uint32_t w, float x) {
+    return __funnelshift_l(__float_as_uint(x), w, 1);
+}
+__device__ __forceinline__ uint32_t pushi(uint32_t w, int32_t x) {
+    return __funnelshift_l((uint32_t)x, w, 1);
+}
+
+// Default split (near backward j = 1, 2; far j >= 3; NFWD near forward
+// offsets in {0, 1}).  One thread = one line, 32 positions of block b walked
+// toward lower u.  Every per-position test is reduced to a sign bit and
+// packed into 32-bit words (one bit per position); the Eq. 5 interval tests,
+// window coverage and the far-filter verdict are then combined word-wise.
+// Far survivors are resolved exactly afterwards: at the offset of the line's
+// previous hit, or (first survivor of the line) at the offset guessed from
+// the suffix-max witness, else by a warp-cooperative exhaustive search.
+template <int SG, int NFWD>
+__device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const uint32_t *cw,
+                                           const int16_t *last, const int16_t *next,
+                                           uint8_t *so, int lane, int32_t b, int32_t L0,
+                                           int32_t NP32, int32_t NB32, int32_t h, int32_t s,
+                                           float T, int32_t Jr, float blo0, float bhi0,
+                                           float blo1, float bhi1, float flo0, float fhi0,
+                                           float t_dist, float t_disp) {
+    const float fs_ = (float)s;
+    const float a1 = nextup(blo0), a2 = nextup(blo1), af = nextup(flo0);
+    const int32_t i0 = SG > 0 ? 32 * b + 31 : 32 * b;       // first (highest-u) position
+    const float *col = sv + lane;
+    float uf = (float)(SG * (i0 - L0));
+    // suffix max of B = s v - u over i0 + SG*[4, Jr] and its witness SA
+    float SX = -INFINITY;
+    int32_t SA = i0;
+    {
+        const int32_t jend = min(Jr, SG > 0 ? NP32 - 1 - i0 : i0);
+        const float *pq = col + (i0 + 4 * SG) * VPITCH;
+        float uq = uf + 4.0f;
+        for (int32_t j = 4; j <= jend; ++j) {
+            const float Bq = __fmaf_rn(fs_, *pq, -uq);
+            if (Bq > SX) { SX = Bq; SA = i0 + SG * j; }
+            pq += SG * VPITCH;
+            uq += 1.0f;
+        }
+    }
+    const float *pc = col + i0 * VPITCH;
+    float vp = pc[0], v1 = pc[SG * VPITCH], v2 = pc[2 * SG * VPITCH], v3 = pc[3 * SG * VPITCH];
+    int32_t cst = SG > 0 ? prevcand(cw, last, i0 + h, lane) : nextcand(cw, next, i0 - h, NB32, lane);
+    auto dcov_of = [&](int32_t i) -> int32_t {
+        if (SG > 0) {
+            const int32_t x = i + h;
+            if (cst > x) cst = prevcand(cw, last, x, lane);
+            return (cst >= i - h) ? cst + h - i : -1;
+        }
+        const int32_t x = i - h;
+        if (cst < x) cst = nextcand(cw, next, x, NB32, lane);
+        return (cst <= i + h) ? i + h - cst : -1;
+    };
+    int32_t dc = dcov_of(i0);
+    uint32_t G1 = 0, L1 = 0, G2 = 0, L2 = 0, GF = 0, LF = 0;   // interval sign words
+    uint32_t C1 = 0, C2 = 0, C3 = 0, CF = 0, FR = 0;           // coverage / far words
+    bool got = false;                                          // first raw far survivor seen
+    int32_t sa0 = 0;
+    float sx0 = 0.0f;
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+        const int32_t i = i0 - SG * r;
+        const float vf = pc[-SG * VPITCH];                       // forward neighbour
+        {   // fold position i + 3 SG into the suffix max
+            const float B3 = __fmaf_rn(fs_, v3, -(uf + 3.0f));
+            if (B3 > SX) { SX = B3; SA = i + 3 * SG; }
+        }
+        const int32_t dcn = dcov_of(i - SG);
+        const float d1 = __fsub_rn(v1, vp), d2 = __fsub_rn(v2, vp);
+        G1 = pushf(G1, __fsub_rn(d1, a1)); L1 = pushf(L1, __fsub_rn(d1, bhi0));
+        G2 = pushf(G2, __fsub_rn(d2, a2)); L2 = pushf(L2, __fsub_rn(d2, bhi1));
+        if (NFWD) {
+            const float df = __fsub_rn(vf, vp);
+            GF = pushf(GF, __fsub_rn(df, af)); LF = pushf(LF, __fsub_rn(df, fhi0));
+            CF = pushi(CF, -dcn);                                // dc(i - SG) >= 1
+        }
+        C1 = pushi(C1, -dc);                                     // dc >= 1
+        C2 = pushi(C2, 1 - dc);                                  // dc >= 2
+        C3 = pushi(C3, 2 - dc);                                  // dc >= 3
+        // far filter: survivor <=> SX > fl(B_p - T)
+        const float fr = __fsub_rn(__fsub_rn(__fmaf_rn(fs_, vp, -uf), T), SX);
+        FR = pushf(FR, fr);
+        if (!got && fr < 0.0f) { got = true; sa0 = SA; sx0 = SX; }
+        v3 = v2; v2 = v1; v1 = vp; vp = vf;
+        pc -= SG * VPITCH;
+        dc = dcn;
+        uf -= 1.0f;
+    }
+    if (SG < 0) {   // packed first-processed-highest: restore bit r <-> position 32b + r
+        G1 = __brev(G1); L1 = __brev(L1); G2 = __brev(G2); L2 = __brev(L2);
+        GF = __brev(GF); LF = __brev(LF); C1 = __brev(C1); C2 = __brev(C2);
+        C3 = __brev(C3); CF = __brev(CF); FR = __brev(FR);
+    }
+    uint32_t m = (~G1 & L1 & C1) | (~G2 & L2 & C2);
+    if (NFWD) m |= ~GF & LF & CF;
+    uint32_t sv_bits = (2 * h >= 3) ? (FR & C3 & ~m) : 0u;      // far survivors
+    // exact resolution, u-descending order; jl = offset of the line's last hit
+    int32_t jl = 0;
+    uint32_t miss = 0;
+    bool first = true;
+    while (sv_bits) {
+        const int32_t rr = SG > 0 ? 31 - __clz(sv_bits) : __ffs(sv_bits) - 1;
+        sv_bits &= ~(1u << rr);
+        const int32_t i = 32 * b + rr;
+        const float vq0 = sv[i * VPITCH + lane];
+        int32_t dci;
+        if (SG > 0) {
+            const int32_t pcv = prevcand(cw, last, i + h, lane);
+            dci = pcv >= i - h ? pcv + h - i : -1;
+        } else {
+            const int32_t ncv = nextcand(cw, next, i - h, NB32, lane);
+            dci = ncv <= i + h ? i + h - ncv : -1;
+        }
+        const int32_t jm = min(min(dci, 2 * h), SG > 0 ? NP32 - 1 - i : i);
+        int32_t jg = jl;
+        if (first) {
+            const float Bp = __fmaf_rn(fs_, vq0, -(float)(SG * (i - L0)));
+            jg = SG * (sa0 - i) + min(max(0, __float2int_rn(__fsub_rn(sx0, Bp))), 1023);
+            first = false;
+        }
+        bool hit = false;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            const int32_t j = jg + (c == 0 ? 0 : (c == 1 ? -1 : (c == 2 ? 1 : (c == 3 ? -2 : 2))));
+            if (!hit && j >= 3 && j <= jm &&
+                pair_exact(sv[(i + SG * j) * VPITCH + lane], vq0, -j, s, t_dist, t_disp)) {
+                hit = true; jl = j;
+            }
+        }
+        if (hit) m |= 1u << rr; else miss |= 1u << rr;
+    }
+    // misses: warp-cooperative exhaustive search over j in [3, jm], 32 at a time
+    unsigned pend = __ballot_sync(0xffffffffu, miss != 0u);
+    while (pend) {
+        const int src = __ffs(pend) - 1;
+        const uint32_t mw = __shfl_sync(0xffffffffu, miss, src);
+        const int32_t rr = __ffs(mw) - 1;
+        if (lane == src) miss &= ~(1u << rr);
+        pend = __ballot_sync(0xffffffffu, miss != 0u);
+        const int32_t i = 32 * b + rr;
+        const float vs = sv[i * VPITCH + src];
+        int32_t dci;
+        if (SG > 0) {
+            const int32_t pcv = prevcand(cw, last, i + h, src);
+            dci = pcv >= i - h ? pcv + h - i : -1;
+        } else {
+            const int32_t ncv = nextcand(cw, next, i - h, NB32, src);
+            dci = ncv <= i + h ? i + h - ncv : -1;
+        }
+        const int32_t jm = min(min(dci, 2 * h), SG > 0 ? NP32 - 1 - i : i);
+        bool found = false;
+        for (int32_t j0 = 3; j0 <= jm && !found; j0 += 32) {
+            const int32_t j = j0 + lane;
+            const bool ok = j <= jm && pair_exact(sv[(i + SG * j) * VPITCH + src], vs, -j, s,
+                                                  t_dist, t_disp);
+            found = __ballot_sync(0xffffffffu, ok) != 0u;
+        }
+        if (found && lane == src) m |= 1u << rr;
+    }
+    // bytes of the block for the store phase
+    uint8_t *ob = so + (32 * b - L0) * OPITCH + lane;
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) ob[r * OPITCH] = (uint8_t)((m >> r) & 1u);
+}
+
 // ------------------------------------------------------------ tile body
 struct ViewRegs {
     int32_t s, sg, h, jstar, nback, nfwd, vid, jr;
@@ -499,17 +677,17 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                 const int32_t b = (L0 >> 5) + ob;
                 if (sg > 0) {
                     if (cv.nfwd)
-                        sweep_fast<1, 1>(sv, cwd, ld, nd, so, squeue, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                        sweep_bits<1, 1>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
                                          blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                     else
-                        sweep_fast<1, 0>(sv, cwd, ld, nd, so, squeue, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                        sweep_bits<1, 0>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
                                          blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                 } else {
                     if (cv.nfwd)
-                        sweep_fast<-1, 1>(sv, cwd, ld, nd, so, squeue, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                        sweep_bits<-1, 1>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
                                           blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                     else
-                        sweep_fast<-1, 0>(sv, cwd, ld, nd, so, squeue, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                        sweep_bits<-1, 0>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
                                           blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                 }
             }
