@@ -39,11 +39,10 @@ constexpr int NWARP = NT / 32;
 constexpr int HMAX = kTileHaloMax;     // max staged halo per side
 constexpr int NPMAX = TP + 2 * HMAX;   // staged positions
 constexpr int NB = NPMAX / 32;         // 32-position blocks
-constexpr int VPITCH = 33;             // floats per staged position (32 lanes + pad)
+constexpr int VPITCH = 34;             // max floats per staged position (32 lanes + pad)
 constexpr int OPITCH = 36;             // bytes per output position (32 lanes + pad)
 constexpr int DC = TP + 2 * kMaxNear;  // dcov entries (outputs +- near reach)
 constexpr int16_t NONE_LO = -30000, NONE_HI = 30000;
-constexpr int kQueueCap = 128;         // survivor queue entries per warp
 
 constexpr size_t OFF_V = 0;
 constexpr size_t OFF_CW = OFF_V + sizeof(float) * NPMAX * VPITCH;
@@ -52,8 +51,7 @@ constexpr size_t OFF_NEXT = OFF_LAST + sizeof(int16_t) * 2 * NB * 32;
 constexpr size_t OFF_DCOV = OFF_NEXT + sizeof(int16_t) * 2 * NB * 32;
 constexpr size_t OFF_AGG = OFF_DCOV + sizeof(int16_t) * DC * 32;
 constexpr size_t OFF_OUT = OFF_AGG + sizeof(float) * 2 * NB * 32;
-constexpr size_t OFF_Q = OFF_OUT + (size_t)kGroupViews * TP * OPITCH;
-constexpr size_t SMEM = OFF_Q + sizeof(uint32_t) * NWARP * kQueueCap;
+constexpr size_t SMEM = OFF_OUT + (size_t)kGroupViews * TP * OPITCH;
 }  // namespace
 
 size_t tile_smem_bytes() { return SMEM; }
@@ -133,146 +131,6 @@ __device__ __forceinline__ uint32_t load_code(const unsigned char *Cb, int64_t i
     return __ldg(reinterpret_cast<const uint32_t *>(Cb) + idx);
 }
 
-// ------------------------------------------------------------ fast sweep
-// Default split (near backward j = 1, 2; far j >= 3; NFWD near forward
-// offsets in {0, 1}): one thread = one line, 32 output positions walked
-// toward lower u (SG = direction of u along pos) with a register window,
-// incremental coverage state and the far filter's suffix maximum carried in
-// a register.  Survivors of the filter are queued (warp-aggregated) and
-// resolved afterwards one per lane.
-template <int SG, int NFWD>
-__device__ __forceinline__ void sweep_fast(const float *__restrict__ sv, const uint32_t *cw,
-                                           const int16_t *last, const int16_t *next,
-                                           uint8_t *so, uint32_t *queue, int lane, int32_t b,
-                                           int32_t L0, int32_t NP32, int32_t NB32, int32_t h,
-                                           int32_t s, float T, int32_t Jr,
-                                           float blo0, float bhi0, float blo1, float bhi1,
-                                           float flo0, float fhi0, float t_dist, float t_disp) {
-    const float fs_ = (float)s;
-    const int32_t i0 = SG > 0 ? 32 * b + 31 : 32 * b;       // first (highest-u) position
-    const float *col = sv + lane;                           // this line's column
-    float uf = (float)(SG * (i0 - L0));                     // u of the current position
-    // suffix max of B = s v - u over positions i0 + SG*[4, Jr] (partners of any
-    // position of the block lie within Jr; a superset keeps the filter sound);
-    // SA = position where SX is attained (the witness used to guess partners)
-    float SX = -INFINITY;
-    int32_t SA = i0;
-    {
-        const int32_t jend = min(Jr, SG > 0 ? NP32 - 1 - i0 : i0);
-        const float *pq = col + (i0 + 4 * SG) * VPITCH;
-        float uq = uf + 4.0f;
-        for (int32_t j = 4; j <= jend; ++j) {
-            const float Bq = __fmaf_rn(fs_, *pq, -uq);
-            if (Bq > SX) { SX = Bq; SA = i0 + SG * j; }
-            pq += SG * VPITCH;
-            uq += 1.0f;
-        }
-    }
-    // the staged range has >= 32 NaN-padded positions beyond every output block
-    const float *pc = col + i0 * VPITCH;
-    float vp = pc[0], v1 = pc[SG * VPITCH], v2 = pc[2 * SG * VPITCH], v3 = pc[3 * SG * VPITCH];
-    // coverage state: SG > 0 tracks pc(x) for x = i + h (x decreasing),
-    // SG < 0 tracks nc(x) for x = i - h (x increasing)
-    int32_t cst = SG > 0 ? prevcand(cw, last, i0 + h, lane) : nextcand(cw, next, i0 - h, NB32, lane);
-    auto dcov_of = [&](int32_t i) -> int32_t {
-        if (SG > 0) {
-            const int32_t x = i + h;
-            if (cst > x) cst = prevcand(cw, last, x, lane);
-            return (cst >= i - h) ? cst + h - i : -1;         // NONE_LO < i - h
-        }
-        const int32_t x = i - h;
-        if (cst < x) cst = nextcand(cw, next, x, NB32, lane);
-        return (cst <= i + h) ? i + h - cst : -1;             // NONE_HI > i + h
-    };
-    int32_t dc = dcov_of(i0);
-    int32_t qn = 0;                                         // warp-uniform queue length
-    const uint32_t lt = (1u << lane) - 1u;
-    // exact resolution of queued survivors, one per lane, at guessed offsets;
-    // misses go to a warp-cooperative exhaustive search (32 offsets per step)
-    auto flush = [&]() {
-        __syncwarp();
-        for (int32_t e0 = 0; e0 < qn; e0 += 32) {
-            const int32_t e = e0 + lane;
-            bool miss = false;
-            uint32_t ent = 0;
-            if (e < qn) {
-                ent = queue[e];
-                const int32_t r = ent & 31, ln = (ent >> 5) & 31, jg = (ent >> 10) & 2047, jm = ent >> 21;
-                const int32_t i = i0 - SG * r;
-                const float vq0 = sv[i * VPITCH + ln];
-                bool hit = false;
-#pragma unroll
-                for (int c = 0; c < 5; ++c) {
-                    const int32_t j = jg + (c == 0 ? 0 : (c == 1 ? -1 : (c == 2 ? 1 : (c == 3 ? -2 : 2))));
-                    if (!hit && j >= 3 && j <= jm &&
-                        pair_exact(sv[(i + SG * j) * VPITCH + ln], vq0, -j, s, t_dist, t_disp)) hit = true;
-                }
-                if (hit) so[(i - L0) * OPITCH + ln] = 1;
-                miss = !hit;
-            }
-            unsigned pend = __ballot_sync(0xffffffffu, miss);
-            while (pend) {
-                const int src = __ffs(pend) - 1;
-                pend &= pend - 1;
-                const uint32_t en = __shfl_sync(0xffffffffu, ent, src);
-                const int32_t r = en & 31, ln = (en >> 5) & 31, jm = en >> 21;
-                const int32_t i = i0 - SG * r;
-                const float vs = sv[i * VPITCH + ln];
-                bool found = false;
-                for (int32_t j0 = 3; j0 <= jm && !found; j0 += 32) {
-                    const int32_t j = j0 + lane;
-                    const bool ok = j <= jm && pair_exact(sv[(i + SG * j) * VPITCH + ln], vs, -j, s,
-                                                          t_dist, t_disp);
-                    found = __ballot_sync(0xffffffffu, ok) != 0u;
-                }
-                if (found && lane == 0) so[(i - L0) * OPITCH + ln] = 1;
-            }
-        }
-        __syncwarp();
-        qn = 0;
-    };
-    const int32_t lim0 = SG > 0 ? NP32 - 1 - i0 : i0;       // staged extent beyond i0
-#pragma unroll 2
-    for (int r = 0; r < 32; ++r) {
-        const int32_t i = i0 - SG * r;
-        const float vf = pc[-SG * VPITCH];                   // forward neighbour
-        {   // fold position i + 3 SG into the suffix max
-            const float B3 = __fmaf_rn(fs_, v3, -(uf + 3.0f));
-            if (B3 > SX) { SX = B3; SA = i + 3 * SG; }
-        }
-        const int32_t dcn = dcov_of(i - SG);
-        const float d1 = __fsub_rn(v1, vp), d2 = __fsub_rn(v2, vp);
-        bool m = ((d1 > blo0) & (d1 < bhi0) & (dc >= 1)) | ((d2 > blo1) & (d2 < bhi1) & (dc >= 2));
-        if (NFWD) {
-            const float df = __fsub_rn(vf, vp);
-            m |= (df > flo0) & (df < fhi0) & (dcn >= 1);
-        }
-        // far filter: a partner at j >= 3 needs some B_q > B_p - t_dist;
-        // partners lie within the staged reach (>= min(2h, t_dist + s R))
-        const float Bp = __fmaf_rn(fs_, vp, -uf);
-        const int32_t jmax = min(min(dc, 2 * h), lim0 + r);
-        const bool surv = !m && jmax >= 3 && SX > __fsub_rn(Bp, T);
-        const unsigned bal = __ballot_sync(0xffffffffu, surv);
-        if (bal) {
-            if (qn + __popc(bal) > kQueueCap) flush();
-            if (surv) {
-                // guess: past the witness SA, B falls ~1 per step on a flat
-                // occluder, so the partner sits ~(SX - Bp) beyond it
-                const int32_t jg = SG * (SA - i) + min(max(0, __float2int_rn(__fsub_rn(SX, Bp))), 1023);
-                queue[qn + __popc(bal & lt)] = (uint32_t)r | ((uint32_t)lane << 5) |
-                                               ((uint32_t)min(jg, 2047) << 10) | ((uint32_t)jmax << 21);
-            }
-            qn += __popc(bal);
-        }
-        so[(i - L0) * OPITCH + lane] = (uint8_t)m;
-        v3 = v2; v2 = v1; v1 = vp; vp = vf;
-        pc -= SG * VPITCH;
-        dc = dcn;
-        uf -= 1.0f;
-    }
-    flush();
-}
-
 // ------------------------------------------------------------ bit-sliced sweep
 // Smallest float > x (x finite): the exact rewrite x > a <=> x >= nextup(a).
 __device__ __forceinline__ float nextup(float a) {
@@ -282,8 +140,9 @@ __device__ __forceinline__ float nextup(float a) {
 }
 // Appends the sign bit of a float / int to a word: (w << 1) | sign(x).
 // The sign of fl(x - c) is the exact sign of x - c, so fl(x - nextup(a)) < 0
-// <=> !(x > a) and fl(x - b) < 0 <=> x < b; a NaN operand gives a positive
-// canonical NaN (sign 0) and therefore fails every "x < b" test.
+// <=> !(x > a) and fl(x - b) < 0 <=> x < b.  For a NaN x (absent sample)
+// both differences are NaN with one common sign, so the interval bit
+// ~sign(x - a') & sign(x - b) is 0 whatever that sign is.
 __device__ __forceinline__ uint32_t pushf(uint32_t w, float x) {
     return __funnelshift_l(__float_as_uint(x), w, 1);
 }
@@ -299,7 +158,7 @@ __device__ __forceinline__ uint32_t pushi(uint32_t w, int32_t x) {
 // Far survivors are resolved exactly afterwards: at the offset of the line's
 // previous hit, or (first survivor of the line) at the offset guessed from
 // the suffix-max witness, else by a warp-cooperative exhaustive search.
-template <int SG, int NFWD>
+template <int SG, int NFWD, int VP>
 __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const uint32_t *cw,
                                            const int16_t *last, const int16_t *next,
                                            uint8_t *so, int lane, int32_t b, int32_t L0,
@@ -317,17 +176,17 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
     int32_t SA = i0;
     {
         const int32_t jend = min(Jr, SG > 0 ? NP32 - 1 - i0 : i0);
-        const float *pq = col + (i0 + 4 * SG) * VPITCH;
+        const float *pq = col + (i0 + 4 * SG) * VP;
         float uq = uf + 4.0f;
         for (int32_t j = 4; j <= jend; ++j) {
             const float Bq = __fmaf_rn(fs_, *pq, -uq);
             if (Bq > SX) { SX = Bq; SA = i0 + SG * j; }
-            pq += SG * VPITCH;
+            pq += SG * VP;
             uq += 1.0f;
         }
     }
-    const float *pc = col + i0 * VPITCH;
-    float vp = pc[0], v1 = pc[SG * VPITCH], v2 = pc[2 * SG * VPITCH], v3 = pc[3 * SG * VPITCH];
+    const float *pc = col + i0 * VP;
+    float vp = pc[0], v1 = pc[SG * VP], v2 = pc[2 * SG * VP], v3 = pc[3 * SG * VP];
     int32_t cst = SG > 0 ? prevcand(cw, last, i0 + h, lane) : nextcand(cw, next, i0 - h, NB32, lane);
     auto dcov_of = [&](int32_t i) -> int32_t {
         if (SG > 0) {
@@ -342,13 +201,10 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
     int32_t dc = dcov_of(i0);
     uint32_t G1 = 0, L1 = 0, G2 = 0, L2 = 0, GF = 0, LF = 0;   // interval sign words
     uint32_t C1 = 0, C2 = 0, C3 = 0, CF = 0, FR = 0;           // coverage / far words
-    bool got = false;                                          // first raw far survivor seen
-    int32_t sa0 = 0;
-    float sx0 = 0.0f;
 #pragma unroll 8
     for (int r = 0; r < 32; ++r) {
         const int32_t i = i0 - SG * r;
-        const float vf = pc[-SG * VPITCH];                       // forward neighbour
+        const float vf = pc[-SG * VP];                       // forward neighbour
         {   // fold position i + 3 SG into the suffix max
             const float B3 = __fmaf_rn(fs_, v3, -(uf + 3.0f));
             if (B3 > SX) { SX = B3; SA = i + 3 * SG; }
@@ -366,11 +222,18 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
         C2 = pushi(C2, 1 - dc);                                  // dc >= 2
         C3 = pushi(C3, 2 - dc);                                  // dc >= 3
         // far filter: survivor <=> SX > fl(B_p - T)
-        const float fr = __fsub_rn(__fsub_rn(__fmaf_rn(fs_, vp, -uf), T), SX);
+        const float Bp = __fmaf_rn(fs_, vp, -uf);
+        const float fr = __fsub_rn(__fsub_rn(Bp, T), SX);
         FR = pushf(FR, fr);
-        if (!got && fr < 0.0f) { got = true; sa0 = SA; sx0 = SX; }
+        if (fr < 0.0f) {
+            // guessed partner offset: past the witness SA, B falls ~1 per step on
+            // a flat occluder, so the partner sits ~(SX - Bp) beyond it; parked
+            // in this position's output byte until the exact resolution below
+            const int32_t jg = SG * (SA - i) + min(max(0, __float2int_rn(__fsub_rn(SX, Bp))), 255);
+            so[(i - L0) * OPITCH + lane] = (uint8_t)min(jg, 255);
+        }
         v3 = v2; v2 = v1; v1 = vp; vp = vf;
-        pc -= SG * VPITCH;
+        pc -= SG * VP;
         dc = dcn;
         uf -= 1.0f;
     }
@@ -385,12 +248,11 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
     // exact resolution, u-descending order; jl = offset of the line's last hit
     int32_t jl = 0;
     uint32_t miss = 0;
-    bool first = true;
     while (sv_bits) {
         const int32_t rr = SG > 0 ? 31 - __clz(sv_bits) : __ffs(sv_bits) - 1;
         sv_bits &= ~(1u << rr);
         const int32_t i = 32 * b + rr;
-        const float vq0 = sv[i * VPITCH + lane];
+        const float vq0 = sv[i * VP + lane];
         int32_t dci;
         if (SG > 0) {
             const int32_t pcv = prevcand(cw, last, i + h, lane);
@@ -400,18 +262,13 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
             dci = ncv <= i + h ? i + h - ncv : -1;
         }
         const int32_t jm = min(min(dci, 2 * h), SG > 0 ? NP32 - 1 - i : i);
-        int32_t jg = jl;
-        if (first) {
-            const float Bp = __fmaf_rn(fs_, vq0, -(float)(SG * (i - L0)));
-            jg = SG * (sa0 - i) + min(max(0, __float2int_rn(__fsub_rn(sx0, Bp))), 1023);
-            first = false;
-        }
+        const int32_t jg = so[(i - L0) * OPITCH + lane];
         bool hit = false;
 #pragma unroll
-        for (int c = 0; c < 5; ++c) {
-            const int32_t j = jg + (c == 0 ? 0 : (c == 1 ? -1 : (c == 2 ? 1 : (c == 3 ? -2 : 2))));
+        for (int c = 0; c < 6; ++c) {
+            const int32_t j = c == 5 ? jl : jg + (c == 0 ? 0 : (c == 1 ? -1 : (c == 2 ? 1 : (c == 3 ? -2 : 2))));
             if (!hit && j >= 3 && j <= jm &&
-                pair_exact(sv[(i + SG * j) * VPITCH + lane], vq0, -j, s, t_dist, t_disp)) {
+                pair_exact(sv[(i + SG * j) * VP + lane], vq0, -j, s, t_dist, t_disp)) {
                 hit = true; jl = j;
             }
         }
@@ -426,7 +283,7 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
         if (lane == src) miss &= ~(1u << rr);
         pend = __ballot_sync(0xffffffffu, miss != 0u);
         const int32_t i = 32 * b + rr;
-        const float vs = sv[i * VPITCH + src];
+        const float vs = sv[i * VP + src];
         int32_t dci;
         if (SG > 0) {
             const int32_t pcv = prevcand(cw, last, i + h, src);
@@ -439,7 +296,7 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
         bool found = false;
         for (int32_t j0 = 3; j0 <= jm && !found; j0 += 32) {
             const int32_t j = j0 + lane;
-            const bool ok = j <= jm && pair_exact(sv[(i + SG * j) * VPITCH + src], vs, -j, s,
+            const bool ok = j <= jm && pair_exact(sv[(i + SG * j) * VP + src], vs, -j, s,
                                                   t_dist, t_disp);
             found = __ballot_sync(0xffffffffu, ok) != 0u;
         }
@@ -472,11 +329,10 @@ struct TileArgs {
     const void *codes;
 };
 
-template <class G, int CB>
+template <class G, int CB, int VP>
 __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const TileDesc &td,
                                           const GroupDesc &gd, const FamilyDesc &fd,
                                           unsigned char *smem) {
-    uint32_t *squeue = reinterpret_cast<uint32_t *>(smem + OFF_Q) + (threadIdx.x >> 5) * kQueueCap;
     float *sv = reinterpret_cast<float *>(smem + OFF_V);
     uint32_t *scw = reinterpret_cast<uint32_t *>(smem + OFF_CW);
     int16_t *slast = reinterpret_cast<int16_t *>(smem + OFF_LAST);
@@ -534,7 +390,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
 
     if (any_staged) {
         // ------------------------------------------------ 1. stage
-        for (int k = tid; k < NP32 * 32; k += NT) sv[(k >> 5) * VPITCH + (k & 31)] = __int_as_float(0x7fc00000);
+        for (int k = tid; k < NP32 * 32; k += NT) sv[(k >> 5) * VP + (k & 31)] = __int_as_float(0x7fc00000);
         for (int k = tid; k < 2 * NB * 32; k += NT) scw[k] = 0u;
         __syncthreads();
         // only [L0 - halo, L0 + TPe + halo) is ever read; the rest stays NaN
@@ -555,7 +411,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                     const int32_t x = l0 + lane + geo.fl(y);
                     if (x < 0 || x >= W) continue;
                     const int64_t idx = (int64_t)y * W + x;
-                    sv[i * VPITCH + lane] = __ldg(Df + idx);
+                    sv[i * VP + lane] = __ldg(Df + idx);
                     const uint32_t c = load_code<CB>(Cb, idx) >> cshift;
                     w0 |= (c & 1u) << r;
                     w1 |= ((c >> 1) & 1u) << r;
@@ -583,7 +439,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                             const int32_t i = x - base;
                             uint32_t c = 0u;
                             if (ok) {
-                                sv[i * VPITCH + l] = __ldg(Drow + x);
+                                sv[i * VP + l] = __ldg(Drow + x);
                                 c = load_code<CB>(Cb, (int64_t)y * W + x) >> cshift;
                             }
                             const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u);
@@ -602,7 +458,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                         for (int32_t x = xa + lane; x <= xb; x += 32) {
                             const int32_t l = y - l0 - geo.fl(x);
                             const int32_t i = x - base;
-                            sv[i * VPITCH + l] = __ldg(Drow + x);
+                            sv[i * VP + l] = __ldg(Drow + x);
                             const uint32_t c = load_code<CB>(Cb, (int64_t)y * W + x) >> cshift;
                             if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
                             if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + l], 1u << (i & 31));
@@ -677,17 +533,17 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                 const int32_t b = (L0 >> 5) + ob;
                 if (sg > 0) {
                     if (cv.nfwd)
-                        sweep_bits<1, 1>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                        sweep_bits<1, 1, VP>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
                                          blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                     else
-                        sweep_bits<1, 0>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                        sweep_bits<1, 0, VP>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
                                          blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                 } else {
                     if (cv.nfwd)
-                        sweep_bits<-1, 1>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                        sweep_bits<-1, 1, VP>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
                                           blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                     else
-                        sweep_bits<-1, 0>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
+                        sweep_bits<-1, 0, VP>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
                                           blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
                 }
             }
@@ -715,7 +571,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
             float A = -INFINITY, Ap = -INFINITY;
             for (int r = 0; r < 32; ++r) {
                 const int32_t i = 32 * b + r;
-                const float Bv = __fsub_rn(__fmul_rn(fs_, sv[i * VPITCH + lane]), (float)(sg * (i - L0)));
+                const float Bv = __fsub_rn(__fmul_rn(fs_, sv[i * VP + lane]), (float)(sg * (i - L0)));
                 A = fmaxf(A, Bv);
                 const bool excl = sg > 0 ? (r < jstar - 1) : (r > 32 - jstar);
                 if (!excl) Ap = fmaxf(Ap, Bv);
@@ -742,12 +598,12 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                 {   // fold position i + sg*jstar into the suffix max
                     const int32_t qf = i + sg * jstar;
                     if (qf >= 0 && qf < NP32)
-                        SX = fmaxf(SX, __fsub_rn(__fmul_rn(fs_, sv[qf * VPITCH + lane]),
+                        SX = fmaxf(SX, __fsub_rn(__fmul_rn(fs_, sv[qf * VP + lane]),
                                                  (float)(sg * (qf - L0))));
                 }
                 const int32_t k = i - L0;          // output index
                 if (k < 0 || k >= TPe) continue;
-                const float vp = sv[i * VPITCH + lane];
+                const float vp = sv[i * VP + lane];
                 bool m = false;
                 if (!isnan(vp)) {
                     const int32_t dc = sdcov[(i - D0) * 32 + lane];
@@ -755,7 +611,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                     for (int j = 1; j <= kMaxNear; ++j) {
                         if (j > cv.nback) break;
                         const int32_t q = i + sg * j;
-                        const float vq = (q >= 0 && q < NP32) ? sv[q * VPITCH + lane] : __int_as_float(0x7fc00000);
+                        const float vq = (q >= 0 && q < NP32) ? sv[q * VP + lane] : __int_as_float(0x7fc00000);
                         const float dl = __fsub_rn(vq, vp);
                         m |= (dl > blo[j - 1]) & (dl < bhi[j - 1]) & (j <= dc);
                     }
@@ -763,7 +619,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                     for (int fo = 1; fo <= kMaxNear; ++fo) {
                         if (fo > cv.nfwd) break;
                         const int32_t q = i - sg * fo;
-                        const float vq = (q >= 0 && q < NP32) ? sv[q * VPITCH + lane] : __int_as_float(0x7fc00000);
+                        const float vq = (q >= 0 && q < NP32) ? sv[q * VP + lane] : __int_as_float(0x7fc00000);
                         const float dl = __fsub_rn(vq, vp);
                         const int32_t dq = sdcov[(q - D0) * 32 + lane];
                         m |= (dl > flo[fo - 1]) & (dl < fhi[fo - 1]) & (dq >= fo);
@@ -780,12 +636,12 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                                     for (int dj = 0; dj < 3 && !m; ++dj) {
                                         const int32_t j = jl + (dj == 0 ? 0 : (dj == 1 ? -1 : 1));
                                         if (j < jstar || j > jmax) continue;
-                                        if (pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s,
+                                        if (pair_exact(sv[(i + sg * j) * VP + lane], vp, -j, s,
                                                        p.t_dist, p.t_disp)) { m = true; jl = j; }
                                     }
                                 }
                                 for (int32_t j = jstar; j <= jmax && !m; ++j) {
-                                    if (pair_exact(sv[(i + sg * j) * VPITCH + lane], vp, -j, s,
+                                    if (pair_exact(sv[(i + sg * j) * VP + lane], vp, -j, s,
                                                    p.t_dist, p.t_disp)) { m = true; jl = j; }
                                 }
                             }
@@ -873,17 +729,18 @@ __global__ void __launch_bounds__(NT, 2) k_tile(TileArgs a) {
     const GroupDesc gd = a.groups[td.group];
     const FamilyDesc fd = a.fams[gd.fam];
     switch (fd.kind) {
-        case 0: tile_body<GeoK<true, 0, 1>, CB>(a, GeoK<true, 0, 1>(), td, gd, fd, smem); break;
-        case 1: tile_body<GeoK<false, 0, 1>, CB>(a, GeoK<false, 0, 1>(), td, gd, fd, smem); break;
-        case 2: tile_body<GeoK<true, 1, 1>, CB>(a, GeoK<true, 1, 1>(), td, gd, fd, smem); break;
-        case 3: tile_body<GeoK<true, -1, 1>, CB>(a, GeoK<true, -1, 1>(), td, gd, fd, smem); break;
-        case 4: tile_body<GeoK<true, 1, 2>, CB>(a, GeoK<true, 1, 2>(), td, gd, fd, smem); break;
-        case 5: tile_body<GeoK<true, -1, 2>, CB>(a, GeoK<true, -1, 2>(), td, gd, fd, smem); break;
-        case 6: tile_body<GeoK<false, 1, 2>, CB>(a, GeoK<false, 1, 2>(), td, gd, fd, smem); break;
-        case 7: tile_body<GeoK<false, -1, 2>, CB>(a, GeoK<false, -1, 2>(), td, gd, fd, smem); break;
+        case 0: tile_body<GeoK<true, 0, 1>, CB, 33>(a, GeoK<true, 0, 1>(), td, gd, fd, smem); break;
+        case 1: tile_body<GeoK<false, 0, 1>, CB, 33>(a, GeoK<false, 0, 1>(), td, gd, fd, smem); break;
+        case 2: tile_body<GeoK<true, 1, 1>, CB, 34>(a, GeoK<true, 1, 1>(), td, gd, fd, smem); break;
+        case 3: tile_body<GeoK<true, -1, 1>, CB, 34>(a, GeoK<true, -1, 1>(), td, gd, fd, smem); break;
+        case 4: tile_body<GeoK<true, 1, 2>, CB, 34>(a, GeoK<true, 1, 2>(), td, gd, fd, smem); break;
+        case 5: tile_body<GeoK<true, -1, 2>, CB, 34>(a, GeoK<true, -1, 2>(), td, gd, fd, smem); break;
+        case 6: tile_body<GeoK<false, 1, 2>, CB, 33>(a, GeoK<false, 1, 2>(), td, gd, fd, smem); break;
+        case 7: tile_body<GeoK<false, -1, 2>, CB, 33>(a, GeoK<false, -1, 2>(), td, gd, fd, smem); break;
         default: {
             GeoR g{fd.xmajor != 0, fd.num, fd.den};
-            tile_body<GeoR, CB>(a, g, td, gd, fd, smem);
+            if (g.xm()) tile_body<GeoR, CB, 34>(a, g, td, gd, fd, smem);
+            else tile_body<GeoR, CB, 33>(a, g, td, gd, fd, smem);
         }
     }
 }
