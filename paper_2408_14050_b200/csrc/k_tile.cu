@@ -161,7 +161,7 @@ __device__ __forceinline__ uint32_t pushi(uint32_t w, int32_t x) {
 template <int SG, int NFWD, int VP>
 __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const uint32_t *cw,
                                            const int16_t *last, const int16_t *next,
-                                           uint8_t *so, int lane, int32_t b, int32_t L0,
+                                           uint8_t *so, int lane, int32_t b, int32_t nblk, int32_t L0,
                                            int32_t NP32, int32_t NB32, int32_t h, int32_t s,
                                            float T, int32_t Jr, float blo0, float bhi0,
                                            float blo1, float bhi1, float flo0, float fhi0,
@@ -199,11 +199,16 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
         return (cst <= i + h) ? i + h - cst : -1;
     };
     int32_t dc = dcov_of(i0);
+    // nblk consecutive blocks in u-descending order share the carried state
+    // (window, suffix max, coverage), so the suffix-max start-up scan is paid once
+    for (int kb = 0; kb < nblk; ++kb) {
+    const int32_t bb = b - SG * kb;
+    const int32_t ib = SG > 0 ? 32 * bb + 31 : 32 * bb;       // block's first position
     uint32_t G1 = 0, L1 = 0, G2 = 0, L2 = 0, GF = 0, LF = 0;   // interval sign words
     uint32_t C1 = 0, C2 = 0, C3 = 0, CF = 0, FR = 0;           // coverage / far words
 #pragma unroll 8
     for (int r = 0; r < 32; ++r) {
-        const int32_t i = i0 - SG * r;
+        const int32_t i = ib - SG * r;
         const float vf = pc[-SG * VP];                       // forward neighbour
         {   // fold position i + 3 SG into the suffix max
             const float B3 = __fmaf_rn(fs_, v3, -(uf + 3.0f));
@@ -251,7 +256,7 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
     while (sv_bits) {
         const int32_t rr = SG > 0 ? 31 - __clz(sv_bits) : __ffs(sv_bits) - 1;
         sv_bits &= ~(1u << rr);
-        const int32_t i = 32 * b + rr;
+        const int32_t i = 32 * bb + rr;
         const float vq0 = sv[i * VP + lane];
         int32_t dci;
         if (SG > 0) {
@@ -282,7 +287,7 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
         const int32_t rr = __ffs(mw) - 1;
         if (lane == src) miss &= ~(1u << rr);
         pend = __ballot_sync(0xffffffffu, miss != 0u);
-        const int32_t i = 32 * b + rr;
+        const int32_t i = 32 * bb + rr;
         const float vs = sv[i * VP + src];
         int32_t dci;
         if (SG > 0) {
@@ -303,9 +308,10 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
         if (found && lane == src) m |= 1u << rr;
     }
     // bytes of the block for the store phase
-    uint8_t *ob = so + (32 * b - L0) * OPITCH + lane;
+    uint8_t *ob = so + (32 * bb - L0) * OPITCH + lane;
 #pragma unroll 8
     for (int r = 0; r < 32; ++r) ob[r * OPITCH] = (uint8_t)((m >> r) & 1u);
+    }
 }
 
 // ------------------------------------------------------------ tile body
@@ -422,7 +428,22 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
         } else {
             // x-major: pos = x, lane = y - l0 - fl(x); walk image rows
             const int32_t xs = max(base + lo_i, 0), xe = min(base + hi_i, W) - 1;
-            if (xs <= xe) {
+            if (xs <= xe && geo.den() == 1 && (geo.num() == 1 || geo.num() == -1)) {
+                // diagonals: image row y = l0 + t holds lane l at x = t - l (num = 1)
+                // or x = l - t (num = -1): one coalesced row segment per step t
+                const int32_t nm = geo.num();
+                const int32_t tlo = nm > 0 ? xs : -xe, thi = nm > 0 ? xe + 31 : 31 - xs;
+                for (int32_t t = max(tlo, -l0) + warp; t <= min(thi, H - 1 - l0); t += NWARP) {
+                    const int32_t y = l0 + t, x = nm > 0 ? t - lane : lane - t;
+                    if (x < xs || x > xe) continue;
+                    const int32_t i = x - base;
+                    const int64_t idx = (int64_t)y * W + x;
+                    sv[i * VP + lane] = __ldg(Df + idx);
+                    const uint32_t c = load_code<CB>(Cb, idx) >> cshift;
+                    if (c & 1u) atomicOr(&scw[(0 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
+                    if (c & 2u) atomicOr(&scw[(1 * NB + (i >> 5)) * 32 + lane], 1u << (i & 31));
+                }
+            } else if (xs <= xe) {
                 const int32_t fa = geo.fl(xs), fb = geo.fl(xe);
                 const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
                 for (int32_t y = ylo + warp; y <= yhi; y += NWARP) {
@@ -524,31 +545,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                 flo[j] = vd.fwd_lo[j]; fhi[j] = vd.fwd_hi[j];
             }
         }
-        if (cv.nback == 2 && cv.jstar == 3 && cv.nfwd <= 1) {
-            // default thresholds: barrier-free register sweep
-            const int32_t nob = (TPe + 31) >> 5;
-            const uint32_t *cwd = scw + d * NB * 32;
-            const int16_t *ld = slast + d * NB * 32, *nd = snext + d * NB * 32;
-            for (int ob = warp; ob < nob; ob += NWARP) {
-                const int32_t b = (L0 >> 5) + ob;
-                if (sg > 0) {
-                    if (cv.nfwd)
-                        sweep_bits<1, 1, VP>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
-                                         blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
-                    else
-                        sweep_bits<1, 0, VP>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
-                                         blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
-                } else {
-                    if (cv.nfwd)
-                        sweep_bits<-1, 1, VP>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
-                                          blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
-                    else
-                        sweep_bits<-1, 0, VP>(sv, cwd, ld, nd, so, lane, b, L0, NP32, NB32, h, s, T, cv.jr,
-                                          blo[0], bhi[0], blo[1], bhi[1], flo[0], fhi[0], p.t_dist, p.t_disp);
-                }
-            }
-            continue;
-        }
+        if (cv.nback == 2 && cv.jstar == 3 && cv.nfwd <= 1) continue;   // fast pass below
         // ---- generic thresholds: dcov table, block aggregates, per-position sweep
         // a. dcov for local positions [L0 - kMaxNear, L0 + TPe + kMaxNear)
         const int32_t D0 = L0 - kMaxNear;
@@ -653,6 +650,40 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
         }
         __syncthreads();    // sdcov / sagg reused by the next view
     }
+    // ---- default thresholds: barrier-free bit-sliced sweeps, all views at once;
+    // a warp owns (view, pair of adjacent 32-position blocks)
+    if (!fs.nonfinite) {
+        const int32_t nob = (TPe + 31) >> 5, npair = (nob + 1) >> 1;
+        for (int u = warp; u < gd.nv * npair; u += NWARP) {
+            const int g = u / npair, pr = u - g * npair;
+            const ViewRegs cv = g == 0 ? vr[0] : vr[kGroupViews - 1];
+            if (!(cv.staged && cv.nback == 2 && cv.jstar == 3 && cv.nfwd <= 1)) continue;
+            uint8_t *so = sout + (size_t)g * TP * OPITCH;
+            const ViewDesc &vd = a.views[cv.vid];
+            const float blo0 = vd.back_lo[0], bhi0 = vd.back_hi[0], blo1 = vd.back_lo[1],
+                        bhi1 = vd.back_hi[1], flo0 = vd.fwd_lo[0], fhi0 = vd.fwd_hi[0];
+            const int32_t blo = (L0 >> 5) + 2 * pr, bhi = min(blo + 1, (L0 >> 5) + nob - 1);
+            const int32_t nb = bhi - blo + 1;
+            const int d = cv.sg > 0 ? 0 : 1;
+            const uint32_t *cwd = scw + d * NB * 32;
+            const int16_t *ld = slast + d * NB * 32, *nd = snext + d * NB * 32;
+            if (cv.sg > 0) {
+                if (cv.nfwd)
+                    sweep_bits<1, 1, VP>(sv, cwd, ld, nd, so, lane, bhi, nb, L0, NP32, NB32, cv.h, cv.s, cv.T,
+                                         cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
+                else
+                    sweep_bits<1, 0, VP>(sv, cwd, ld, nd, so, lane, bhi, nb, L0, NP32, NB32, cv.h, cv.s, cv.T,
+                                         cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
+            } else {
+                if (cv.nfwd)
+                    sweep_bits<-1, 1, VP>(sv, cwd, ld, nd, so, lane, blo, nb, L0, NP32, NB32, cv.h, cv.s, cv.T,
+                                          cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
+                else
+                    sweep_bits<-1, 0, VP>(sv, cwd, ld, nd, so, lane, blo, nb, L0, NP32, NB32, cv.h, cv.s, cv.T,
+                                          cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
+            }
+        }
+    }
     __syncthreads();
 
     // ------------------------------------------------ 3. store (row-contiguous)
@@ -705,6 +736,17 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
         } else {
             const int32_t xs = max(P0, 0), xe = min(P1, W) - 1;
             if (xs > xe) continue;
+            if (geo.den() == 1 && (geo.num() == 1 || geo.num() == -1)) {
+                // diagonals: row y = l0 + t, lane l at x = t - l (num = 1) / l - t
+                const int32_t nm = geo.num();
+                const int32_t tlo = nm > 0 ? xs : -xe, thi = nm > 0 ? xe + 31 : 31 - xs;
+                for (int32_t t = max(tlo, -l0) + warp; t <= min(thi, H - 1 - l0); t += NWARP) {
+                    const int32_t x = nm > 0 ? t - lane : lane - t;
+                    if (x < xs || x > xe) continue;
+                    __stcs(Mv + (int64_t)(l0 + t) * W + x, so[(x - P0) * OPITCH + lane]);
+                }
+                continue;
+            }
             const int32_t fa = geo.fl(xs), fb = geo.fl(xe);
             const int32_t ylo = max(0, l0 + min(fa, fb)), yhi = min(H - 1, l0 + 31 + max(fa, fb));
             for (int32_t y = ylo + warp; y <= yhi; y += NWARP) {
