@@ -40,18 +40,16 @@ constexpr int HMAX = kTileHaloMax;     // max staged halo per side
 constexpr int NPMAX = TP + 2 * HMAX;   // staged positions
 constexpr int NB = NPMAX / 32;         // 32-position blocks
 constexpr int VPITCH = 34;             // max floats per staged position (32 lanes + pad)
-constexpr int OPITCH = 36;             // bytes per output position (32 lanes + pad)
-constexpr int DC = TP + 2 * kMaxNear;  // dcov entries (outputs +- near reach)
 constexpr int16_t NONE_LO = -30000, NONE_HI = 30000;
 
+constexpr int NOB = TP / 32;            // output blocks per tile
 constexpr size_t OFF_V = 0;
 constexpr size_t OFF_CW = OFF_V + sizeof(float) * NPMAX * VPITCH;
 constexpr size_t OFF_LAST = OFF_CW + sizeof(uint32_t) * 2 * NB * 32;
 constexpr size_t OFF_NEXT = OFF_LAST + sizeof(int16_t) * 2 * NB * 32;
-constexpr size_t OFF_DCOV = OFF_NEXT + sizeof(int16_t) * 2 * NB * 32;
-constexpr size_t OFF_AGG = OFF_DCOV + sizeof(int16_t) * DC * 32;
-constexpr size_t OFF_OUT = OFF_AGG + sizeof(float) * 2 * NB * 32;
-constexpr size_t SMEM = OFF_OUT + (size_t)kGroupViews * TP * OPITCH;
+constexpr size_t OFF_OUT = OFF_NEXT + sizeof(int16_t) * 2 * NB * 32;     // mask bits
+constexpr size_t OFF_JG = OFF_OUT + sizeof(uint32_t) * kGroupViews * NOB * 32;
+constexpr size_t SMEM = OFF_JG + (size_t)NWARP * 32 * 32;               // parked guesses
 }  // namespace
 
 size_t tile_smem_bytes() { return SMEM; }
@@ -161,7 +159,8 @@ __device__ __forceinline__ uint32_t pushi(uint32_t w, int32_t x) {
 template <int SG, int NFWD, int VP>
 __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const uint32_t *cw,
                                            const int16_t *last, const int16_t *next,
-                                           uint8_t *so, int lane, int32_t b, int32_t nblk, int32_t L0,
+                                           uint32_t *ow, uint8_t *jgb, int lane, int32_t b,
+                                           int32_t nblk, int32_t L0,
                                            int32_t NP32, int32_t NB32, int32_t h, int32_t s,
                                            float T, int32_t Jr, float blo0, float bhi0,
                                            float blo1, float bhi1, float flo0, float fhi0,
@@ -233,9 +232,9 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
         if (fr < 0.0f) {
             // guessed partner offset: past the witness SA, B falls ~1 per step on
             // a flat occluder, so the partner sits ~(SX - Bp) beyond it; parked
-            // in this position's output byte until the exact resolution below
+            // in the warp's scratch until the exact resolution below
             const int32_t jg = SG * (SA - i) + min(max(0, __float2int_rn(__fsub_rn(SX, Bp))), 255);
-            so[(i - L0) * OPITCH + lane] = (uint8_t)min(jg, 255);
+            jgb[(i - 32 * bb) * 32 + lane] = (uint8_t)min(jg, 255);
         }
         v3 = v2; v2 = v1; v1 = vp; vp = vf;
         pc -= SG * VP;
@@ -267,7 +266,7 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
             dci = ncv <= i + h ? i + h - ncv : -1;
         }
         const int32_t jm = min(min(dci, 2 * h), SG > 0 ? NP32 - 1 - i : i);
-        const int32_t jg = so[(i - L0) * OPITCH + lane];
+        const int32_t jg = jgb[rr * 32 + lane];
         bool hit = false;
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
@@ -307,10 +306,8 @@ __device__ __forceinline__ void sweep_bits(const float *__restrict__ sv, const u
         }
         if (found && lane == src) m |= 1u << rr;
     }
-    // bytes of the block for the store phase
-    uint8_t *ob = so + (32 * bb - L0) * OPITCH + lane;
-#pragma unroll 8
-    for (int r = 0; r < 32; ++r) ob[r * OPITCH] = (uint8_t)((m >> r) & 1u);
+    ow[(bb - (L0 >> 5)) * 32 + lane] = m;      // bit r = position 32 bb + r
+    __syncwarp();                              // jgb reused by the next block
     }
 }
 
@@ -343,9 +340,8 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
     uint32_t *scw = reinterpret_cast<uint32_t *>(smem + OFF_CW);
     int16_t *slast = reinterpret_cast<int16_t *>(smem + OFF_LAST);
     int16_t *snext = reinterpret_cast<int16_t *>(smem + OFF_NEXT);
-    int16_t *sdcov = reinterpret_cast<int16_t *>(smem + OFF_DCOV);
-    float *sagg = reinterpret_cast<float *>(smem + OFF_AGG);
-    uint8_t *sout = smem + OFF_OUT;
+    uint32_t *outw = reinterpret_cast<uint32_t *>(smem + OFF_OUT);
+    uint8_t *sjg = smem + OFF_JG + (size_t)(threadIdx.x >> 5) * 32 * 32;
     const Params &p = a.p;
     const int32_t H = a.H, W = a.W;
 
@@ -508,157 +504,35 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
         __syncthreads();
     }
 
-    // ------------------------------------------------ 2. per view
+    // ------------------------------------------------ 2. masks as bit words
+    // outw[g][ob][lane]: bit r = mask of output position 32 ob + r of line lane
+    for (int k = tid; k < kGroupViews * NOB * 32; k += NT) outw[k] = 0u;
+    __syncthreads();
+    if (!fs.nonfinite) {       // non-finite frame: masks stay zero
+        // views without the default staged sweep: exact per-pixel routine
 #pragma unroll 1
-    for (int g = 0; g < gd.nv; ++g) {
-        const ViewRegs cv = g == 0 ? vr[0] : vr[kGroupViews - 1];   // static register selection
-        uint8_t *so = sout + (size_t)g * TP * OPITCH;
-        if (fs.nonfinite) {            // reject the frame, masks all zero
-            for (int k = tid; k < TP * 32; k += NT) so[(k >> 5) * OPITCH + (k & 31)] = 0;
-            continue;
-        }
-        if (!cv.staged) {           // halo too large: exact per-pixel routine
+        for (int g = 0; g < gd.nv; ++g) {
+            const ViewRegs cv = g == 0 ? vr[0] : vr[kGroupViews - 1];
+            if (cv.staged && cv.nback == 2 && cv.jstar == 3 && cv.nfwd <= 1) continue;
             const ViewDesc vd = a.views[cv.vid];
             for (int k = tid; k < TPe * 32; k += NT) {
                 const int32_t pos = P0 + (k >> 5), l = k & 31, ln = l0 + l;
                 int32_t x, y;
                 if (xm) { x = pos; y = ln + geo.fl(pos); }
                 else { y = pos; x = ln + geo.fl(pos); }
-                bool m = false;
-                if (x >= 0 && x < W && y >= 0 && y < H)
-                    m = direct_pixel<false>(Df, H, W, vd, fd, p, cv.h, x, y);
-                so[(k >> 5) * OPITCH + l] = (uint8_t)m;
-            }
-            continue;
-        }
-        const int32_t s = cv.s, sg = cv.sg, h = cv.h, jstar = cv.jstar;
-        const int d = sg > 0 ? 0 : 1;
-        const float fs_ = (float)s;
-        const float T = cv.T;
-        // exact fp32 interval bounds of the near offsets (host-precomputed, S7)
-        float blo[kMaxNear], bhi[kMaxNear], flo[kMaxNear], fhi[kMaxNear];
-        {
-            const ViewDesc &vd = a.views[cv.vid];
-#pragma unroll
-            for (int j = 0; j < kMaxNear; ++j) {
-                blo[j] = vd.back_lo[j]; bhi[j] = vd.back_hi[j];
-                flo[j] = vd.fwd_lo[j]; fhi[j] = vd.fwd_hi[j];
+                if (x >= 0 && x < W && y >= 0 && y < H &&
+                    direct_pixel<false>(Df, H, W, vd, fd, p, cv.h, x, y))
+                    atomicOr(&outw[(g * NOB + ((k >> 5) >> 5)) * 32 + l], 1u << ((k >> 5) & 31));
             }
         }
-        if (cv.nback == 2 && cv.jstar == 3 && cv.nfwd <= 1) continue;   // fast pass below
-        // ---- generic thresholds: dcov table, block aggregates, per-position sweep
-        // a. dcov for local positions [L0 - kMaxNear, L0 + TPe + kMaxNear)
-        const int32_t D0 = L0 - kMaxNear;
-        for (int k = warp; k < TPe + 2 * kMaxNear; k += NWARP) {
-            const int32_t i = D0 + k;
-            int32_t dc = -1;
-            if (i >= 0 && i < NP32) {
-                if (sg > 0) {
-                    const int32_t pcv = prevcand(scw + d * NB * 32, slast + d * NB * 32, min(i + h, NP32 - 1), lane);
-                    if (pcv != NONE_LO && pcv >= i - h) dc = pcv + h - i;
-                } else {
-                    const int32_t ncv = nextcand(scw + d * NB * 32, snext + d * NB * 32, max(i - h, 0), NB32, lane);
-                    if (ncv != NONE_HI && ncv <= i + h) dc = i + h - ncv;
-                }
-            }
-            sdcov[k * 32 + lane] = (int16_t)dc;
-        }
-        // b. block aggregates of B = s v - u for the far filter (u = sg (i - L0))
-        for (int b = warp; b < NB32; b += NWARP) {
-            float A = -INFINITY, Ap = -INFINITY;
-            for (int r = 0; r < 32; ++r) {
-                const int32_t i = 32 * b + r;
-                const float Bv = __fsub_rn(__fmul_rn(fs_, sv[i * VP + lane]), (float)(sg * (i - L0)));
-                A = fmaxf(A, Bv);
-                const bool excl = sg > 0 ? (r < jstar - 1) : (r > 32 - jstar);
-                if (!excl) Ap = fmaxf(Ap, Bv);
-            }
-            sagg[(0 * NB + b) * 32 + lane] = A;
-            sagg[(1 * NB + b) * 32 + lane] = Ap;
-        }
-        __syncthreads();
-        // c. sweep: warp w owns output block L0/32 + w, moving toward lower u
-        const int32_t nob = (TPe + 31) >> 5;
-        for (int ob = warp; ob < nob; ob += NWARP) {
-            const int32_t b = (L0 >> 5) + ob;
-            float SX = -INFINITY;
-            if (sg > 0) {
-                if (b + 1 < NB32) SX = sagg[(1 * NB + b + 1) * 32 + lane];
-                for (int bb = b + 2; bb < NB32; ++bb) SX = fmaxf(SX, sagg[(0 * NB + bb) * 32 + lane]);
-            } else {
-                if (b - 1 >= 0) SX = sagg[(1 * NB + b - 1) * 32 + lane];
-                for (int bb = 0; bb <= b - 2; ++bb) SX = fmaxf(SX, sagg[(0 * NB + bb) * 32 + lane]);
-            }
-            int32_t jl = 0;
-            for (int r = 0; r < 32; ++r) {
-                const int32_t i = sg > 0 ? 32 * b + 31 - r : 32 * b + r;
-                {   // fold position i + sg*jstar into the suffix max
-                    const int32_t qf = i + sg * jstar;
-                    if (qf >= 0 && qf < NP32)
-                        SX = fmaxf(SX, __fsub_rn(__fmul_rn(fs_, sv[qf * VP + lane]),
-                                                 (float)(sg * (qf - L0))));
-                }
-                const int32_t k = i - L0;          // output index
-                if (k < 0 || k >= TPe) continue;
-                const float vp = sv[i * VP + lane];
-                bool m = false;
-                if (!isnan(vp)) {
-                    const int32_t dc = sdcov[(i - D0) * 32 + lane];
-#pragma unroll
-                    for (int j = 1; j <= kMaxNear; ++j) {
-                        if (j > cv.nback) break;
-                        const int32_t q = i + sg * j;
-                        const float vq = (q >= 0 && q < NP32) ? sv[q * VP + lane] : __int_as_float(0x7fc00000);
-                        const float dl = __fsub_rn(vq, vp);
-                        m |= (dl > blo[j - 1]) & (dl < bhi[j - 1]) & (j <= dc);
-                    }
-#pragma unroll
-                    for (int fo = 1; fo <= kMaxNear; ++fo) {
-                        if (fo > cv.nfwd) break;
-                        const int32_t q = i - sg * fo;
-                        const float vq = (q >= 0 && q < NP32) ? sv[q * VP + lane] : __int_as_float(0x7fc00000);
-                        const float dl = __fsub_rn(vq, vp);
-                        const int32_t dq = sdcov[(q - D0) * 32 + lane];
-                        m |= (dl > flo[fo - 1]) & (dl < fhi[fo - 1]) & (dq >= fo);
-                    }
-                    if (!m) {
-                        const float Bp = __fsub_rn(__fmul_rn(fs_, vp), (float)(sg * (i - L0)));
-                        if (SX > __fsub_rn(Bp, T)) {
-                            // exact resolution over backward offsets j in [jstar, jmax]
-                            const int32_t lim = sg > 0 ? NP32 - 1 - i : i;
-                            const int32_t jmax = min(min(dc, 2 * h), lim);
-                            if (jmax >= jstar) {
-                                if (jl >= jstar) {
-#pragma unroll
-                                    for (int dj = 0; dj < 3 && !m; ++dj) {
-                                        const int32_t j = jl + (dj == 0 ? 0 : (dj == 1 ? -1 : 1));
-                                        if (j < jstar || j > jmax) continue;
-                                        if (pair_exact(sv[(i + sg * j) * VP + lane], vp, -j, s,
-                                                       p.t_dist, p.t_disp)) { m = true; jl = j; }
-                                    }
-                                }
-                                for (int32_t j = jstar; j <= jmax && !m; ++j) {
-                                    if (pair_exact(sv[(i + sg * j) * VP + lane], vp, -j, s,
-                                                   p.t_dist, p.t_disp)) { m = true; jl = j; }
-                                }
-                            }
-                        }
-                    }
-                }
-                so[k * OPITCH + lane] = (uint8_t)m;
-            }
-        }
-        __syncthreads();    // sdcov / sagg reused by the next view
-    }
-    // ---- default thresholds: barrier-free bit-sliced sweeps, all views at once;
-    // a warp owns (view, pair of adjacent 32-position blocks)
-    if (!fs.nonfinite) {
+        // default thresholds: barrier-free bit-sliced sweeps of all views at
+        // once; a warp owns (view, pair of adjacent 32-position blocks)
         const int32_t nob = (TPe + 31) >> 5, npair = (nob + 1) >> 1;
         for (int u = warp; u < gd.nv * npair; u += NWARP) {
             const int g = u / npair, pr = u - g * npair;
             const ViewRegs cv = g == 0 ? vr[0] : vr[kGroupViews - 1];
             if (!(cv.staged && cv.nback == 2 && cv.jstar == 3 && cv.nfwd <= 1)) continue;
-            uint8_t *so = sout + (size_t)g * TP * OPITCH;
+            uint32_t *ow = outw + g * NOB * 32;
             const ViewDesc &vd = a.views[cv.vid];
             const float blo0 = vd.back_lo[0], bhi0 = vd.back_hi[0], blo1 = vd.back_lo[1],
                         bhi1 = vd.back_hi[1], flo0 = vd.fwd_lo[0], fhi0 = vd.fwd_hi[0];
@@ -669,58 +543,63 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
             const int16_t *ld = slast + d * NB * 32, *nd = snext + d * NB * 32;
             if (cv.sg > 0) {
                 if (cv.nfwd)
-                    sweep_bits<1, 1, VP>(sv, cwd, ld, nd, so, lane, bhi, nb, L0, NP32, NB32, cv.h, cv.s, cv.T,
-                                         cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
+                    sweep_bits<1, 1, VP>(sv, cwd, ld, nd, ow, sjg, lane, bhi, nb, L0, NP32, NB32, cv.h, cv.s,
+                                         cv.T, cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
                 else
-                    sweep_bits<1, 0, VP>(sv, cwd, ld, nd, so, lane, bhi, nb, L0, NP32, NB32, cv.h, cv.s, cv.T,
-                                         cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
+                    sweep_bits<1, 0, VP>(sv, cwd, ld, nd, ow, sjg, lane, bhi, nb, L0, NP32, NB32, cv.h, cv.s,
+                                         cv.T, cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
             } else {
                 if (cv.nfwd)
-                    sweep_bits<-1, 1, VP>(sv, cwd, ld, nd, so, lane, blo, nb, L0, NP32, NB32, cv.h, cv.s, cv.T,
-                                          cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
+                    sweep_bits<-1, 1, VP>(sv, cwd, ld, nd, ow, sjg, lane, blo, nb, L0, NP32, NB32, cv.h, cv.s,
+                                          cv.T, cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
                 else
-                    sweep_bits<-1, 0, VP>(sv, cwd, ld, nd, so, lane, blo, nb, L0, NP32, NB32, cv.h, cv.s, cv.T,
-                                          cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
+                    sweep_bits<-1, 0, VP>(sv, cwd, ld, nd, ow, sjg, lane, blo, nb, L0, NP32, NB32, cv.h, cv.s,
+                                          cv.T, cv.jr, blo0, bhi0, blo1, bhi1, flo0, fhi0, p.t_dist, p.t_disp);
             }
         }
     }
     __syncthreads();
 
     // ------------------------------------------------ 3. store (row-contiguous)
+    // mask bit of output position k (0 <= k < TPe) of line l
+    auto bit_at = [&](const uint32_t *ow, int32_t k, int32_t l) -> uint32_t {
+        return (ow[(k >> 5) * 32 + l] >> (k & 31)) & 1u;
+    };
 #pragma unroll 1
     for (int g = 0; g < gd.nv; ++g) {
-        const uint8_t *so = sout + (size_t)g * TP * OPITCH;
+        const uint32_t *ow = outw + g * NOB * 32;
         uint8_t *Mv = a.masks + ((int64_t)f * a.nviews + gd.view[g]) * HW;
         const bool al4 = ((W & 3) == 0) && ((l0 & 3) == 0) && ((P0 & 3) == 0) && geo.num() == 0;
         if (!xm && al4) {
-            // columns: each output row is 32 contiguous bytes -> 8 x 4-byte stores
-            for (int k = warp * 4 + (lane >> 3); k < TPe; k += NT / 8) {
-                const int32_t y = P0 + k, x = l0 + 4 * (lane & 7);
+            // columns: output row y = P0 + k holds lanes l0..l0+31 -> 4 lanes per thread
+            for (int t = tid; t < TPe * 8; t += NT) {
+                const int32_t k = t >> 3, q = t & 7;
+                const int32_t y = P0 + k, x = l0 + 4 * q;
                 if (y >= H || x >= W) continue;
-                const uint8_t *src = so + k * OPITCH + 4 * (lane & 7);
+                uint32_t w = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) w |= bit_at(ow, k, 4 * q + e) << (8 * e);
                 if (x + 3 < W) {
-                    __stcs(reinterpret_cast<uint32_t *>(Mv + (int64_t)y * W + x),
-                           *reinterpret_cast<const uint32_t *>(src));
+                    __stcs(reinterpret_cast<uint32_t *>(Mv + (int64_t)y * W + x), w);
                 } else {
-                    for (int e = 0; e < 4 && x + e < W; ++e) Mv[(int64_t)y * W + x + e] = src[e];
+                    for (int e = 0; e < 4 && x + e < W; ++e) Mv[(int64_t)y * W + x + e] = (uint8_t)(w >> (8 * e));
                 }
             }
             continue;
         }
         if (xm && al4) {
-            // rows: row l0 + l, positions [P0, P1) -> 4-byte packed stores
+            // rows: row l0 + l, positions [P0, P1): 4 mask bits -> 4 bytes per store
             const int32_t nq = (TPe + 3) >> 2;
             for (int t = tid; t < 32 * nq; t += NT) {
                 const int32_t l = t / nq, q = t - l * nq;
                 const int32_t y = l0 + l, x = P0 + 4 * q;
                 if (y >= H) continue;
-                const uint8_t *src = so + (4 * q) * OPITCH + l;
+                const uint32_t b4 = (ow[((4 * q) >> 5) * 32 + l] >> ((4 * q) & 31)) & 0xfu;
+                const uint32_t w = (b4 * 0x00204081u) & 0x01010101u;     // bit e -> byte e
                 if (x + 3 < P1) {
-                    const uint32_t w = (uint32_t)src[0] | ((uint32_t)src[OPITCH] << 8) |
-                                       ((uint32_t)src[2 * OPITCH] << 16) | ((uint32_t)src[3 * OPITCH] << 24);
                     __stcs(reinterpret_cast<uint32_t *>(Mv + (int64_t)y * W + x), w);
                 } else {
-                    for (int e = 0; e < 4 && x + e < P1; ++e) Mv[(int64_t)y * W + x + e] = src[e * OPITCH];
+                    for (int e = 0; e < 4 && x + e < P1; ++e) Mv[(int64_t)y * W + x + e] = (uint8_t)(w >> (8 * e));
                 }
             }
             continue;
@@ -731,7 +610,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                 if (y < 0 || y >= H) continue;
                 const int32_t x = l0 + lane + geo.fl(y);
                 if (x < 0 || x >= W) continue;
-                __stcs(Mv + (int64_t)y * W + x, so[k * OPITCH + lane]);
+                __stcs(Mv + (int64_t)y * W + x, (uint8_t)bit_at(ow, k, lane));
             }
         } else {
             const int32_t xs = max(P0, 0), xe = min(P1, W) - 1;
@@ -743,7 +622,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                 for (int32_t t = max(tlo, -l0) + warp; t <= min(thi, H - 1 - l0); t += NWARP) {
                     const int32_t x = nm > 0 ? t - lane : lane - t;
                     if (x < xs || x > xe) continue;
-                    __stcs(Mv + (int64_t)(l0 + t) * W + x, so[(x - P0) * OPITCH + lane]);
+                    __stcs(Mv + (int64_t)(l0 + t) * W + x, (uint8_t)bit_at(ow, x - P0, lane));
                 }
                 continue;
             }
@@ -754,7 +633,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
                 row_run(geo, y, l0, xs, xe, xa, xb);
                 for (int32_t x = xa + lane; x <= xb; x += 32) {
                     const int32_t l = y - l0 - geo.fl(x);
-                    __stcs(Mv + (int64_t)y * W + x, so[(x - P0) * OPITCH + l]);
+                    __stcs(Mv + (int64_t)y * W + x, (uint8_t)bit_at(ow, x - P0, l));
                 }
             }
         }
@@ -765,7 +644,7 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
 // 0 rows, 1 columns, 2 diagonal, 3 anti-diagonal, 4/5 x-major knight +-1/2,
 // 6/7 y-major knight +-1/2, 8 any other slope (runtime geometry).
 template <int CB>
-__global__ void __launch_bounds__(NT, 2) k_tile(TileArgs a) {
+__global__ void __launch_bounds__(NT, 3) k_tile(TileArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const TileDesc td = a.tiles[blockIdx.x];
     const GroupDesc gd = a.groups[td.group];

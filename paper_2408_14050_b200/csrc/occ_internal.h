@@ -96,7 +96,7 @@ cudaError_t launch_direct(const float *D, int32_t H, int32_t W, int32_t batch,
                           const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
                           const FrameStats *st, const Params &p, uint8_t *masks, cudaStream_t s);
 size_t tile_smem_bytes();
-constexpr int kTilePositions = 256;    // TP
+constexpr int kTilePositions = 224;    // TP (7 blocks of 32: smem for 3 CTAs per SM)
 constexpr int kTileHaloMax = 96;       // staged halo per side (multiple of 32)
 cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
                         const TileDesc *tiles, int32_t ntiles, const GroupDesc *groups,
