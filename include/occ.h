@@ -60,9 +60,12 @@ enum {
     OCC_ERR_UNSUPPORTED = -5    /* |bx| or |by| > 8, or too many views */
 };
 
-/* Paths (occ_set_path): AUTO picks the tiled sweep kernel and falls back to
- * the direct per-pixel kernel for frames whose scan half-length exceeds the
- * tile halo.  DIRECT forces the per-pixel kernel (debug / cross-check). */
+/* Paths (occ_set_path): AUTO runs the line-sweep kernel for the view pairs
+ * +-b of row / column / diagonal / anti-diagonal families under the default
+ * near/far split, and the tiled kernel for every other view group; both fall
+ * back in-kernel to the exact per-pixel routine for frames outside their
+ * staging range.  TILED forces the tiled kernel for every group; DIRECT the
+ * per-pixel kernel (debug / cross-check). */
 enum { OCC_PATH_AUTO = 0, OCC_PATH_TILED = 1, OCC_PATH_DIRECT = 2 };
 
 /* Fills the paper's defaults. */
@@ -116,7 +119,7 @@ int32_t occ_last_launches(const occ_ctx *ctx);
  * synchronises and returns, for one kernel kind, the summed device time in
  * milliseconds and the number of launches since the last reset. */
 enum { OCC_KERNEL_INIT = 0, OCC_KERNEL_STATS = 1, OCC_KERNEL_TILE = 2, OCC_KERNEL_DIRECT = 3,
-       OCC_KERNEL_CAND = 4, OCC_KERNEL_KINDS = 5 };
+       OCC_KERNEL_CAND = 4, OCC_KERNEL_LINE = 5, OCC_KERNEL_KINDS = 6 };
 int occ_profile(occ_ctx *ctx, int32_t enable);
 int occ_profile_read(occ_ctx *ctx, int32_t kind, double *total_ms, int32_t *launches);
 

@@ -7,6 +7,7 @@ built .so is self-contained on the GPU box.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -31,8 +32,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(p) for p in deps)
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= newest:
         return SO
-    cmd = [NVCC, *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", SO, *sources()]
-    subprocess.run(cmd, check=True)
+    # one object per translation unit, compiled in parallel, then linked
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    jobs = []
+    hdr_newest = max(os.path.getmtime(p) for p in deps if not p.endswith(".cu"))
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_newest):
+            continue
+        jobs.append([NVCC, *ARCH, *cflags, *(["-Xptxas", "-v"] if verbose else []), "-c", src, "-o", obj])
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, len(jobs))) as ex:
+        for r in ex.map(lambda c: subprocess.run(c, capture_output=not verbose, text=True), jobs):
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed: {' '.join(r.args)}\n{r.stderr}")
+    objs = [os.path.join(objdir, os.path.basename(src)[:-3] + ".o") for src in sources()]
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", SO, *objs], check=True)
     return SO
 
 

@@ -1,0 +1,945 @@
+// k_line.cu -- K2, the line-sweep kernel for the four line families of
+// |b| <= 1 camera arrays (rows, columns, diagonals, anti-diagonals): Eqs. 1-6
+// for a pair of views +-b of one family.
+//
+// One warp = one work unit: 32 consecutive digital epipolar lines (SURVEY
+// §8.0 S6; lane = line) x a segment of up to kLineSeg positions, one frame.
+// Every lane works in its own "time" coordinate tau = pos + off(lane)
+// (off = 0 for rows/columns, lane for diagonals, 31 - lane for
+// anti-diagonals) so that at every tau the 32 lanes read one coalesced run of
+// one image row (diagonals) or one row/column segment; all bit words below
+// are indexed by tau (bit r of block k <-> tau = 32k + r).
+//
+//  pass 0  candidate words (Eqs. 1-2, from K0's per-pixel codes) of both
+//          views for the segment +- (h + 32) positions, into shared memory.
+//  pass A  descending tau.  Per position: the shared Eq. 5 near tests of
+//          both views -- delta1 = fl(v[i+1] - v[i]) and delta2 = fl(v[i+2] -
+//          v[i]) against the exact fp32 interval bounds, reduced to sign bits
+//          of |delta| - bound and the sign of delta (view +b uses delta > 0,
+//          view -b delta < 0) -- and the far-partner filter of view +b (suffix
+//          max of A = s v - pos over q >= i + 3).  Per 32 positions: window
+//          coverage of both views as two threshold masks (previous / next
+//          candidate), the near marks, far survivors and
+//          their exact resolution, the +b mask store; the -b near marks are
+//          parked in shared memory.
+//  pass B  ascending tau: far filter of view -b (prefix max of s v + pos),
+//          exact resolution of its survivors, the -b mask store.
+// Far survivors (filter passed, no near mark, dcov >= 3) are resolved with
+// the exact Eq. 5 test (pair_exact): first at the offset of the line's last
+// far hit +-2, then at the offset suggested by the nearest edge candidate,
+// then by a warp-cooperative exhaustive search.  D is staged per warp in a
+// ring of kLineRingChunks x 32 positions (cp.async, coalesced); probes
+// outside the ring read global memory (L2).
+//
+// Frames the kernel cannot serve with this scheme (h < 17 or h + 32 beyond
+// the candidate margin) are computed by the exact per-pixel
+// routine (direct_pixel) inside the same warp.
+#include "occ_device.cuh"
+
+namespace occ {
+
+namespace {
+constexpr int SEGB = kLineSeg / 32;            // blocks per segment
+constexpr int RCH = kLineRingChunks;            // ring chunks (32 positions each)
+constexpr int RING = RCH * 32;
+constexpr int RP = 33;                          // ring pitch (floats per position)
+constexpr int CMW = kLineCandMarginWords;       // candidate margin words per side
+constexpr int NCW = SEGB + 2 * CMW;             // candidate words per view
+constexpr size_t OFF_RING = 0;
+constexpr size_t OFF_CW = OFF_RING + sizeof(float) * RING * RP;
+constexpr size_t OFF_NN = OFF_CW + sizeof(uint32_t) * 2 * NCW * 32;
+constexpr int QCAP = 256;                       // deferred hard survivors per warp
+constexpr size_t OFF_Q = OFF_NN + sizeof(uint32_t) * SEGB * 32;
+constexpr size_t WSMEM = OFF_Q + sizeof(int32_t) * 2 * QCAP;
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr int32_t NONE_LO = -(1 << 28), NONE_HI = (1 << 28);
+}  // namespace
+
+size_t line_smem_bytes() { return WSMEM; }
+
+// ------------------------------------------------------------ small helpers
+__device__ __forceinline__ uint32_t ge_mask(int32_t a) {      // bits r >= a
+    return a <= 0 ? FULL : (a >= 32 ? 0u : (FULL << a));
+}
+__device__ __forceinline__ uint32_t le_mask(int32_t b) {      // bits r <= b
+    return b < 0 ? 0u : (b >= 31 ? FULL : ((2u << b) - 1u));
+}
+// sign bit of x appended to w (w << 1 | sign(x))
+__device__ __forceinline__ uint32_t push(uint32_t w, float x) {
+    return __funnelshift_l(__float_as_uint(x), w, 1);
+}
+__device__ __forceinline__ uint32_t sgnbit(float x) { return __float_as_uint(x) >> 31; }
+// smallest float > a (finite a): x > a <=> x >= nextup(a) <=> !(fl(x - nextup(a)) < 0)
+__device__ __forceinline__ float nextup_f(float a) {
+    const int32_t b = __float_as_int(a);
+    if (a == 0.0f) return __int_as_float(1);
+    return __int_as_float(a > 0.0f ? b + 1 : b - 1);
+}
+__device__ __forceinline__ int slot_of(int32_t tau) {
+    if (RING == 128) return tau & 127;
+    int32_t m = tau % RING;
+    return m < 0 ? m + RING : m;
+}
+__device__ __forceinline__ void cp_async4(float *dst, const float *src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// 32x32 bit transpose across the warp: returns, for lane j, the word whose
+// bit l is bit j of lane l's input.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+    const uint32_t M[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int s = 16 >> k;
+        const uint32_t m = M[k];
+        const uint32_t y = __shfl_xor_sync(FULL, x, s);
+        x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+    }
+    return x;
+}
+// 4 mask bits -> 4 bytes 0/1
+__device__ __forceinline__ uint32_t expand4(uint32_t b4) { return (b4 * 0x00204081u) & 0x01010101u; }
+
+// warp-aggregated event counter (debug statistics only)
+__device__ __forceinline__ void dbg_add(unsigned long long *dbg, int idx, uint32_t n) {
+    if (!dbg) return;
+    const uint32_t tot = __reduce_add_sync(__activemask(), n);
+    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && tot) atomicAdd(dbg + idx, (unsigned long long)tot);
+}
+
+// ------------------------------------------------------------ line geometry
+// KIND 0 rows (line y, pos x), 1 columns (line x, pos y), 2 diagonals
+// (x-major, line y - x, pos x), 3 anti-diagonals (x-major, line y + x, pos x).
+template <int KIND>
+struct LG {
+    // pixel of lane l (line l0 + l) at time tau
+    static __device__ __forceinline__ void px(int32_t l0, int32_t l, int32_t tau, int32_t &x, int32_t &y) {
+        if (KIND == 0) { x = tau; y = l0 + l; }
+        else if (KIND == 1) { x = l0 + l; y = tau; }
+        else if (KIND == 2) { x = tau - l; y = l0 + tau; }
+        else { x = tau - 31 + l; y = l0 + 31 - tau; }
+    }
+    // in-image extent of lane l in tau: [lo, hi) (lo >= hi when empty)
+    static __device__ __forceinline__ void ext(int32_t l0, int32_t l, int32_t H, int32_t W,
+                                               int32_t &lo, int32_t &hi) {
+        const int32_t L = l0 + l;
+        if (KIND == 0) { lo = 0; hi = (L >= 0 && L < H) ? W : 0; }
+        else if (KIND == 1) { lo = 0; hi = (L >= 0 && L < W) ? H : 0; }
+        else if (KIND == 2) {
+            const int32_t a = max(0, -L), b = min(W, H - L);
+            lo = a + l; hi = max(a, b) + l;
+        } else {
+            const int32_t a = max(0, L - H + 1), b = min(W, L + 1);
+            lo = a + 31 - l; hi = max(a, b) + 31 - l;
+        }
+    }
+};
+
+// Every digital line is an arithmetic progression in memory: pixel index of
+// line l0 + l at time tau = base(l) + tau * stride.
+__device__ __forceinline__ int64_t line_base(int kind, int32_t l0, int32_t l, int32_t W) {
+    if (kind == 0) return (int64_t)(l0 + l) * W;
+    if (kind == 1) return (int64_t)(l0 + l);
+    if (kind == 2) return (int64_t)l0 * W - l;
+    return (int64_t)(l0 + 31) * W - 31 + l;
+}
+__device__ __forceinline__ int32_t line_stride(int kind, int32_t W) {
+    return kind == 0 ? 1 : (kind == 1 ? W : (kind == 2 ? W + 1 : 1 - W));
+}
+
+// runtime forms (the kind is warp-uniform: one code path for all families)
+__device__ __forceinline__ void lg_px(int kind, int32_t l0, int32_t l, int32_t tau, int32_t &x, int32_t &y) {
+    if (kind == 0) { x = tau; y = l0 + l; }
+    else if (kind == 1) { x = l0 + l; y = tau; }
+    else if (kind == 2) { x = tau - l; y = l0 + tau; }
+    else { x = tau - 31 + l; y = l0 + 31 - tau; }
+}
+__device__ __forceinline__ void lg_ext(int kind, int32_t l0, int32_t l, int32_t H, int32_t W, int32_t &lo,
+                                       int32_t &hi) {
+    if (kind == 0) LG<0>::ext(l0, l, H, W, lo, hi);
+    else if (kind == 1) LG<1>::ext(l0, l, H, W, lo, hi);
+    else if (kind == 2) LG<2>::ext(l0, l, H, W, lo, hi);
+    else LG<3>::ext(l0, l, H, W, lo, hi);
+}
+
+// ------------------------------------------------------------ candidate words
+// cw: one view's words [NCW][32] for tau blocks WB .. WB + NCW - 1.
+// Largest candidate tau <= x with tau >= lo (NONE_LO if none).
+__device__ __forceinline__ int32_t prev_cand(const uint32_t *cw, int32_t x, int32_t lo, int32_t WB, int lane) {
+    int32_t w = (x >> 5) - WB;
+    uint32_t m;
+    if (w >= NCW) { w = NCW - 1; m = cw[w * 32 + lane]; }
+    else if (w < 0) return NONE_LO;
+    else m = cw[w * 32 + lane] & le_mask(x & 31);
+    const int32_t wlo = max((lo >> 5) - WB, 0);
+    while (!m) {
+        if (--w < wlo) return NONE_LO;
+        m = cw[w * 32 + lane];
+    }
+    const int32_t c = (WB + w) * 32 + 31 - __clz(m);
+    return c >= lo ? c : NONE_LO;
+}
+// Smallest candidate tau >= x with tau <= hi (NONE_HI if none).
+__device__ __forceinline__ int32_t next_cand(const uint32_t *cw, int32_t x, int32_t hi, int32_t WB, int lane) {
+    int32_t w = (x >> 5) - WB;
+    uint32_t m;
+    if (w < 0) { w = 0; m = cw[lane]; }
+    else if (w >= NCW) return NONE_HI;
+    else m = cw[w * 32 + lane] & ge_mask(x & 31);
+    const int32_t whi = min((hi >> 5) - WB, NCW - 1);
+    while (!m) {
+        if (++w > whi) return NONE_HI;
+        m = cw[w * 32 + lane];
+    }
+    const int32_t c = (WB + w) * 32 + __ffs(m) - 1;
+    return c <= hi ? c : NONE_HI;
+}
+
+struct LineArgs {
+    const float *D;
+    int32_t H, W;
+    const LineUnit *units;
+    const GroupDesc *groups;
+    const ViewDesc *views;
+    int32_t nviews;
+    const FamilyDesc *fams;
+    const FrameStats *st;
+    Params p;
+    uint8_t *masks;
+    const void *codes;
+    unsigned long long *dbg;   // optional event counters (occ_debug_line_stats), or null
+    int32_t frames;
+};
+
+// Per-warp context
+struct Ctx {
+    unsigned long long *dbg;
+    int32_t kind;              // line family (0 rows, 1 columns, 2 diagonals, 3 anti-diagonals)
+    const float *Df;
+    int32_t H, W, l0, lane;
+    int32_t elo, ehi;          // lane's extent in tau
+    float *ring;               // warp's ring (float [RING][RP])
+    int64_t B;                 // lane's line: pixel index = B + tau * S
+    int32_t S;
+    const float *col;          // ring + lane
+};
+
+__device__ __forceinline__ float gload(const Ctx &c, int32_t l, int32_t tau) {
+    const int64_t b = l == c.lane ? c.B : line_base(c.kind, c.l0, l, c.W);
+    return __ldg(c.Df + b + (int64_t)tau * c.S);
+}
+
+// fill one chunk (32 tau) of the ring with cp.async (NaN outside the image)
+__device__ __forceinline__ void fill_chunk(const Ctx &c, int32_t k) {
+    const float NaN = __int_as_float(0x7fc00000);
+    const int lane = c.lane;
+    const int32_t t0 = 32 * k;
+    float *dst0 = c.ring + slot_of(t0) * RP;          // the 32 slots of a chunk are contiguous
+    if (c.kind == 0) {
+        // rows: lane = position, one coalesced row segment per line j
+        const int32_t x = t0 + lane;
+        const int32_t nrow = (x >= 0 && x < c.W) ? min(32, c.H - c.l0) : 0;
+        const float *src = c.Df + (int64_t)c.l0 * c.W + x;
+        float *dst = dst0 + lane * RP;
+        if (nrow == 32) {
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) cp_async4(dst + j, src + (int64_t)j * c.W);
+        } else {
+            for (int j = 0; j < 32; ++j) {
+                if (j < nrow) cp_async4(dst + j, src + (int64_t)j * c.W); else dst[j] = NaN;
+            }
+        }
+    } else {
+        // lane = line: one coalesced run per tau (row segment / skewed row)
+        const float *src = c.Df + c.B + (int64_t)t0 * c.S;
+        float *dst = dst0 + lane;
+        if (t0 >= c.elo && t0 + 32 <= c.ehi) {
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) cp_async4(dst + j * RP, src + (int64_t)j * c.S);
+        } else {
+            for (int j = 0; j < 32; ++j) {
+                const int32_t tau = t0 + j;
+                if (tau >= c.elo && tau < c.ehi) cp_async4(dst + j * RP, src + (int64_t)j * c.S);
+                else dst[j * RP] = NaN;
+            }
+        }
+    }
+}
+
+template <int CB>
+__device__ __forceinline__ uint32_t code_at(const void *codes, int64_t idx) {
+    if (CB == 1) return __ldg(reinterpret_cast<const uint8_t *>(codes) + idx);
+    if (CB == 2) return __ldg(reinterpret_cast<const uint16_t *>(codes) + idx);
+    return __ldg(reinterpret_cast<const uint32_t *>(codes) + idx);
+}
+
+// pass 0: candidate words of both views (bit cb and cb + 1 of the codes)
+template <int CB>
+__device__ __forceinline__ void build_cand(const Ctx &c, const void *codesf, int32_t cb, int32_t WB,
+                                           uint32_t *cw) {
+    const int lane = c.lane;
+    for (int w = 0; w < NCW; ++w) {
+        const int32_t t0 = 32 * (WB + w);
+        uint32_t wp = 0u, wn = 0u;
+        if (t0 + 31 >= c.elo && t0 < c.ehi) {
+            if (c.kind == 0 && CB == 1 && (c.W & 15) == 0 && t0 >= 0 && t0 + 32 <= c.W) {
+                // rows: 32 consecutive codes of the lane's row in two 16-byte loads
+                const uint8_t *row = reinterpret_cast<const uint8_t *>(codesf) + (int64_t)(c.l0 + lane) * c.W + t0;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint4 q = __ldg(reinterpret_cast<const uint4 *>(row + 16 * hh));
+                    const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t tp = (u[e] >> cb) & 0x01010101u;
+                        const uint32_t tn = (u[e] >> (cb + 1)) & 0x01010101u;
+                        wp |= ((tp * 0x10204080u) >> 28) << (16 * hh + 4 * e);
+                        wn |= ((tn * 0x10204080u) >> 28) << (16 * hh + 4 * e);
+                    }
+                }
+            } else if (t0 >= c.elo && t0 + 32 <= c.ehi) {
+                const int64_t i0 = c.B + (int64_t)t0 * c.S;
+#pragma unroll 8
+                for (int j = 31; j >= 0; --j) {
+                    const uint32_t code = code_at<CB>(codesf, i0 + (int64_t)j * c.S) >> cb;
+                    wp = (wp << 1) | (code & 1u);
+                    wn = (wn << 1) | ((code >> 1) & 1u);
+                }
+            } else {
+                for (int j = 31; j >= 0; --j) {
+                    const int32_t tau = t0 + j;
+                    uint32_t code = 0u;
+                    if (tau >= c.elo && tau < c.ehi) code = code_at<CB>(codesf, c.B + (int64_t)tau * c.S) >> cb;
+                    wp = (wp << 1) | (code & 1u);
+                    wn = (wn << 1) | ((code >> 1) & 1u);
+                }
+            }
+        }
+        cw[(0 * NCW + w) * 32 + lane] = wp;
+        cw[(1 * NCW + w) * 32 + lane] = wn;
+    }
+}
+
+// Window coverage of view +b for the 32 positions tau0 + r (SURVEY App. A.2,
+// h >= 17): covered_k(i) <=> a candidate lies in [i + k - h, i + h]
+//   = [i >= fc - h] or [i <= pcl + h - k],
+// fc = first candidate >= tau0 + h, pcl = last candidate <= tau0 + h - 1.
+struct CovP { int32_t fc, pcl; };
+__device__ __forceinline__ CovP cov_p(const uint32_t *cw, int32_t tau0, int32_t h, int32_t WB, int lane) {
+    CovP r;
+    r.fc = next_cand(cw, tau0 + h, tau0 + 31 + h, WB, lane);
+    r.pcl = prev_cand(cw, tau0 + h - 1, tau0 - h, WB, lane);
+    return r;
+}
+__device__ __forceinline__ uint32_t cov_p_k(const CovP &v, int32_t tau0, int32_t h, int32_t k) {
+    return ge_mask(v.fc - h - tau0) | le_mask(v.pcl + h - k - tau0);
+}
+// forward pair (i - 1, i): covered_1(i - 1)
+__device__ __forceinline__ uint32_t cov_p_f(const CovP &v, int32_t tau0, int32_t h) {
+    return ge_mask(v.fc - h + 1 - tau0) | le_mask(v.pcl + h - tau0);
+}
+// view -b (backward = lower tau): covered_k(i) <=> candidate in [i - h, i - k + h]
+//   = [i <= lc + h] or [i >= ncl + k - h],
+// lc = last candidate <= tau0 + 31 - h, ncl = first candidate >= tau0 + 32 - h.
+struct CovN { int32_t lc, ncl; };
+__device__ __forceinline__ CovN cov_n(const uint32_t *cw, int32_t tau0, int32_t h, int32_t WB, int lane) {
+    CovN r;
+    r.lc = prev_cand(cw, tau0 + 31 - h, tau0 - h, WB, lane);
+    r.ncl = next_cand(cw, tau0 + 32 - h, tau0 + 31 + h, WB, lane);
+    return r;
+}
+__device__ __forceinline__ uint32_t cov_n_k(const CovN &v, int32_t tau0, int32_t h, int32_t k) {
+    return le_mask(v.lc + h - tau0) | ge_mask(v.ncl + k - h - tau0);
+}
+// forward pair (i, i + 1): covered_1(i + 1)
+__device__ __forceinline__ uint32_t cov_n_f(const CovN &v, int32_t tau0, int32_t h) {
+    return le_mask(v.lc + h - 1 - tau0) | ge_mask(v.ncl - h - tau0);
+}
+
+struct ViewK {
+    int32_t s, h;
+    float fs;              // (float)s
+    float T;               // far-filter margin
+    float tlo, thi;        // t_dist -+ 2^-10: fp32 fast path of the exact Eq. 5 test
+};
+
+// Per-block context of the far-survivor resolution.
+struct Blk {
+    int32_t tau0, base;    // block start and its ring slot
+    int32_t wlo, whi;      // ring window (tau) valid during this block
+    uint32_t Wc;           // candidate bits of [tau0 + h, +31] (+b) / [tau0 - h, +31] (-b)
+    int32_t cfall;         // last candidate < tau0 + h (+b) / first candidate >= tau0 + 32 - h (-b)
+};
+
+__device__ __forceinline__ int32_t ring_slot(const Blk &b, int32_t tau) {
+    int32_t x = b.base + (tau - b.tau0);
+    x = x >= RING ? x - RING : x;
+    return x < 0 ? x + RING : x;
+}
+// value of line l at tau: ring inside the block's window, else global; NaN outside the line
+__device__ __forceinline__ float probe_b(const Ctx &c, const Blk &b, int32_t l, int32_t tau, int32_t elo,
+                                         int32_t ehi) {
+    if (tau < elo || tau >= ehi) return __int_as_float(0x7fc00000);
+    if (tau >= b.wlo && tau <= b.whi) return c.ring[ring_slot(b, tau) * RP + l];
+    if (c.dbg) atomicAdd(c.dbg + 6, 1ull);
+    return gload(c, l, tau);
+}
+// dcov of the survivor at tau0 + r (largest far offset sharing a scan window, App. A.2)
+template <int DIR>
+__device__ __forceinline__ int32_t dcov_of(uint32_t Wc, int32_t cfall, int32_t tau0, int32_t r, int32_t h) {
+    if (DIR > 0) {
+        const uint32_t m = Wc & le_mask(r);
+        const int32_t pc = m ? tau0 + h + 31 - __clz(m) : cfall;
+        return pc + h - (tau0 + r);
+    }
+    const uint32_t m = Wc & ge_mask(r);
+    const int32_t nc = m ? tau0 - h + __ffs(m) - 1 : cfall;
+    return tau0 + r + h - nc;
+}
+// Eq. 5 for a far pair (offset j >= jstar, so delta > t_disp is implied):
+// |s fl(vq - vp) - j| < t_dist.  s delta is exact; one rounding in the fma,
+// far below the 2^-10 band; inside the band the binary64 test decides.
+__device__ __forceinline__ bool pair_far(float vq, float vp, int32_t j, const ViewK &vk, const Params &p) {
+    const float d = __fsub_rn(vq, vp);
+    const float x = fabsf(__fmaf_rn(vk.fs, d, -(float)j));
+    if (x < vk.tlo) return true;
+    if (!(x <= vk.thi)) return false;
+    return pair_exact(vq, vp, -j, vk.s, p.t_dist, p.t_disp);
+}
+
+// Deferred exhaustive searches: one lane per queued survivor (tau, dcov,
+// line), scanning offsets 3..dcov of its line in global memory (L2) with 16
+// loads in flight; a confirmed Eq. 5 pair sets the mask byte directly (the
+// block store already wrote 0 there).
+template <int DIR>
+__device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int32_t qn, const ViewK &vk,
+                                         const Params &p, uint8_t *Mv) {
+    __syncwarp();
+    const float NaN = __int_as_float(0x7fc00000);
+    for (int32_t e0 = 0; e0 < qn; e0 += 32) {
+        const int32_t e = e0 + c.lane;
+        if (e < qn) {
+            const int32_t tau = qbuf[2 * e], w = qbuf[2 * e + 1];
+            const int32_t src = w & 31, jm = w >> 5;
+            const float *Ds = c.Df + line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S;
+            const int32_t st = DIR * c.S;
+            const float vp = __ldg(Ds);
+            bool hit = false;
+            for (int32_t j0 = 3; j0 <= jm && !hit; j0 += 16) {
+                float vq[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * st) : NaN;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
+            }
+            dbg_add(c.dbg, 4, hit ? 1u : 0u);
+            if (hit) Mv[line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S] = 1;
+        }
+    }
+    __syncwarp();
+}
+
+// Appends the survivors of `bits` (bit r <-> tau0 + r) to the deferred queue,
+// at most `quota` per lane; returns the bits not queued.  Warp-collective;
+// the caller guarantees room for 32 * quota entries.
+template <int DIR>
+__device__ __forceinline__ uint32_t queue_bits(const Ctx &c, const Blk &b, int32_t h, uint32_t bits,
+                                               int quota, int32_t *qbuf, int32_t &qn) {
+    const int lane = c.lane;
+    uint32_t take = 0u, t = bits;
+    for (int i = 0; i < quota && t; ++i) { const uint32_t lb = t & (0u - t); take |= lb; t ^= lb; }
+    const uint32_t n = __popc(take);
+    uint32_t inc = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t tt = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += tt;
+    }
+    const int32_t tot = (int32_t)__shfl_sync(FULL, inc, 31);
+    int32_t pos = qn + (int32_t)(inc - n);
+    uint32_t w = take;
+    while (w) {
+        const int32_t r = __ffs(w) - 1;
+        w &= w - 1u;
+        const int32_t tau = b.tau0 + r;
+        int32_t jm = dcov_of<DIR>(b.Wc, b.cfall, b.tau0, r, h);
+        jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
+        qbuf[2 * pos] = tau;
+        qbuf[2 * pos + 1] = (max(jm, 0) << 5) | lane;
+        ++pos;
+    }
+    qn += tot;
+    __syncwarp();
+    return bits & ~take;
+}
+
+// Exact resolution of far survivors S (bit r <-> tau0 + r) of one view.
+// DIR = +1: partners at tau + j (view +b), -1: at tau - j (view -b).
+// These are the survivors the sweep's witness probe did not confirm: first
+// the line's last far offset -1..+2, then a warp-cooperative exhaustive search.
+template <int DIR>
+__device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b, const ViewK &vk,
+                                         const Params &p, int32_t &jl, int32_t *qbuf, int32_t &qn,
+                                         uint8_t *Mv, uint32_t &left) {
+    const int lane = c.lane;
+    const int32_t h = vk.h;
+    uint32_t hits = 0u, hard = 0u;
+    dbg_add(c.dbg, DIR > 0 ? 0 : 1, __popc(S));
+    while (__any_sync(FULL, S != 0u)) {
+        dbg_add(c.dbg, 9, 1u);
+        if (S) {
+            const int32_t r = DIR > 0 ? 31 - __clz(S) : __ffs(S) - 1;
+            S &= ~(1u << r);
+            const int32_t tau = b.tau0 + r;
+            const float vp = c.col[(b.base + r) * RP];
+            int32_t jm = dcov_of<DIR>(b.Wc, b.cfall, b.tau0, r, h);
+            jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
+            bool hit = false;
+            // the line's last far offset, its neighbours, and one secant step
+            // from it (A falls ~1 per step along an occluder: the residual
+            // y = s delta - j is the remaining distance)
+            float y0 = 0.0f;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                int32_t j = q == 0 ? jl : (q == 1 ? jl - 1 : (q == 2 ? jl + 1 : jl + (int32_t)rintf(y0)));
+                if (q == 3 && (j == jl || j == jl - 1 || j == jl + 1)) j = -1;
+                if (!hit && j >= 3 && j <= jm) {
+                    const float vq = probe_b(c, b, lane, tau + DIR * j, c.elo, c.ehi);
+                    if (q == 0) {
+                        const float yy = __fmaf_rn(vk.fs, __fsub_rn(vq, vp), -(float)j);
+                        y0 = (yy == yy) ? fminf(fmaxf(yy, -64.0f), 64.0f) : 0.0f;
+                    }
+                    if (pair_far(vq, vp, j, vk, p)) { hit = true; jl = j; }
+                }
+            }
+            if (hit) hits |= 1u << r; else hard |= 1u << r;
+        }
+    }
+    dbg_add(c.dbg, 2, __popc(hits));
+    dbg_add(c.dbg, 3, __popc(hard));
+    // queue the rest for the deferred lane-parallel search.  Flushing here is
+    // safe: the queue holds only earlier blocks, whose masks are stored.
+    // More than QCAP at once (rare): the remainder is returned in `left` and
+    // queued by the caller after this block's mask store.
+    {
+        const int32_t tot = __reduce_add_sync(FULL, __popc(hard));
+        if (lane == 0) dbg_add(c.dbg, 10, tot > QCAP ? 1u : 0u);
+        if (qn + tot > QCAP) {
+            flush_queue<DIR>(c, qbuf, qn, vk, p, Mv);
+            qn = 0;
+        }
+        left = queue_bits<DIR>(c, b, h, hard, tot <= QCAP ? 32 : QCAP / 32, qbuf, qn);
+    }
+    return hits;
+}
+
+// candidate bits of [x, x + 31] from one view's words (0 outside the staged range)
+__device__ __forceinline__ uint32_t cand_bits32(const uint32_t *cw, int32_t x, int32_t WB, int lane) {
+    const int32_t w = (x >> 5) - WB, sh = x & 31;
+    const uint32_t lo = (w >= 0 && w < NCW) ? cw[w * 32 + lane] : 0u;
+    const uint32_t hi = (w + 1 >= 0 && w + 1 < NCW) ? cw[(w + 1) * 32 + lane] : 0u;
+    return __funnelshift_r(lo, hi, sh);
+}
+
+// mask bytes of one view for the 32 tau of block k (bit r <-> tau = 32k + r)
+__device__ __noinline__ void store_block(const Ctx &c, uint8_t *Mv, uint32_t word, int32_t k) {
+    const int lane = c.lane;
+    const int32_t H = c.H, W = c.W;
+    if (c.kind == 0) {
+        const int32_t y = c.l0 + lane, x0 = 32 * k;
+        if (y < 0 || y >= H) return;
+        uint8_t *row = Mv + (int64_t)y * W;
+        if ((W & 15) == 0 && x0 >= 0 && x0 + 32 <= W) {
+            uint4 *d = reinterpret_cast<uint4 *>(row + x0);
+            __stcs(d, make_uint4(expand4(word & 15u), expand4((word >> 4) & 15u),
+                                 expand4((word >> 8) & 15u), expand4((word >> 12) & 15u)));
+            __stcs(d + 1, make_uint4(expand4((word >> 16) & 15u), expand4((word >> 20) & 15u),
+                                     expand4((word >> 24) & 15u), expand4(word >> 28)));
+        } else {
+            for (int r = 0; r < 32; ++r) {
+                const int32_t x = x0 + r;
+                if (x >= 0 && x < W) row[x] = (uint8_t)((word >> r) & 1u);
+            }
+        }
+    } else if (c.kind == 1) {
+        const uint32_t t = transpose32(word, lane);      // lane r: row y = 32k + r, bit l = column l0 + l
+        const int32_t y = 32 * k + lane;
+        if (y < 0 || y >= H) return;
+        uint8_t *row = Mv + (int64_t)y * W;
+        if ((W & 15) == 0 && c.l0 >= 0 && c.l0 + 32 <= W && (c.l0 & 15) == 0) {
+            uint4 *d = reinterpret_cast<uint4 *>(row + c.l0);
+            __stcs(d, make_uint4(expand4(t & 15u), expand4((t >> 4) & 15u), expand4((t >> 8) & 15u),
+                                 expand4((t >> 12) & 15u)));
+            __stcs(d + 1, make_uint4(expand4((t >> 16) & 15u), expand4((t >> 20) & 15u),
+                                     expand4((t >> 24) & 15u), expand4(t >> 28)));
+        } else {
+            for (int l = 0; l < 32; ++l) {
+                const int32_t x = c.l0 + l;
+                if (x >= 0 && x < W) row[x] = (uint8_t)((t >> l) & 1u);
+            }
+        }
+    } else {
+        // one image row per tau: the 32 lanes write one contiguous (reversed) run
+        uint8_t *dst = Mv + c.B + (int64_t)(32 * k) * c.S;
+        if (32 * k >= c.elo && 32 * k + 32 <= c.ehi) {
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) __stcs(dst + (int64_t)r * c.S, (uint8_t)((word >> r) & 1u));
+        } else {
+            for (int r = 0; r < 32; ++r) {
+                const int32_t tau = 32 * k + r;
+                if (tau >= c.elo && tau < c.ehi) __stcs(dst + (int64_t)r * c.S, (uint8_t)((word >> r) & 1u));
+            }
+        }
+    }
+}
+
+// exact per-pixel fallback for the unit (frames outside the sweep's range of h)
+__device__ __noinline__ void unit_direct(const Ctx &c, const LineArgs &a, const GroupDesc &gd,
+                                         const FamilyDesc &fd, int32_t f, int32_t T0, int32_t T1,
+                                         bool zero) {
+    const int64_t HW = (int64_t)c.H * c.W;
+    const float R = frame_range(a.st[f]);
+    for (int g = 0; g < gd.nv; ++g) {
+        const ViewDesc &vd = a.views[gd.view[g]];
+        const int32_t h = view_h(R, vd.s, a.p.max_scan);
+        uint8_t *Mv = a.masks + ((int64_t)f * a.nviews + gd.view[g]) * HW;
+        for (int32_t tau = max(T0, c.elo); tau < min(T1, c.ehi); ++tau) {
+            int32_t x, y;
+            lg_px(c.kind, c.l0, c.lane, tau, x, y);
+            const bool m = !zero && direct_pixel<false>(c.Df, c.H, c.W, vd, fd, a.p, h, x, y);
+            Mv[(int64_t)y * c.W + x] = (uint8_t)m;
+        }
+    }
+}
+
+template <int CB>
+__device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, const GroupDesc &gd,
+                                          const FamilyDesc &fd, int32_t f, unsigned char *smem) {
+    const int kind = fd.kind;
+    const bool NFWD = a.views[gd.view[0]].nfwd > 0;
+    const int lane = threadIdx.x & 31;
+    const int32_t H = a.H, W = a.W;
+    const int64_t HW = (int64_t)H * W;
+    Ctx c;
+    c.dbg = a.dbg;
+    c.kind = kind;
+    c.Df = a.D + (int64_t)f * HW;
+    c.H = H; c.W = W; c.l0 = u.l0; c.lane = lane;
+    lg_ext(kind, u.l0, lane, H, W, c.elo, c.ehi);
+    c.B = line_base(kind, u.l0, lane, W);
+    c.S = line_stride(kind, W);
+    c.ring = reinterpret_cast<float *>(smem + OFF_RING);
+    c.col = c.ring + lane;
+    uint32_t *cw = reinterpret_cast<uint32_t *>(smem + OFF_CW);
+    uint32_t *nn = reinterpret_cast<uint32_t *>(smem + OFF_NN);
+    int32_t *qbuf = reinterpret_cast<int32_t *>(smem + OFF_Q);
+    int32_t qn = 0;
+    const int32_t T0 = u.t0, T1 = u.t1;            // multiples of 32
+    const int32_t kB = T0 >> 5, kT = (T1 >> 5) - 1;
+
+    // views: P = +b0 (sg > 0), N = -b0
+    int32_t vP = -1, vN = -1;
+    for (int g = 0; g < gd.nv; ++g) {
+        if (a.views[gd.view[g]].sg > 0) vP = gd.view[g]; else vN = gd.view[g];
+    }
+    const ViewDesc &vd0 = a.views[vP >= 0 ? vP : vN];
+    const FrameStats fs = a.st[f];
+    const float R = frame_range(fs);
+    const int32_t s = vd0.s;
+    const int32_t h = view_h(R, s, a.p.max_scan);
+    if (fs.nonfinite || h <= 0) {            // SPEC.md:76 reject / Q17: zero masks
+        unit_direct(c, a, gd, fd, f, T0, T1, true);
+        return;
+    }
+    if (h < 17 || h + 32 > 32 * CMW) {
+        dbg_add(c.dbg, 8, 1u);
+        unit_direct(c, a, gd, fd, f, T0, T1, false);
+        return;
+    }
+    const float M = fmaxf(fabsf(key_float(fs.minkey)), fabsf(key_float(fs.maxkey)));
+    ViewK vk;
+    vk.s = s; vk.h = h; vk.fs = (float)s;
+    vk.tlo = __fsub_rn(a.p.t_dist, 0x1p-10f);
+    vk.thi = __fadd_rn(a.p.t_dist, 0x1p-10f);
+    {
+        const double eps = ldexp(1.0, -19) * ((double)s * (double)M + 4096.0 + (double)a.p.t_dist);
+        vk.T = __double2float_ru(__dadd_rn((double)a.p.t_dist, eps));
+    }
+    const int32_t reach = min(2 * h, (int32_t)floor(__dadd_rn((double)a.p.t_dist,
+                                                               __dmul_rn((double)s, (double)R))) + 1);
+    const int32_t nbr = (reach + 3 + 31) >> 5;
+    // thresholds (identical for the two views of the group)
+    const float a1n = nextup_f(vd0.back_lo[0]), bhi0 = vd0.back_hi[0];
+    const float a2n = nextup_f(vd0.back_lo[1]), bhi1 = vd0.back_hi[1];
+    const float fhi0 = NFWD ? vd0.fwd_hi[0] : 0.0f;
+    const float fs_ = (float)s;
+    int32_t kEmin = c.elo >> 5, kEmax = (c.ehi - 1) >> 5;
+    if (c.elo >= c.ehi) { kEmin = 1 << 20; kEmax = -(1 << 20); }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kEmin = min(kEmin, __shfl_xor_sync(FULL, kEmin, o));
+        kEmax = max(kEmax, __shfl_xor_sync(FULL, kEmax, o));
+    }
+
+    // ---------------------------------------------------- pass 0: candidates
+    const int32_t WB = kB - CMW;
+    {
+        const unsigned char *codesf = reinterpret_cast<const unsigned char *>(a.codes) + (int64_t)f * HW * CB;
+        build_cand<CB>(c, codesf, 2 * gd.fam, WB, cw);
+    }
+    const uint32_t *cwP = cw, *cwN = cw + NCW * 32;
+    __syncwarp();
+
+    const float NaN = __int_as_float(0x7fc00000);
+    uint8_t *MP = vP >= 0 ? a.masks + ((int64_t)f * a.nviews + vP) * HW : nullptr;
+    uint8_t *MN = vN >= 0 ? a.masks + ((int64_t)f * a.nviews + vN) * HW : nullptr;
+
+    // ---------------------------------------------------- pass A (descending)
+    // Far filter of view +b: SX = max A(q) over q >= i + 3, A = s v - pos, with
+    // its witness SA.  Past the witness A falls ~1 per step on a flat
+    // occluder, so the Eq. 5 partner of i sits near offset
+    // jw = (SA - i) + max(SX - A_i, 0); it is probed at every position (exact
+    // fp32 test, clamped to offsets <= dcov(i), so every confirmed pair is a
+    // far mark).
+    {
+        const int32_t kS = max(min(kT + nbr, kEmax), kT);
+        float v1 = NaN, v2 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY;
+        int32_t SA = 0, jl = 0;
+        fill_chunk(c, kS + 1);               // guard chunk for the witness probes of block kS
+        fill_chunk(c, kS); cp_commit();
+        if (kS - 1 >= kB - 1) fill_chunk(c, kS - 1);
+        cp_commit();
+        for (int32_t k = kS; k >= kB; --k) {
+            __syncwarp();
+            if (k - 2 >= kB - 1) fill_chunk(c, k - 2);
+            cp_commit();
+            cp_wait<1>();
+            __syncwarp();
+            const int base = slot_of(32 * k);
+            const float *cb = c.col + base * RP;
+            float ip = (float)(32 * k + 31 - T0);
+            if (k > kT) {
+                // start-up: suffix max only
+#pragma unroll 8
+                for (int r = 31; r >= 0; --r) {
+                    const float v0 = cb[r * RP];
+                    const float A0 = __fmaf_rn(fs_, v0, -ip);
+                    if (A3 > SX) { SX = A3; SA = 32 * k + r + 3; }
+                    A3 = A2; A2 = A1; A1 = A0; v2 = v1; v1 = v0;
+                    ip = __fsub_rn(ip, 1.0f);
+                }
+                continue;
+            }
+            const int32_t tau0 = 32 * k;
+            const CovP cp = cov_p(cwP, tau0, h, WB, lane);
+            // probe offsets j <= dcov(i) = pc(i + h) + h - i (covered) and inside
+            // the ring window (tau + j <= min(tau0 + 95, 32 kS + 34)); pc from the
+            // candidate bits of [tau0 + h, tau0 + h + 31]
+            const uint32_t Wh = cand_bits32(cwP, tau0 + h, WB, lane);
+            const int32_t hh = tau0 + h + 31, eA = h - tau0;
+            const int32_t wtop = min(32 * (RCH - 2) - 1, 32 * kS + 34 - tau0);
+            uint32_t Xs1 = 0, Xg1 = 0, Xl1 = 0, Xlf = 0, Xs2 = 0, Xg2 = 0, Xl2 = 0, XFR = 0, XH = 0;
+#pragma unroll 8
+            for (int r = 31; r >= 0; --r) {
+                const float v0 = cb[r * RP];
+                const float d1 = __fsub_rn(v1, v0), d2 = __fsub_rn(v2, v0);
+                const float e1 = fabsf(d1), e2 = fabsf(d2);
+                Xs1 = push(Xs1, d1);
+                Xg1 = push(Xg1, __fsub_rn(e1, a1n));
+                Xl1 = push(Xl1, __fsub_rn(e1, bhi0));
+                Xlf = push(Xlf, __fsub_rn(e1, fhi0));
+                Xs2 = push(Xs2, d2);
+                Xg2 = push(Xg2, __fsub_rn(e2, a2n));
+                Xl2 = push(Xl2, __fsub_rn(e2, bhi1));
+                const float A0 = __fmaf_rn(fs_, v0, -ip);
+                if (A3 > SX) { SX = A3; SA = tau0 + r + 3; }
+                XFR = push(XFR, __fsub_rn(__fsub_rn(A0, vk.T), SX));
+                {   // witness probe
+                    const uint32_t m = Wh & (r == 31 ? FULL : ((2u << r) - 1u));
+                    const int32_t pcr = m ? hh - __clz(m) : cp.pcl;
+                    // partner guess: past the witness SA, A falls ~1 per step on a flat occluder
+                    const float g = fminf(fmaxf(__fsub_rn(SX, A0), 0.0f), 4096.0f);
+                    const int32_t jw = max(3, min(SA - (tau0 + r) + __float2int_rn(g), min(pcr + eA, wtop) - r));
+                    int32_t sl = base + r + jw;
+                    sl = sl >= RING ? sl - RING : sl;
+                    const float x = __fsub_rn(fabsf(__fmaf_rn(fs_, __fsub_rn(c.col[sl * RP], v0), -(float)jw)), vk.tlo);
+                    XH = push(XH, x);
+                    jl = x < 0.0f ? jw : jl;
+                }
+                A3 = A2; A2 = A1; A1 = A0; v2 = v1; v1 = v0;
+                ip = __fsub_rn(ip, 1.0f);
+            }
+            // tails: delta1 at 32k - 1, delta2 at 32k - 1 and 32k - 2
+            const float vm1 = c.col[slot_of(32 * k - 1) * RP], vm2 = c.col[slot_of(32 * k - 2) * RP];
+            const float d1m = __fsub_rn(v1, vm1), d2m1 = __fsub_rn(v2, vm1), d2m2 = __fsub_rn(v1, vm2);
+            const uint32_t s1m = sgnbit(d1m), g1m = sgnbit(__fsub_rn(fabsf(d1m), a1n));
+            const uint32_t t1m = (g1m ^ 1u) & sgnbit(__fsub_rn(fabsf(d1m), bhi0));
+            const uint32_t tfm = NFWD ? ((g1m ^ 1u) & sgnbit(__fsub_rn(fabsf(d1m), fhi0))) : 0u;
+            const uint32_t t2m1 = (sgnbit(__fsub_rn(fabsf(d2m1), a2n)) ^ 1u) & sgnbit(__fsub_rn(fabsf(d2m1), bhi1));
+            const uint32_t t2m2 = (sgnbit(__fsub_rn(fabsf(d2m2), a2n)) ^ 1u) & sgnbit(__fsub_rn(fabsf(d2m2), bhi1));
+            const uint32_t s2m1 = sgnbit(d2m1), s2m2 = sgnbit(d2m2);
+            const uint32_t T1 = ~Xg1 & Xl1, T2 = ~Xg2 & Xl2, TF = NFWD ? (~Xg1 & Xlf) : 0u;
+            // view -b near marks (parked for pass B)
+            if (vN >= 0) {
+                const CovN cn = cov_n(cwN, tau0, h, WB, lane);
+                const uint32_t n1 = ((T1 & Xs1) << 1) | (t1m & s1m);
+                const uint32_t n2 = ((T2 & Xs2) << 2) | ((t2m1 & s2m1) << 1) | (t2m2 & s2m2);
+                uint32_t mN = (n1 & cov_n_k(cn, tau0, h, 1)) | (n2 & cov_n_k(cn, tau0, h, 2));
+                if (NFWD) mN |= (TF & ~Xs1) & cov_n_f(cn, tau0, h);
+                nn[(k - kB) * 32 + lane] = mN;
+            }
+            if (vP >= 0) {
+                const uint32_t C3 = cov_p_k(cp, tau0, h, 3);
+                uint32_t mP = ((T1 & ~Xs1) & cov_p_k(cp, tau0, h, 1)) | ((T2 & ~Xs2) & cov_p_k(cp, tau0, h, 2));
+                if (NFWD) mP |= (((TF & Xs1) << 1) | (tfm & s1m)) & cov_p_f(cp, tau0, h);
+                mP |= XH & C3;
+                const uint32_t surv = XFR & C3 & ~mP;
+                uint32_t left = 0u;
+                Blk b;
+                if (__any_sync(FULL, surv != 0u)) {
+                    b.tau0 = tau0; b.base = base;
+                    b.wlo = tau0 - 32; b.whi = min(tau0 + 32 * (RCH - 2) - 1, 32 * kS + 31);
+                    b.Wc = cand_bits32(cwP, tau0 + h, WB, lane); b.cfall = cp.pcl;
+                    mP |= resolve<1>(c, surv, b, vk, a.p, jl, qbuf, qn, MP, left);
+                }
+                store_block(c, MP, mP, k);
+                while (__any_sync(FULL, left != 0u)) {        // queue overflow (rare)
+                    flush_queue<1>(c, qbuf, qn, vk, a.p, MP);
+                    qn = 0;
+                    left = queue_bits<1>(c, b, h, left, QCAP / 32, qbuf, qn);
+                }
+            }
+        }
+        cp_wait<0>();
+        if (vP >= 0 && qn > 0) flush_queue<1>(c, qbuf, qn, vk, a.p, MP);
+        qn = 0;
+    }
+    if (vN < 0) return;
+    __syncwarp();
+
+    // ---------------------------------------------------- pass B (ascending)
+    // Far filter of view -b: SX = max A(q) over q <= i - 3, A = s v + pos,
+    // with its witness SA, and the witness probe toward lower tau.
+    {
+        const int32_t kS = min(max(kB - nbr, kEmin), kB);
+        float A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY;
+        int32_t SA = 0, jl = 0;
+        fill_chunk(c, kS - 1);               // guard chunk for the witness probes of block kS
+        fill_chunk(c, kS); cp_commit();
+        for (int32_t k = kS; k <= kT; ++k) {
+            __syncwarp();
+            if (k + 1 <= kT) fill_chunk(c, k + 1);
+            cp_commit();
+            cp_wait<1>();
+            __syncwarp();
+            const int base = slot_of(32 * k);
+            const float *cb = c.col + base * RP;
+            float ip = (float)(32 * k - T0);
+            if (k < kB) {
+#pragma unroll 8
+                for (int r = 0; r < 32; ++r) {
+                    const float v0 = cb[r * RP];
+                    const float A0 = __fmaf_rn(fs_, v0, ip);
+                    if (A3 > SX) { SX = A3; SA = 32 * k + r - 3; }
+                    A3 = A2; A2 = A1; A1 = A0;
+                    ip = __fadd_rn(ip, 1.0f);
+                }
+                continue;
+            }
+            const int32_t tau0 = 32 * k;
+            const CovN cn = cov_n(cwN, tau0, h, WB, lane);
+            // probe offsets j <= dcov(i) = i + h - nc(i - h) and inside the ring
+            // window (tau - j >= max(tau0 - 96, 32 kS - 3)); nc from the candidate
+            // bits of [tau0 - h, tau0 - h + 31]
+            const uint32_t Wl = cand_bits32(cwN, tau0 - h, WB, lane);
+            const int32_t ll = tau0 - h - 1, eB = tau0 + h;
+            const int32_t wbot = min(32 * (RCH - 2), tau0 - 32 * kS + 3);
+            uint32_t XFR = 0, XH = 0;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) {
+                const float v0 = cb[r * RP];
+                const float A0 = __fmaf_rn(fs_, v0, ip);
+                if (A3 > SX) { SX = A3; SA = tau0 + r - 3; }
+                XFR = push(XFR, __fsub_rn(__fsub_rn(A0, vk.T), SX));
+                {   // witness probe toward lower tau
+                    const uint32_t m = Wl & (FULL << r);
+                    const int32_t ncr = m ? ll + __ffs(m) : cn.ncl;
+                    const float g = fminf(fmaxf(__fsub_rn(SX, A0), 0.0f), 4096.0f);
+                    const int32_t jw = max(3, min((tau0 + r) - SA + __float2int_rn(g), min(eB - ncr, wbot) + r));
+                    int32_t sl = base + r - jw;
+                    sl = sl < 0 ? sl + RING : sl;
+                    const float x = __fsub_rn(fabsf(__fmaf_rn(fs_, __fsub_rn(c.col[sl * RP], v0), -(float)jw)), vk.tlo);
+                    XH = push(XH, x);
+                    jl = x < 0.0f ? jw : jl;
+                }
+                A3 = A2; A2 = A1; A1 = A0;
+                ip = __fadd_rn(ip, 1.0f);
+            }
+            XFR = __brev(XFR);                     // bit r <-> tau0 + r
+            XH = __brev(XH);
+            const uint32_t C3 = cov_n_k(cn, tau0, h, 3);
+            uint32_t mN = nn[(k - kB) * 32 + lane] | (XH & C3);
+            const uint32_t surv = XFR & C3 & ~mN;
+            uint32_t left = 0u;
+            Blk b;
+            if (__any_sync(FULL, surv != 0u)) {
+                b.tau0 = tau0; b.base = base;
+                b.wlo = max(tau0 - 32 * (RCH - 2), 32 * kS); b.whi = tau0 + 31;
+                b.Wc = cand_bits32(cwN, tau0 - h, WB, lane); b.cfall = cn.ncl;
+                mN |= resolve<-1>(c, surv, b, vk, a.p, jl, qbuf, qn, MN, left);
+            }
+            dbg_add(c.dbg, 7, 32u);
+            store_block(c, MN, mN, k);
+            while (__any_sync(FULL, left != 0u)) {            // queue overflow (rare)
+                flush_queue<-1>(c, qbuf, qn, vk, a.p, MN);
+                qn = 0;
+                left = queue_bits<-1>(c, b, h, left, QCAP / 32, qbuf, qn);
+            }
+        }
+        cp_wait<0>();
+        if (qn > 0) flush_queue<-1>(c, qbuf, qn, vk, a.p, MN);
+    }
+}
+
+// grid: (units, frames); one warp per block
+template <int CB>
+__global__ void __launch_bounds__(32) k_line(LineArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    // frames fastest: co-resident warps work on the same line family (shared
+    // instruction cache footprint) and on neighbouring frames
+    const int32_t f = (int32_t)(blockIdx.x % (unsigned)a.frames);
+    const LineUnit u = a.units[blockIdx.x / (unsigned)a.frames];
+    const GroupDesc gd = a.groups[u.group];
+    const FamilyDesc fd = a.fams[gd.fam];
+    unit_body<CB>(a, u, gd, fd, f, smem);
+}
+
+cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
+                        int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
+                        const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
+                        const void *codes, int32_t code_bytes, unsigned long long *dbg, cudaStream_t s) {
+    if (nunits <= 0) return cudaSuccess;
+    LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch};
+    dim3 grid((unsigned)nunits * (unsigned)batch);
+    cudaError_t e;
+    if (code_bytes == 1) {
+        e = cudaFuncSetAttribute(k_line<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
+        if (e != cudaSuccess) return e;
+        k_line<1><<<grid, 32, WSMEM, s>>>(a);
+    } else if (code_bytes == 2) {
+        e = cudaFuncSetAttribute(k_line<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
+        if (e != cudaSuccess) return e;
+        k_line<2><<<grid, 32, WSMEM, s>>>(a);
+    } else {
+        e = cudaFuncSetAttribute(k_line<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
+        if (e != cudaSuccess) return e;
+        k_line<4><<<grid, 32, WSMEM, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace occ

@@ -29,6 +29,11 @@ struct occ_ctx {
     std::vector<TileDesc> tiles;
     GroupDesc *d_groups = nullptr;
     TileDesc *d_tiles = nullptr;
+    std::vector<LineUnit> units;          // k_line work (eligible groups)
+    std::vector<TileDesc> all_tiles;      // k_tile work for every group (OCC_PATH_TILED)
+    LineUnit *d_units = nullptr;
+    TileDesc *d_all_tiles = nullptr;
+    unsigned long long *d_dbg = nullptr;  // k_line event counters (occ_debug_line_stats)
     void *d_codes = nullptr;             // K0 -> K1 candidate codes, one chunk of frames
     int32_t code_bytes = 1, chunk = 1;
     float *d_stage_D = nullptr;          // occ_detect_host staging (lazy)
@@ -39,7 +44,7 @@ struct occ_ctx {
     // kernel timing (occ_profile)
     bool profiling = false;
     std::vector<cudaEvent_t> ev[OCC_KERNEL_KINDS];   // start/end pairs
-    size_t ev_used[OCC_KERNEL_KINDS] = {0, 0, 0, 0, 0};
+    size_t ev_used[OCC_KERNEL_KINDS] = {};
 };
 
 namespace {
@@ -154,6 +159,68 @@ struct ProfScope {
     }
 };
 
+// k_line serves a group when its family is rows / columns / diagonals /
+// anti-diagonals, its views use the default near/far split (near backward
+// offsets {1, 2}, far >= 3, <= 1 near forward offset whose lower bound equals
+// the backward one), and the two views (if two) are +-b with equal s.
+bool line_eligible(const occ_ctx *c, const GroupDesc &g) {
+    const FamilyDesc &fd = c->fams[g.fam];
+    if (fd.kind < 0 || fd.kind > 3 || g.nv < 1 || g.nv > 2) return false;
+    for (int32_t k = 0; k < g.nv; ++k) {
+        const ViewDesc &v = c->views[g.view[k]];
+        if (v.nback != 2 || v.jstar != 3 || v.nfwd > 1) return false;
+        if (v.nfwd == 1 && v.fwd_lo[0] != v.back_lo[0]) return false;
+    }
+    if (g.nv == 2) {
+        const ViewDesc &a = c->views[g.view[0]], &b = c->views[g.view[1]];
+        if (a.sg == b.sg || a.s != b.s || a.nfwd != b.nfwd) return false;
+        for (int i = 0; i < 2; ++i)
+            if (a.back_lo[i] != b.back_lo[i] || a.back_hi[i] != b.back_hi[i]) return false;
+        if (a.nfwd && (a.fwd_lo[0] != b.fwd_lo[0] || a.fwd_hi[0] != b.fwd_hi[0])) return false;
+    }
+    return true;
+}
+
+// Host copy of k_line's lane extent (LG<KIND>::ext): in-image positions of
+// line L in the lane's time coordinate tau = pos + off(l).
+void line_extent(int32_t kind, int32_t l0, int32_t l, int32_t H, int32_t W, int32_t &lo, int32_t &hi) {
+    const int32_t L = l0 + l;
+    if (kind == 0) { lo = 0; hi = (L >= 0 && L < H) ? W : 0; }
+    else if (kind == 1) { lo = 0; hi = (L >= 0 && L < W) ? H : 0; }
+    else if (kind == 2) {
+        const int32_t a = std::max(0, -L), b = std::min(W, H - L);
+        lo = a + l; hi = std::max(a, b) + l;
+    } else {
+        const int32_t a = std::max(0, L - H + 1), b = std::min(W, L + 1);
+        lo = a + 31 - l; hi = std::max(a, b) + 31 - l;
+    }
+}
+
+void add_line_units(occ_ctx *c, int32_t gi) {
+    const int32_t kind = c->fams[c->groups[gi].fam].kind;
+    const int32_t H = c->H, W = c->W;
+    int32_t lmin = 0, lmax = 0;
+    if (kind == 0) { lmin = 0; lmax = H - 1; }
+    else if (kind == 1) { lmin = 0; lmax = W - 1; }
+    else if (kind == 2) { lmin = -(W - 1); lmax = H - 1; }
+    else { lmin = 0; lmax = H + W - 2; }
+    for (int32_t l0 = lmin; l0 <= lmax; l0 += 32) {
+        int32_t tlo = INT32_MAX, thi = INT32_MIN;
+        for (int32_t l = 0; l < 32; ++l) {
+            int32_t lo, hi;
+            line_extent(kind, l0, l, H, W, lo, hi);
+            if (lo < hi) { tlo = std::min(tlo, lo); thi = std::max(thi, hi); }
+        }
+        if (tlo >= thi) continue;
+        const int32_t a = tlo & ~31, b = (thi + 31) & ~31;
+        for (int32_t t0 = a; t0 < b; t0 += kLineSeg) {
+            LineUnit u{};
+            u.group = gi; u.l0 = l0; u.t0 = t0; u.t1 = std::min(t0 + kLineSeg, b);
+            c->units.push_back(u);
+        }
+    }
+}
+
 // View groups (<= 2 views of one family, +-b pairs of equal s first) and the
 // static tile list: for every group, blocks of 32 consecutive lines and
 // segments of kTilePositions positions covering the lines' in-image extent.
@@ -175,6 +242,11 @@ void build_tiles(occ_ctx *c) {
         }
     }
     const int32_t H = c->H, W = c->W;
+    std::vector<char> eligible(c->groups.size(), 0);
+    for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi) {
+        eligible[gi] = line_eligible(c, c->groups[gi]);
+        if (eligible[gi]) add_line_units(c, gi);
+    }
     for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi) {
         const FamilyDesc &fd = c->fams[c->groups[gi].fam];
         const int32_t num = fd.num, den = fd.den;
@@ -193,7 +265,8 @@ void build_tiles(occ_ctx *c) {
             for (int32_t p0 = plo; p0 <= phi; p0 += kTilePositions) {
                 TileDesc t{};
                 t.group = gi; t.l0 = l0; t.p0 = p0; t.p1 = std::min(p0 + kTilePositions, phi + 1);
-                c->tiles.push_back(t);
+                c->all_tiles.push_back(t);
+                if (!eligible[gi]) c->tiles.push_back(t);
             }
         }
     }
@@ -295,7 +368,9 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
     if (cudaMalloc(&c->d_views, sizeof(ViewDesc) * c->views.size()) != cudaSuccess ||
         cudaMalloc(&c->d_fams, sizeof(FamilyDesc) * c->fams.size()) != cudaSuccess ||
         cudaMalloc(&c->d_groups, sizeof(GroupDesc) * c->groups.size()) != cudaSuccess ||
-        cudaMalloc(&c->d_tiles, sizeof(TileDesc) * c->tiles.size()) != cudaSuccess ||
+        cudaMalloc(&c->d_tiles, sizeof(TileDesc) * std::max<size_t>(1, c->tiles.size())) != cudaSuccess ||
+        cudaMalloc(&c->d_all_tiles, sizeof(TileDesc) * std::max<size_t>(1, c->all_tiles.size())) != cudaSuccess ||
+        cudaMalloc(&c->d_units, sizeof(LineUnit) * std::max<size_t>(1, c->units.size())) != cudaSuccess ||
         cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess ||
         cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess) {
         cudaGetLastError();
@@ -308,8 +383,13 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
                    cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(c->d_groups, c->groups.data(), sizeof(GroupDesc) * c->groups.size(),
                    cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(c->d_tiles, c->tiles.data(), sizeof(TileDesc) * c->tiles.size(),
-                   cudaMemcpyHostToDevice) != cudaSuccess) {
+        (c->tiles.size() && cudaMemcpy(c->d_tiles, c->tiles.data(), sizeof(TileDesc) * c->tiles.size(),
+                                       cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (c->all_tiles.size() && cudaMemcpy(c->d_all_tiles, c->all_tiles.data(),
+                                           sizeof(TileDesc) * c->all_tiles.size(),
+                                           cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (c->units.size() && cudaMemcpy(c->d_units, c->units.data(), sizeof(LineUnit) * c->units.size(),
+                                       cudaMemcpyHostToDevice) != cudaSuccess)) {
         occ_destroy(c);
         return OCC_ERR_CUDA;
     }
@@ -363,11 +443,24 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
                                    c->d_stats + c0, c->d_codes, c->code_bytes, s)); ++launches;
                 ps.end();
             }
-            ProfScope pt(c, OCC_KERNEL_TILE, s);
-            CK(launch_tile(Dc, c->H, c->W, n, c->d_tiles, (int32_t)c->tiles.size(), c->d_groups,
-                           c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params,
-                           M + (int64_t)c0 * c->V * HW, c->d_codes, c->code_bytes, s)); ++launches;
-            pt.end();
+            const bool tiled_only = c->path == OCC_PATH_TILED;
+            if (!tiled_only && !c->units.empty()) {
+                ProfScope pl(c, OCC_KERNEL_LINE, s);
+                CK(launch_line(Dc, c->H, c->W, n, c->d_units, (int32_t)c->units.size(), c->d_groups,
+                               c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params,
+                               M + (int64_t)c0 * c->V * HW, c->d_codes, c->code_bytes, c->d_dbg, s));
+                ++launches;
+                pl.end();
+            }
+            const TileDesc *tl = tiled_only ? c->d_all_tiles : c->d_tiles;
+            const int32_t nt = (int32_t)(tiled_only ? c->all_tiles.size() : c->tiles.size());
+            if (nt > 0) {
+                ProfScope pt(c, OCC_KERNEL_TILE, s);
+                CK(launch_tile(Dc, c->H, c->W, n, tl, nt, c->d_groups, c->d_views, c->V, c->d_fams,
+                               c->d_stats + c0, c->params, M + (int64_t)c0 * c->V * HW, c->d_codes,
+                               c->code_bytes, s)); ++launches;
+                pt.end();
+            }
         }
     }
     c->last_stream = s;
@@ -452,6 +545,30 @@ int occ_profile_read(occ_ctx *c, int32_t kind, double *total_ms, int32_t *launch
     return OCC_OK;
 }
 
+// Debug statistics of the line-sweep kernel (not part of include/occ.h):
+// enable != 0 allocates/zeroes 16 counters that subsequent occ_detect calls
+// accumulate; out (host, 16 entries, may be NULL) receives the current values.
+int occ_debug_line_stats(occ_ctx *c, int32_t enable, unsigned long long *out) {
+    if (!c) return OCC_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    if (out) {
+        if (c->d_dbg) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaMemcpy(out, c->d_dbg, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        } else {
+            memset(out, 0, 16 * sizeof(unsigned long long));
+        }
+    }
+    if (enable) {
+        if (!c->d_dbg) CK(cudaMalloc(&c->d_dbg, 16 * sizeof(unsigned long long)));
+        CK(cudaMemset(c->d_dbg, 0, 16 * sizeof(unsigned long long)));
+    } else if (c->d_dbg) {
+        CK(cudaFree(c->d_dbg));
+        c->d_dbg = nullptr;
+    }
+    return OCC_OK;
+}
+
 int occ_destroy(occ_ctx *c) {
     if (!c) return OCC_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
@@ -462,6 +579,9 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_codes);
     cudaFree(c->d_groups);
     cudaFree(c->d_tiles);
+    cudaFree(c->d_all_tiles);
+    cudaFree(c->d_units);
+    cudaFree(c->d_dbg);
     cudaFree(c->d_stage_D);
     cudaFree(c->d_stage_M);
     for (int k = 0; k < OCC_KERNEL_KINDS; ++k)

@@ -103,6 +103,20 @@ cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
                         const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
                         const FrameStats *st, const Params &p, uint8_t *masks, const void *codes,
                         int32_t code_bytes, cudaStream_t s);
+// Line-sweep kernel (k_line.cu) for the four line families of |b| <= 1
+// arrays: one warp per unit = 32 consecutive lines x [t0, t1) in the lane's
+// time coordinate (t0, t1 multiples of 32, t1 - t0 <= kLineSeg).
+constexpr int kLineSeg = 512;
+constexpr int kLineRingChunks = 5;       // ring of 5 x 32 staged positions per warp
+constexpr int kLineCandMarginWords = 4;  // candidate words staged beyond the segment (h + 32 <= 128)
+struct LineUnit {
+    int32_t group, l0, t0, t1;
+};
+size_t line_smem_bytes();
+cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
+                        int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
+                        const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
+                        const void *codes, int32_t code_bytes, unsigned long long *dbg, cudaStream_t s);
 cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
                             const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
                             FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s);

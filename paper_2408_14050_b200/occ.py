@@ -28,7 +28,7 @@ PATHS = {"auto": 0, "tiled": 1, "direct": 2}
 EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", "occ_status",
            "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
            "occ_version", "occ_profile", "occ_profile_read"]
-KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4}
+KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5}
 
 
 class occ_baseline(ctypes.Structure):

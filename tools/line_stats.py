@@ -1,0 +1,43 @@
+"""Event statistics of the line-sweep kernel on C3 frames, per line family
+(debug tool; uses the non-public occ_debug_line_stats entry point)."""
+import ctypes
+import sys
+import os
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2408_14050_b200 import scenes  # noqa: E402
+from paper_2408_14050_b200.occ import Detector, lib  # noqa: E402
+
+L = lib()
+L.occ_debug_line_stats.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_ulonglong)]
+names = ["survP", "survN", "stage1_hits", "hard", "exh_found", "exh_steps", "global_probes",
+         "blocks(x32)", "direct_units", "resolve_iters(x32)"]
+names2 = ["q_overflow", "q_tot", "q_n"]
+nf = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+D = torch.from_numpy(scenes.make_batch(3, nf)).cuda()
+H, W = D.shape[1:]
+for fam, views in [("rows", [(1, 0), (-1, 0)]), ("cols", [(0, 1), (0, -1)]),
+                   ("diag", [(1, 1), (-1, -1)]), ("anti", [(1, -1), (-1, 1)]), ("all", scenes.VIEWS_3X3)]:
+    det = Detector(H, W, views, max_batch=nf)
+    det.detect(D)
+    torch.cuda.synchronize()
+    L.occ_debug_line_stats(det._h, 1, None)
+    det.detect(D)
+    out = (ctypes.c_ulonglong * 16)()
+    L.occ_debug_line_stats(det._h, 0, out)
+    pv = nf * H * W * len(views)
+    vals = list(out)[:10]
+    print(fam, " ".join(f"{n}={v / pv:.5f}" if i not in (7, 9) else f"{n}={v / 32 / pv:.5f}"
+                        for i, (n, v) in enumerate(zip(names, vals))))
+    print("   raw:", {n: int(v) for n, v in zip(names2, list(out)[10:13])}, "steps", int(out[5]))
+    # timing
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    for _ in range(3):
+        det.detect(D)
+    torch.cuda.synchronize()
+    print(f"   {(time.perf_counter() - t0) / 3 * 1e3:.2f} ms per call of {nf} frames")
+    det.close()
