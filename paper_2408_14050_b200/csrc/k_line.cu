@@ -34,23 +34,24 @@
 // Frames the kernel cannot serve with this scheme (h < 17 or h + 32 beyond
 // the candidate margin) are computed by the exact per-pixel
 // routine (direct_pixel) inside the same warp.
+#include <cstdlib>
+
 #include "occ_device.cuh"
 
 namespace occ {
 
 namespace {
 constexpr int SEGB = kLineSeg / 32;            // blocks per segment
-constexpr int RCH = kLineRingChunks;            // ring chunks (32 positions each)
-constexpr int RING = RCH * 32;
-constexpr int RP = 33;                          // ring pitch (floats per position)
 constexpr int CMW = kLineCandMarginWords;       // candidate margin words per side
 constexpr int NCW = SEGB + 2 * CMW;             // candidate words per view
-constexpr size_t OFF_RING = 0;
-constexpr size_t OFF_CW = OFF_RING + sizeof(float) * RING * RP;
+constexpr size_t OFF_CW = 0;
 constexpr size_t OFF_NN = OFF_CW + sizeof(uint32_t) * 2 * NCW * 32;
-constexpr int QCAP = 256;                       // deferred hard survivors per warp
+constexpr int QCAP = 128;                       // deferred hard survivors per warp
 constexpr size_t OFF_Q = OFF_NN + sizeof(uint32_t) * SEGB * 32;
-constexpr size_t WSMEM = OFF_Q + sizeof(int32_t) * 2 * QCAP;
+constexpr size_t OFF_SAB = OFF_Q + sizeof(int32_t) * 2 * QCAP;
+constexpr int SP = 33;                          // staging pitch (floats per position)
+constexpr size_t OFF_STG = OFF_SAB + sizeof(int16_t) * 32 * 32;
+constexpr size_t WSMEM = OFF_STG + sizeof(float) * 2 * 32 * SP;
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr int32_t NONE_LO = -(1 << 28), NONE_HI = (1 << 28);
 }  // namespace
@@ -74,11 +75,6 @@ __device__ __forceinline__ float nextup_f(float a) {
     const int32_t b = __float_as_int(a);
     if (a == 0.0f) return __int_as_float(1);
     return __int_as_float(a > 0.0f ? b + 1 : b - 1);
-}
-__device__ __forceinline__ int slot_of(int32_t tau) {
-    if (RING == 128) return tau & 127;
-    int32_t m = tau % RING;
-    return m < 0 ? m + RING : m;
 }
 __device__ __forceinline__ void cp_async4(float *dst, const float *src) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
@@ -213,19 +209,27 @@ struct LineArgs {
     const void *codes;
     unsigned long long *dbg;   // optional event counters (occ_debug_line_stats), or null
     int32_t frames;
+    HardEntry *gq;             // global queue of exhaustive searches (k_hard), capacity gq_cap
+    uint32_t *gq_count;
+    int32_t gq_cap;
 };
 
 // Per-warp context
 struct Ctx {
     unsigned long long *dbg;
+    unsigned long long *ph;    // per-CTA phase timers (debug) or null
     int32_t kind;              // line family (0 rows, 1 columns, 2 diagonals, 3 anti-diagonals)
     const float *Df;
     int32_t H, W, l0, lane;
     int32_t elo, ehi;          // lane's extent in tau
-    float *ring;               // warp's ring (float [RING][RP])
+    const float *Dl;           // lane's line: v(tau) = Dl[tau * S]
+    bool vec4;                 // rows with 16-byte aligned rows (float4 loads)
     int64_t B;                 // lane's line: pixel index = B + tau * S
     int32_t S;
-    const float *col;          // ring + lane
+    int32_t f;                 // frame
+    HardEntry *gq;
+    uint32_t *gq_count;
+    int32_t gq_cap;
 };
 
 __device__ __forceinline__ float gload(const Ctx &c, int32_t l, int32_t tau) {
@@ -233,18 +237,19 @@ __device__ __forceinline__ float gload(const Ctx &c, int32_t l, int32_t tau) {
     return __ldg(c.Df + b + (int64_t)tau * c.S);
 }
 
-// fill one chunk (32 tau) of the ring with cp.async (NaN outside the image)
-__device__ __forceinline__ void fill_chunk(const Ctx &c, int32_t k) {
+// Stages chunk k (tau = 32k .. 32k + 31 of the warp's 32 lines) into st
+// [position][lane] with cp.async, one coalesced run per instruction; NaN
+// outside the image.
+__device__ __noinline__ void stage_chunk(const Ctx &c, float *st, int32_t k) {
     const float NaN = __int_as_float(0x7fc00000);
     const int lane = c.lane;
     const int32_t t0 = 32 * k;
-    float *dst0 = c.ring + slot_of(t0) * RP;          // the 32 slots of a chunk are contiguous
     if (c.kind == 0) {
-        // rows: lane = position, one coalesced row segment per line j
+        // rows: lane = position, one row segment per line j
         const int32_t x = t0 + lane;
         const int32_t nrow = (x >= 0 && x < c.W) ? min(32, c.H - c.l0) : 0;
         const float *src = c.Df + (int64_t)c.l0 * c.W + x;
-        float *dst = dst0 + lane * RP;
+        float *dst = st + lane * SP;
         if (nrow == 32) {
 #pragma unroll 8
             for (int j = 0; j < 32; ++j) cp_async4(dst + j, src + (int64_t)j * c.W);
@@ -254,20 +259,33 @@ __device__ __forceinline__ void fill_chunk(const Ctx &c, int32_t k) {
             }
         }
     } else {
-        // lane = line: one coalesced run per tau (row segment / skewed row)
-        const float *src = c.Df + c.B + (int64_t)t0 * c.S;
-        float *dst = dst0 + lane;
+        const float *src = c.Dl + (int64_t)t0 * c.S;
+        float *dst = st + lane;
         if (t0 >= c.elo && t0 + 32 <= c.ehi) {
 #pragma unroll 8
-            for (int j = 0; j < 32; ++j) cp_async4(dst + j * RP, src + (int64_t)j * c.S);
+            for (int j = 0; j < 32; ++j) cp_async4(dst + j * SP, src + (int64_t)j * c.S);
         } else {
             for (int j = 0; j < 32; ++j) {
                 const int32_t tau = t0 + j;
-                if (tau >= c.elo && tau < c.ehi) cp_async4(dst + j * RP, src + (int64_t)j * c.S);
-                else dst[j * RP] = NaN;
+                if (tau >= c.elo && tau < c.ehi) cp_async4(dst + j * SP, src + (int64_t)j * c.S);
+                else dst[j * SP] = NaN;
             }
         }
     }
+}
+
+// value of the lane's line at tau (NaN outside the image)
+__device__ __forceinline__ float gv(const Ctx &c, int32_t tau) {
+    return (tau >= c.elo && tau < c.ehi) ? __ldg(c.Dl + (int64_t)tau * c.S) : __int_as_float(0x7fc00000);
+}
+// values at tau .. tau + 3 (tau multiple of 4); `inside`: all four are in the image
+__device__ __forceinline__ float4 load4(const Ctx &c, int32_t tau, bool inside) {
+    if (inside) {
+        if (c.vec4) return __ldg(reinterpret_cast<const float4 *>(c.Dl + tau));
+        const float *q = c.Dl + (int64_t)tau * c.S;
+        return make_float4(__ldg(q), __ldg(q + c.S), __ldg(q + 2 * c.S), __ldg(q + 3 * c.S));
+    }
+    return make_float4(gv(c, tau), gv(c, tau + 1), gv(c, tau + 2), gv(c, tau + 3));
 }
 
 template <int CB>
@@ -279,7 +297,7 @@ __device__ __forceinline__ uint32_t code_at(const void *codes, int64_t idx) {
 
 // pass 0: candidate words of both views (bit cb and cb + 1 of the codes)
 template <int CB>
-__device__ __forceinline__ void build_cand(const Ctx &c, const void *codesf, int32_t cb, int32_t WB,
+__device__ __noinline__ void build_cand(const Ctx &c, const void *codesf, int32_t cb, int32_t WB,
                                            uint32_t *cw) {
     const int lane = c.lane;
     for (int w = 0; w < NCW; ++w) {
@@ -369,23 +387,17 @@ struct ViewK {
 
 // Per-block context of the far-survivor resolution.
 struct Blk {
-    int32_t tau0, base;    // block start and its ring slot
-    int32_t wlo, whi;      // ring window (tau) valid during this block
+    int32_t tau0;          // block start
     uint32_t Wc;           // candidate bits of [tau0 + h, +31] (+b) / [tau0 - h, +31] (-b)
     int32_t cfall;         // last candidate < tau0 + h (+b) / first candidate >= tau0 + 32 - h (-b)
+    const int16_t *sab;    // filter witness of each survivor, relative to tau0 ([r][lane])
+    int32_t T0;
 };
 
-__device__ __forceinline__ int32_t ring_slot(const Blk &b, int32_t tau) {
-    int32_t x = b.base + (tau - b.tau0);
-    x = x >= RING ? x - RING : x;
-    return x < 0 ? x + RING : x;
-}
-// value of line l at tau: ring inside the block's window, else global; NaN outside the line
+// value of line l at tau (L1 / L2); NaN outside the line
 __device__ __forceinline__ float probe_b(const Ctx &c, const Blk &b, int32_t l, int32_t tau, int32_t elo,
                                          int32_t ehi) {
     if (tau < elo || tau >= ehi) return __int_as_float(0x7fc00000);
-    if (tau >= b.wlo && tau <= b.whi) return c.ring[ring_slot(b, tau) * RP + l];
-    if (c.dbg) atomicAdd(c.dbg + 6, 1ull);
     return gload(c, l, tau);
 }
 // dcov of the survivor at tau0 + r (largest far offset sharing a scan window, App. A.2)
@@ -403,12 +415,16 @@ __device__ __forceinline__ int32_t dcov_of(uint32_t Wc, int32_t cfall, int32_t t
 // Eq. 5 for a far pair (offset j >= jstar, so delta > t_disp is implied):
 // |s fl(vq - vp) - j| < t_dist.  s delta is exact; one rounding in the fma,
 // far below the 2^-10 band; inside the band the binary64 test decides.
+__device__ __noinline__ bool pair_exact_slow(float vq, float vp, int32_t j, int32_t s, float t_dist,
+                                             float t_disp) {
+    return pair_exact(vq, vp, -j, s, t_dist, t_disp);
+}
 __device__ __forceinline__ bool pair_far(float vq, float vp, int32_t j, const ViewK &vk, const Params &p) {
     const float d = __fsub_rn(vq, vp);
     const float x = fabsf(__fmaf_rn(vk.fs, d, -(float)j));
     if (x < vk.tlo) return true;
     if (!(x <= vk.thi)) return false;
-    return pair_exact(vq, vp, -j, vk.s, p.t_dist, p.t_disp);
+    return pair_exact_slow(vq, vp, j, vk.s, p.t_dist, p.t_disp);
 }
 
 // Deferred exhaustive searches: one lane per queued survivor (tau, dcov,
@@ -417,9 +433,32 @@ __device__ __forceinline__ bool pair_far(float vq, float vp, int32_t j, const Vi
 // block store already wrote 0 there).
 template <int DIR>
 __device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int32_t qn, const ViewK &vk,
-                                         const Params &p, uint8_t *Mv) {
+                                         const Params &p, uint8_t *Mv, int32_t vid) {
+    const long long tph = clock64();
     __syncwarp();
     const float NaN = __int_as_float(0x7fc00000);
+    // normally the searches go to the global queue, resolved after this
+    // kernel by k_hard with the whole GPU (no single warp carries a heavy unit)
+    if (c.gq && qn > 0) {
+        uint32_t base = 0u;
+        if (c.lane == 0) base = atomicAdd(c.gq_count, (uint32_t)qn);
+        base = __shfl_sync(FULL, base, 0);
+        if (base + (uint32_t)qn <= (uint32_t)c.gq_cap) {
+            for (int32_t e = c.lane; e < qn; e += 32) {
+                const int32_t tau = qbuf[2 * e], w = qbuf[2 * e + 1];
+                const int32_t src = w & 31, jm = w >> 5;
+                HardEntry he;
+                he.pix = (int32_t)(line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S);
+                he.step = DIR * c.S;
+                he.jm = jm;
+                he.fv = (c.f << 8) | vid;
+                c.gq[base + (uint32_t)e] = he;
+            }
+            __syncwarp();
+            if (c.ph && c.lane == 0) c.ph[1] += (unsigned long long)(clock64() - tph);
+            return;
+        }
+    }
     for (int32_t e0 = 0; e0 < qn; e0 += 32) {
         const int32_t e = e0 + c.lane;
         if (e < qn) {
@@ -433,7 +472,7 @@ __device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int3
                 float vq[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * st) : NaN;
-#pragma unroll
+#pragma unroll 4
                 for (int u = 0; u < 16; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
             }
             dbg_add(c.dbg, 4, hit ? 1u : 0u);
@@ -441,6 +480,7 @@ __device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int3
         }
     }
     __syncwarp();
+    if (c.ph && c.lane == 0) c.ph[1] += (unsigned long long)(clock64() - tph);
 }
 
 // Appends the survivors of `bits` (bit r <-> tau0 + r) to the deferred queue,
@@ -484,9 +524,10 @@ __device__ __forceinline__ uint32_t queue_bits(const Ctx &c, const Blk &b, int32
 template <int DIR>
 __device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b, const ViewK &vk,
                                          const Params &p, int32_t &jl, int32_t *qbuf, int32_t &qn,
-                                         uint8_t *Mv, uint32_t &left) {
+                                         uint8_t *Mv, uint32_t &left, int32_t vid) {
     const int lane = c.lane;
     const int32_t h = vk.h;
+    const long long tph = clock64();
     uint32_t hits = 0u, hard = 0u;
     dbg_add(c.dbg, DIR > 0 ? 0 : 1, __popc(S));
     while (__any_sync(FULL, S != 0u)) {
@@ -495,25 +536,35 @@ __device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b,
             const int32_t r = DIR > 0 ? 31 - __clz(S) : __ffs(S) - 1;
             S &= ~(1u << r);
             const int32_t tau = b.tau0 + r;
-            const float vp = c.col[(b.base + r) * RP];
+            const float vp = __ldg(c.Dl + (int64_t)tau * c.S);
             int32_t jm = dcov_of<DIR>(b.Wc, b.cfall, b.tau0, r, h);
             jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
-            bool hit = false;
-            // the line's last far offset, its neighbours, and one secant step
-            // from it (A falls ~1 per step along an occluder: the residual
-            // y = s delta - j is the remaining distance)
-            float y0 = 0.0f;
+            // 1. the line's last far offset jl (bands: the partner offset moves
+            //    with the pixel, so consecutive survivors share it)
+            bool hit = jl >= 3 && jl <= jm &&
+                       pair_far(probe_b(c, b, lane, tau + DIR * jl, c.elo, c.ehi), vp, jl, vk, p);
+            if (!hit) {
+                // 2. the filter witness SA (parked by the sweep): past it A falls ~1
+                //    per step on a flat occluder, so the partner sits near
+                //    jw = max(|SA - tau|, s (v_SA - v_p)); probe jw, jw + 1, jw - 1
+                //    and one secant step from jw
+                const int32_t SAa = b.tau0 + (int32_t)b.sab[r * 32 + lane];
+                const float vsa = probe_b(c, b, lane, SAa, c.elo, c.ehi);
+                const float g = fminf(fmaxf(__fmul_rn(vk.fs, __fsub_rn(vsa, vp)), 0.0f), 4096.0f);
+                const int32_t jw = max(DIR * (SAa - tau), __float2int_rn(g));
+                float y0 = 0.0f;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                int32_t j = q == 0 ? jl : (q == 1 ? jl - 1 : (q == 2 ? jl + 1 : jl + (int32_t)rintf(y0)));
-                if (q == 3 && (j == jl || j == jl - 1 || j == jl + 1)) j = -1;
-                if (!hit && j >= 3 && j <= jm) {
-                    const float vq = probe_b(c, b, lane, tau + DIR * j, c.elo, c.ehi);
-                    if (q == 0) {
-                        const float yy = __fmaf_rn(vk.fs, __fsub_rn(vq, vp), -(float)j);
-                        y0 = (yy == yy) ? fminf(fmaxf(yy, -64.0f), 64.0f) : 0.0f;
+                for (int q = 0; q < 4; ++q) {
+                    int32_t j = q == 0 ? jw : (q == 1 ? jw + 1 : (q == 2 ? jw - 1 : jw + (int32_t)rintf(y0)));
+                    if ((q == 3 && j >= jw - 1 && j <= jw + 1) || j == jl) j = -1;
+                    if (!hit && j >= 3 && j <= jm) {
+                        const float vq = probe_b(c, b, lane, tau + DIR * j, c.elo, c.ehi);
+                        if (q == 0) {
+                            const float yy = __fmaf_rn(vk.fs, __fsub_rn(vq, vp), -(float)j);
+                            y0 = (yy == yy) ? fminf(fmaxf(yy, -64.0f), 64.0f) : 0.0f;
+                        }
+                        if (pair_far(vq, vp, j, vk, p)) { hit = true; jl = j; }
                     }
-                    if (pair_far(vq, vp, j, vk, p)) { hit = true; jl = j; }
                 }
             }
             if (hit) hits |= 1u << r; else hard |= 1u << r;
@@ -529,11 +580,12 @@ __device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b,
         const int32_t tot = __reduce_add_sync(FULL, __popc(hard));
         if (lane == 0) dbg_add(c.dbg, 10, tot > QCAP ? 1u : 0u);
         if (qn + tot > QCAP) {
-            flush_queue<DIR>(c, qbuf, qn, vk, p, Mv);
+            flush_queue<DIR>(c, qbuf, qn, vk, p, Mv, vid);
             qn = 0;
         }
         left = queue_bits<DIR>(c, b, h, hard, tot <= QCAP ? 32 : QCAP / 32, qbuf, qn);
     }
+    if (c.ph && lane == 0) c.ph[0] += (unsigned long long)(clock64() - tph);
     return hits;
 }
 
@@ -626,17 +678,23 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     const int64_t HW = (int64_t)H * W;
     Ctx c;
     c.dbg = a.dbg;
+    c.f = f;
+    c.gq = a.gq; c.gq_count = a.gq_count; c.gq_cap = a.gq_cap;
+    c.ph = (a.dbg && blockIdx.x < 32768u) ? a.dbg + 16 + 2 * 32768 + 4 * blockIdx.x : nullptr;
     c.kind = kind;
     c.Df = a.D + (int64_t)f * HW;
     c.H = H; c.W = W; c.l0 = u.l0; c.lane = lane;
     lg_ext(kind, u.l0, lane, H, W, c.elo, c.ehi);
     c.B = line_base(kind, u.l0, lane, W);
     c.S = line_stride(kind, W);
-    c.ring = reinterpret_cast<float *>(smem + OFF_RING);
-    c.col = c.ring + lane;
+    c.Dl = c.Df + c.B;
+    c.vec4 = kind == 0 && (W & 3) == 0;
+
     uint32_t *cw = reinterpret_cast<uint32_t *>(smem + OFF_CW);
     uint32_t *nn = reinterpret_cast<uint32_t *>(smem + OFF_NN);
     int32_t *qbuf = reinterpret_cast<int32_t *>(smem + OFF_Q);
+    int16_t *sab = reinterpret_cast<int16_t *>(smem + OFF_SAB);
+    float *stg = reinterpret_cast<float *>(smem + OFF_STG);
     int32_t qn = 0;
     const int32_t T0 = u.t0, T1 = u.t1;            // multiples of 32
     const int32_t kB = T0 >> 5, kT = (T1 >> 5) - 1;
@@ -689,7 +747,9 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     const int32_t WB = kB - CMW;
     {
         const unsigned char *codesf = reinterpret_cast<const unsigned char *>(a.codes) + (int64_t)f * HW * CB;
+        const long long tph = clock64();
         build_cand<CB>(c, codesf, 2 * gd.fam, WB, cw);
+        if (c.ph && lane == 0) c.ph[2] += (unsigned long long)(clock64() - tph);
     }
     const uint32_t *cwP = cw, *cwN = cw + NCW * 32;
     __syncwarp();
@@ -700,35 +760,34 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
 
     // ---------------------------------------------------- pass A (descending)
     // Far filter of view +b: SX = max A(q) over q >= i + 3, A = s v - pos, with
-    // its witness SA.  Past the witness A falls ~1 per step on a flat
-    // occluder, so the Eq. 5 partner of i sits near offset
-    // jw = (SA - i) + max(SX - A_i, 0); it is probed at every position (exact
-    // fp32 test, clamped to offsets <= dcov(i), so every confirmed pair is a
-    // far mark).
+    // its witness SA, which is parked for every survivor (filter passed) and
+    // seeds the survivor's exact resolution.
     {
         const int32_t kS = max(min(kT + nbr, kEmax), kT);
         float v1 = NaN, v2 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY;
         int32_t SA = 0, jl = 0;
-        fill_chunk(c, kS + 1);               // guard chunk for the witness probes of block kS
-        fill_chunk(c, kS); cp_commit();
-        if (kS - 1 >= kB - 1) fill_chunk(c, kS - 1);
+        int slot = 0;
+        stage_chunk(c, stg, kS);
         cp_commit();
         for (int32_t k = kS; k >= kB; --k) {
+            // chunk k is (being) staged in `slot`; stage k - 1 into the other slot
+            const float *cb = stg + slot * 32 * SP + lane;
+            float *nxt = stg + (slot ^ 1) * 32 * SP;
             __syncwarp();
-            if (k - 2 >= kB - 1) fill_chunk(c, k - 2);
+            stage_chunk(c, nxt, k - 1);
             cp_commit();
             cp_wait<1>();
             __syncwarp();
-            const int base = slot_of(32 * k);
-            const float *cb = c.col + base * RP;
+            slot ^= 1;
             float ip = (float)(32 * k + 31 - T0);
+            SA += 32;                                  // witness offset relative to tau0 = 32 k
             if (k > kT) {
                 // start-up: suffix max only
 #pragma unroll 8
                 for (int r = 31; r >= 0; --r) {
-                    const float v0 = cb[r * RP];
+                    const float v0 = cb[r * SP];
                     const float A0 = __fmaf_rn(fs_, v0, -ip);
-                    if (A3 > SX) { SX = A3; SA = 32 * k + r + 3; }
+                    if (A3 > SX) { SX = A3; SA = r + 3; }
                     A3 = A2; A2 = A1; A1 = A0; v2 = v1; v1 = v0;
                     ip = __fsub_rn(ip, 1.0f);
                 }
@@ -736,16 +795,10 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             }
             const int32_t tau0 = 32 * k;
             const CovP cp = cov_p(cwP, tau0, h, WB, lane);
-            // probe offsets j <= dcov(i) = pc(i + h) + h - i (covered) and inside
-            // the ring window (tau + j <= min(tau0 + 95, 32 kS + 34)); pc from the
-            // candidate bits of [tau0 + h, tau0 + h + 31]
-            const uint32_t Wh = cand_bits32(cwP, tau0 + h, WB, lane);
-            const int32_t hh = tau0 + h + 31, eA = h - tau0;
-            const int32_t wtop = min(32 * (RCH - 2) - 1, 32 * kS + 34 - tau0);
-            uint32_t Xs1 = 0, Xg1 = 0, Xl1 = 0, Xlf = 0, Xs2 = 0, Xg2 = 0, Xl2 = 0, XFR = 0, XH = 0;
+            uint32_t Xs1 = 0, Xg1 = 0, Xl1 = 0, Xlf = 0, Xs2 = 0, Xg2 = 0, Xl2 = 0, XFR = 0;
 #pragma unroll 8
             for (int r = 31; r >= 0; --r) {
-                const float v0 = cb[r * RP];
+                const float v0 = cb[r * SP];
                 const float d1 = __fsub_rn(v1, v0), d2 = __fsub_rn(v2, v0);
                 const float e1 = fabsf(d1), e2 = fabsf(d2);
                 Xs1 = push(Xs1, d1);
@@ -756,25 +809,17 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 Xg2 = push(Xg2, __fsub_rn(e2, a2n));
                 Xl2 = push(Xl2, __fsub_rn(e2, bhi1));
                 const float A0 = __fmaf_rn(fs_, v0, -ip);
-                if (A3 > SX) { SX = A3; SA = tau0 + r + 3; }
-                XFR = push(XFR, __fsub_rn(__fsub_rn(A0, vk.T), SX));
-                {   // witness probe
-                    const uint32_t m = Wh & (r == 31 ? FULL : ((2u << r) - 1u));
-                    const int32_t pcr = m ? hh - __clz(m) : cp.pcl;
-                    // partner guess: past the witness SA, A falls ~1 per step on a flat occluder
-                    const float g = fminf(fmaxf(__fsub_rn(SX, A0), 0.0f), 4096.0f);
-                    const int32_t jw = max(3, min(SA - (tau0 + r) + __float2int_rn(g), min(pcr + eA, wtop) - r));
-                    int32_t sl = base + r + jw;
-                    sl = sl >= RING ? sl - RING : sl;
-                    const float x = __fsub_rn(fabsf(__fmaf_rn(fs_, __fsub_rn(c.col[sl * RP], v0), -(float)jw)), vk.tlo);
-                    XH = push(XH, x);
-                    jl = x < 0.0f ? jw : jl;
-                }
+                if (A3 > SX) { SX = A3; SA = r + 3; }
+                const float fr = __fsub_rn(__fsub_rn(A0, vk.T), SX);
+                XFR = push(XFR, fr);
+                if (fr < 0.0f) sab[r * 32 + lane] = (int16_t)SA;     // witness of a survivor
                 A3 = A2; A2 = A1; A1 = A0; v2 = v1; v1 = v0;
                 ip = __fsub_rn(ip, 1.0f);
             }
-            // tails: delta1 at 32k - 1, delta2 at 32k - 1 and 32k - 2
-            const float vm1 = c.col[slot_of(32 * k - 1) * RP], vm2 = c.col[slot_of(32 * k - 2) * RP];
+            // tails: delta1 at 32k - 1, delta2 at 32k - 1 and 32k - 2 (chunk k - 1)
+            cp_wait<0>();
+            __syncwarp();
+            const float vm1 = nxt[31 * SP + lane], vm2 = nxt[30 * SP + lane];
             const float d1m = __fsub_rn(v1, vm1), d2m1 = __fsub_rn(v2, vm1), d2m2 = __fsub_rn(v1, vm2);
             const uint32_t s1m = sgnbit(d1m), g1m = sgnbit(__fsub_rn(fabsf(d1m), a1n));
             const uint32_t t1m = (g1m ^ 1u) & sgnbit(__fsub_rn(fabsf(d1m), bhi0));
@@ -796,26 +841,29 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 const uint32_t C3 = cov_p_k(cp, tau0, h, 3);
                 uint32_t mP = ((T1 & ~Xs1) & cov_p_k(cp, tau0, h, 1)) | ((T2 & ~Xs2) & cov_p_k(cp, tau0, h, 2));
                 if (NFWD) mP |= (((TF & Xs1) << 1) | (tfm & s1m)) & cov_p_f(cp, tau0, h);
-                mP |= XH & C3;
                 const uint32_t surv = XFR & C3 & ~mP;
                 uint32_t left = 0u;
                 Blk b;
                 if (__any_sync(FULL, surv != 0u)) {
-                    b.tau0 = tau0; b.base = base;
-                    b.wlo = tau0 - 32; b.whi = min(tau0 + 32 * (RCH - 2) - 1, 32 * kS + 31);
+                    b.tau0 = tau0;
                     b.Wc = cand_bits32(cwP, tau0 + h, WB, lane); b.cfall = cp.pcl;
-                    mP |= resolve<1>(c, surv, b, vk, a.p, jl, qbuf, qn, MP, left);
+                    b.sab = sab; b.T0 = T0;
+                    mP |= resolve<1>(c, surv, b, vk, a.p, jl, qbuf, qn, MP, left, vP);
                 }
                 store_block(c, MP, mP, k);
                 while (__any_sync(FULL, left != 0u)) {        // queue overflow (rare)
-                    flush_queue<1>(c, qbuf, qn, vk, a.p, MP);
+                    flush_queue<1>(c, qbuf, qn, vk, a.p, MP, vP);
                     qn = 0;
                     left = queue_bits<1>(c, b, h, left, QCAP / 32, qbuf, qn);
+                }
+                if (qn >= 32) {          // a full lane batch: search while its lines are L1-hot
+                    flush_queue<1>(c, qbuf, qn, vk, a.p, MP, vP);
+                    qn = 0;
                 }
             }
         }
         cp_wait<0>();
-        if (vP >= 0 && qn > 0) flush_queue<1>(c, qbuf, qn, vk, a.p, MP);
+        if (vP >= 0 && qn > 0) flush_queue<1>(c, qbuf, qn, vk, a.p, MP, vP);
         qn = 0;
     }
     if (vN < 0) return;
@@ -823,28 +871,30 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
 
     // ---------------------------------------------------- pass B (ascending)
     // Far filter of view -b: SX = max A(q) over q <= i - 3, A = s v + pos,
-    // with its witness SA, and the witness probe toward lower tau.
+    // with its witness SA parked for every survivor.
     {
         const int32_t kS = min(max(kB - nbr, kEmin), kB);
         float A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY;
         int32_t SA = 0, jl = 0;
-        fill_chunk(c, kS - 1);               // guard chunk for the witness probes of block kS
-        fill_chunk(c, kS); cp_commit();
+        int slot = 0;
+        stage_chunk(c, stg, kS);
+        cp_commit();
         for (int32_t k = kS; k <= kT; ++k) {
+            const float *cb = stg + slot * 32 * SP + lane;
+            float *nxt = stg + (slot ^ 1) * 32 * SP;
             __syncwarp();
-            if (k + 1 <= kT) fill_chunk(c, k + 1);
+            if (k + 1 <= kT) stage_chunk(c, nxt, k + 1);
             cp_commit();
             cp_wait<1>();
             __syncwarp();
-            const int base = slot_of(32 * k);
-            const float *cb = c.col + base * RP;
+            slot ^= 1;
             float ip = (float)(32 * k - T0);
+            SA -= 32;                                  // witness offset relative to tau0 = 32 k
             if (k < kB) {
 #pragma unroll 8
                 for (int r = 0; r < 32; ++r) {
-                    const float v0 = cb[r * RP];
-                    const float A0 = __fmaf_rn(fs_, v0, ip);
-                    if (A3 > SX) { SX = A3; SA = 32 * k + r - 3; }
+                    const float A0 = __fmaf_rn(fs_, cb[r * SP], ip);
+                    if (A3 > SX) { SX = A3; SA = r - 3; }
                     A3 = A2; A2 = A1; A1 = A0;
                     ip = __fadd_rn(ip, 1.0f);
                 }
@@ -852,56 +902,43 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             }
             const int32_t tau0 = 32 * k;
             const CovN cn = cov_n(cwN, tau0, h, WB, lane);
-            // probe offsets j <= dcov(i) = i + h - nc(i - h) and inside the ring
-            // window (tau - j >= max(tau0 - 96, 32 kS - 3)); nc from the candidate
-            // bits of [tau0 - h, tau0 - h + 31]
-            const uint32_t Wl = cand_bits32(cwN, tau0 - h, WB, lane);
-            const int32_t ll = tau0 - h - 1, eB = tau0 + h;
-            const int32_t wbot = min(32 * (RCH - 2), tau0 - 32 * kS + 3);
-            uint32_t XFR = 0, XH = 0;
+            uint32_t XFR = 0;
 #pragma unroll 8
             for (int r = 0; r < 32; ++r) {
-                const float v0 = cb[r * RP];
-                const float A0 = __fmaf_rn(fs_, v0, ip);
-                if (A3 > SX) { SX = A3; SA = tau0 + r - 3; }
-                XFR = push(XFR, __fsub_rn(__fsub_rn(A0, vk.T), SX));
-                {   // witness probe toward lower tau
-                    const uint32_t m = Wl & (FULL << r);
-                    const int32_t ncr = m ? ll + __ffs(m) : cn.ncl;
-                    const float g = fminf(fmaxf(__fsub_rn(SX, A0), 0.0f), 4096.0f);
-                    const int32_t jw = max(3, min((tau0 + r) - SA + __float2int_rn(g), min(eB - ncr, wbot) + r));
-                    int32_t sl = base + r - jw;
-                    sl = sl < 0 ? sl + RING : sl;
-                    const float x = __fsub_rn(fabsf(__fmaf_rn(fs_, __fsub_rn(c.col[sl * RP], v0), -(float)jw)), vk.tlo);
-                    XH = push(XH, x);
-                    jl = x < 0.0f ? jw : jl;
-                }
+                const float A0 = __fmaf_rn(fs_, cb[r * SP], ip);
+                if (A3 > SX) { SX = A3; SA = r - 3; }
+                const float fr = __fsub_rn(__fsub_rn(A0, vk.T), SX);
+                XFR = push(XFR, fr);
+                if (fr < 0.0f) sab[r * 32 + lane] = (int16_t)SA;     // witness of a survivor
                 A3 = A2; A2 = A1; A1 = A0;
                 ip = __fadd_rn(ip, 1.0f);
             }
             XFR = __brev(XFR);                     // bit r <-> tau0 + r
-            XH = __brev(XH);
             const uint32_t C3 = cov_n_k(cn, tau0, h, 3);
-            uint32_t mN = nn[(k - kB) * 32 + lane] | (XH & C3);
+            uint32_t mN = nn[(k - kB) * 32 + lane];
             const uint32_t surv = XFR & C3 & ~mN;
             uint32_t left = 0u;
             Blk b;
             if (__any_sync(FULL, surv != 0u)) {
-                b.tau0 = tau0; b.base = base;
-                b.wlo = max(tau0 - 32 * (RCH - 2), 32 * kS); b.whi = tau0 + 31;
+                b.tau0 = tau0;
                 b.Wc = cand_bits32(cwN, tau0 - h, WB, lane); b.cfall = cn.ncl;
-                mN |= resolve<-1>(c, surv, b, vk, a.p, jl, qbuf, qn, MN, left);
+                b.sab = sab; b.T0 = T0;
+                mN |= resolve<-1>(c, surv, b, vk, a.p, jl, qbuf, qn, MN, left, vN);
             }
             dbg_add(c.dbg, 7, 32u);
             store_block(c, MN, mN, k);
             while (__any_sync(FULL, left != 0u)) {            // queue overflow (rare)
-                flush_queue<-1>(c, qbuf, qn, vk, a.p, MN);
+                flush_queue<-1>(c, qbuf, qn, vk, a.p, MN, vN);
                 qn = 0;
                 left = queue_bits<-1>(c, b, h, left, QCAP / 32, qbuf, qn);
             }
+            if (qn >= 32) {              // a full lane batch: search while its lines are L1-hot
+                flush_queue<-1>(c, qbuf, qn, vk, a.p, MN, vN);
+                qn = 0;
+            }
         }
         cp_wait<0>();
-        if (qn > 0) flush_queue<-1>(c, qbuf, qn, vk, a.p, MN);
+        if (qn > 0) flush_queue<-1>(c, qbuf, qn, vk, a.p, MN, vN);
     }
 }
 
@@ -915,28 +952,83 @@ __global__ void __launch_bounds__(32) k_line(LineArgs a) {
     const LineUnit u = a.units[blockIdx.x / (unsigned)a.frames];
     const GroupDesc gd = a.groups[u.group];
     const FamilyDesc fd = a.fams[gd.fam];
+    const long long t0 = a.dbg ? clock64() : 0;
     unit_body<CB>(a, u, gd, fd, f, smem);
+    if (a.dbg && (threadIdx.x & 31) == 0 && blockIdx.x < 32768u) {
+        a.dbg[16 + blockIdx.x] = (unsigned long long)(clock64() - t0);
+        a.dbg[16 + 32768 + blockIdx.x] = ((unsigned long long)fd.kind << 60) | ((unsigned long long)(u.t1 - u.t0) << 40) |
+                                         ((unsigned long long)(u.l0 + 40000) << 20) | (unsigned long long)(u.t0 + 40000);
+    }
+}
+
+// Exhaustive far-partner searches queued by k_line: one thread per entry
+// (survivor p of view v in frame f), offsets 3..dcov(p) along its line, 16
+// loads in flight; a confirmed Eq. 5 pair sets the mask byte.
+__global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
+                                              int64_t HW, int32_t nviews, const ViewDesc *__restrict__ views,
+                                              Params p, const HardEntry *__restrict__ gq,
+                                              const uint32_t *__restrict__ gq_count, int32_t gq_cap) {
+    const uint32_t n = min(*gq_count, (uint32_t)gq_cap);
+    const float NaN = __int_as_float(0x7fc00000);
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const HardEntry he = gq[e];
+        const int32_t f = he.fv >> 8, v = he.fv & 255;
+        const int32_t s = views[v].s;
+        ViewK vk;
+        vk.s = s; vk.h = 0; vk.fs = (float)s; vk.T = 0.0f;
+        vk.tlo = __fsub_rn(p.t_dist, 0x1p-10f);
+        vk.thi = __fadd_rn(p.t_dist, 0x1p-10f);
+        const float *Ds = D + (int64_t)f * HW + he.pix;
+        const float vp = __ldg(Ds);
+        bool hit = false;
+        for (int32_t j0 = 3; j0 <= he.jm && !hit; j0 += 16) {
+            float vq[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= he.jm) ? __ldg(Ds + (int64_t)(j0 + u) * he.step) : NaN;
+#pragma unroll 4
+            for (int u = 0; u < 16; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
+        }
+        if (hit) masks[((int64_t)f * nviews + v) * HW + he.pix] = 1;
+    }
+}
+
+cudaError_t launch_hard(const float *D, uint8_t *masks, int64_t HW, int32_t nviews, const ViewDesc *views,
+                        const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
+                        int32_t nsm, cudaStream_t s) {
+    k_hard<<<nsm * 8, 256, 0, s>>>(D, masks, HW, nviews, views, p, gq, gq_count, gq_cap);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
                         const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
-                        const void *codes, int32_t code_bytes, unsigned long long *dbg, cudaStream_t s) {
+                        const void *codes, int32_t code_bytes, unsigned long long *dbg, HardEntry *gq,
+                        uint32_t *gq_count, int32_t gq_cap, cudaStream_t s) {
     if (nunits <= 0) return cudaSuccess;
-    LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch};
+    LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch, gq, gq_count, gq_cap};
     dim3 grid((unsigned)nunits * (unsigned)batch);
     cudaError_t e;
+    // shared memory holds only per-warp bit words / queues; the rest of the
+    // SM's 256 KB serves as L1 for the line reads and partner probes
+    static int carve = -2;
+    if (carve == -2) {
+        const char *ev = getenv("OCC_LINE_CARVEOUT");
+        carve = ev ? atoi(ev) : 60;
+    }
     if (code_bytes == 1) {
         e = cudaFuncSetAttribute(k_line<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
         if (e != cudaSuccess) return e;
+        if (carve >= 0) cudaFuncSetAttribute(k_line<1>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         k_line<1><<<grid, 32, WSMEM, s>>>(a);
     } else if (code_bytes == 2) {
         e = cudaFuncSetAttribute(k_line<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
         if (e != cudaSuccess) return e;
+        if (carve >= 0) cudaFuncSetAttribute(k_line<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         k_line<2><<<grid, 32, WSMEM, s>>>(a);
     } else {
         e = cudaFuncSetAttribute(k_line<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
         if (e != cudaSuccess) return e;
+        if (carve >= 0) cudaFuncSetAttribute(k_line<4>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         k_line<4><<<grid, 32, WSMEM, s>>>(a);
     }
     return cudaGetLastError();

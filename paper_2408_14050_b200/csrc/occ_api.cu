@@ -34,6 +34,9 @@ struct occ_ctx {
     LineUnit *d_units = nullptr;
     TileDesc *d_all_tiles = nullptr;
     unsigned long long *d_dbg = nullptr;  // k_line event counters (occ_debug_line_stats)
+    HardEntry *d_gq = nullptr;            // k_line -> k_hard queue (one chunk)
+    uint32_t *d_gq_count = nullptr;
+    int32_t gq_cap = 0, nsm = 148;
     void *d_codes = nullptr;             // K0 -> K1 candidate codes, one chunk of frames
     int32_t code_bytes = 1, chunk = 1;
     float *d_stage_D = nullptr;          // occ_detect_host staging (lazy)
@@ -247,6 +250,15 @@ void build_tiles(occ_ctx *c) {
         eligible[gi] = line_eligible(c, c->groups[gi]);
         if (eligible[gi]) add_line_units(c, gi);
     }
+    // longest units first (diagonal families sweep ~1.7x the work per
+    // position): the last wave of warps is made of short units
+    std::stable_sort(c->units.begin(), c->units.end(), [&](const LineUnit &x, const LineUnit &y) {
+        auto cost = [&](const LineUnit &u) {
+            const int32_t kind = c->fams[c->groups[u.group].fam].kind;
+            return (double)(u.t1 - u.t0 + 96) * (kind >= 2 ? 1.7 : 1.0);
+        };
+        return cost(x) > cost(y);
+    });
     for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi) {
         const FamilyDesc &fd = c->fams[c->groups[gi].fam];
         const int32_t num = fd.num, den = fd.den;
@@ -365,6 +377,7 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
     }
 
     if (cudaGetDevice(&c->device) != cudaSuccess) { cudaGetLastError(); delete c; return OCC_ERR_CUDA; }
+    if (cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess) c->nsm = 148;
     if (cudaMalloc(&c->d_views, sizeof(ViewDesc) * c->views.size()) != cudaSuccess ||
         cudaMalloc(&c->d_fams, sizeof(FamilyDesc) * c->fams.size()) != cudaSuccess ||
         cudaMalloc(&c->d_groups, sizeof(GroupDesc) * c->groups.size()) != cudaSuccess ||
@@ -372,7 +385,11 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
         cudaMalloc(&c->d_all_tiles, sizeof(TileDesc) * std::max<size_t>(1, c->all_tiles.size())) != cudaSuccess ||
         cudaMalloc(&c->d_units, sizeof(LineUnit) * std::max<size_t>(1, c->units.size())) != cudaSuccess ||
         cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess ||
-        cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess) {
+        cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
+        (!c->units.empty() &&
+         (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = (int32_t)std::min<double>(
+              16.0 * 1048576.0, std::max(65536.0, (double)c->chunk * H * W * n_views / 64.0)))) != cudaSuccess ||
+          cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess))) {
         cudaGetLastError();
         occ_destroy(c);
         return OCC_ERR_OOM;
@@ -446,10 +463,14 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
             const bool tiled_only = c->path == OCC_PATH_TILED;
             if (!tiled_only && !c->units.empty()) {
                 ProfScope pl(c, OCC_KERNEL_LINE, s);
+                CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
                 CK(launch_line(Dc, c->H, c->W, n, c->d_units, (int32_t)c->units.size(), c->d_groups,
                                c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params,
-                               M + (int64_t)c0 * c->V * HW, c->d_codes, c->code_bytes, c->d_dbg, s));
-                ++launches;
+                               M + (int64_t)c0 * c->V * HW, c->d_codes, c->code_bytes, c->d_dbg, c->d_gq,
+                               c->d_gq_count, c->gq_cap, s));
+                CK(launch_hard(Dc, M + (int64_t)c0 * c->V * HW, HW, c->V, c->d_views, c->params, c->d_gq,
+                               c->d_gq_count, c->gq_cap, c->nsm, s));
+                launches += 2;
                 pl.end();
             }
             const TileDesc *tl = tiled_only ? c->d_all_tiles : c->d_tiles;
@@ -547,21 +568,22 @@ int occ_profile_read(occ_ctx *c, int32_t kind, double *total_ms, int32_t *launch
 
 // Debug statistics of the line-sweep kernel (not part of include/occ.h):
 // enable != 0 allocates/zeroes 16 counters that subsequent occ_detect calls
-// accumulate; out (host, 16 entries, may be NULL) receives the current values.
+// accumulate, plus per-CTA cycle counts of the last launch (entries 16..);
+// out (host, 16 + 65536 entries, may be NULL) receives the current values.
 int occ_debug_line_stats(occ_ctx *c, int32_t enable, unsigned long long *out) {
     if (!c) return OCC_ERR_INVALID_ARG;
     CK(cudaSetDevice(c->device));
     if (out) {
         if (c->d_dbg) {
             CK(cudaDeviceSynchronize());
-            CK(cudaMemcpy(out, c->d_dbg, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(out, c->d_dbg, (16 + 65536 + 4 * 32768) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
         } else {
-            memset(out, 0, 16 * sizeof(unsigned long long));
+            memset(out, 0, (16 + 65536 + 4 * 32768) * sizeof(unsigned long long));
         }
     }
     if (enable) {
-        if (!c->d_dbg) CK(cudaMalloc(&c->d_dbg, 16 * sizeof(unsigned long long)));
-        CK(cudaMemset(c->d_dbg, 0, 16 * sizeof(unsigned long long)));
+        if (!c->d_dbg) CK(cudaMalloc(&c->d_dbg, (16 + 65536 + 4 * 32768) * sizeof(unsigned long long)));
+        CK(cudaMemset(c->d_dbg, 0, (16 + 65536 + 4 * 32768) * sizeof(unsigned long long)));
     } else if (c->d_dbg) {
         CK(cudaFree(c->d_dbg));
         c->d_dbg = nullptr;
@@ -582,6 +604,8 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_all_tiles);
     cudaFree(c->d_units);
     cudaFree(c->d_dbg);
+    cudaFree(c->d_gq);
+    cudaFree(c->d_gq_count);
     cudaFree(c->d_stage_D);
     cudaFree(c->d_stage_M);
     for (int k = 0; k < OCC_KERNEL_KINDS; ++k)

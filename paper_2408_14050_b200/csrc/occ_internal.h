@@ -106,17 +106,27 @@ cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
 // Line-sweep kernel (k_line.cu) for the four line families of |b| <= 1
 // arrays: one warp per unit = 32 consecutive lines x [t0, t1) in the lane's
 // time coordinate (t0, t1 multiples of 32, t1 - t0 <= kLineSeg).
-constexpr int kLineSeg = 512;
+constexpr int kLineSeg = 256;
 constexpr int kLineRingChunks = 5;       // ring of 5 x 32 staged positions per warp
 constexpr int kLineCandMarginWords = 4;  // candidate words staged beyond the segment (h + 32 <= 128)
 struct LineUnit {
     int32_t group, l0, t0, t1;
 };
+// An exhaustive far-partner search deferred to k_hard: survivor at pixel
+// index pix of frame f, view v (fv = f << 8 | v); partners at pix + j * step,
+// j = 3 .. jm (jm = dcov clipped to the image).
+struct HardEntry {
+    int32_t pix, step, jm, fv;
+};
 size_t line_smem_bytes();
 cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
                         const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
-                        const void *codes, int32_t code_bytes, unsigned long long *dbg, cudaStream_t s);
+                        const void *codes, int32_t code_bytes, unsigned long long *dbg, HardEntry *gq,
+                        uint32_t *gq_count, int32_t gq_cap, cudaStream_t s);
+cudaError_t launch_hard(const float *D, uint8_t *masks, int64_t HW, int32_t nviews, const ViewDesc *views,
+                        const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
+                        int32_t nsm, cudaStream_t s);
 cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
                             const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
                             FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s);
