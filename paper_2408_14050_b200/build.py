@@ -36,6 +36,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build_obj")
     os.makedirs(objdir, exist_ok=True)
     cflags = [f for f in FLAGS if f != "-shared"]
+    if os.environ.get("OCC_LINE_STATS"):        # event counters of k_line (tools/line_stats.py)
+        cflags.append("-DOCC_LINE_STATS")
     jobs = []
     hdr_newest = max(os.path.getmtime(p) for p in deps if not p.endswith(".cu"))
     for src in sources():

@@ -100,8 +100,20 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 // 4 mask bits -> 4 bytes 0/1
 __device__ __forceinline__ uint32_t expand4(uint32_t b4) { return (b4 * 0x00204081u) & 0x01010101u; }
 
+// per-CTA phase timers (debug statistics only)
+#ifdef OCC_LINE_STATS
+#define OCC_PH_T0(v) const long long v = clock64()
+#define OCC_PH_T1(c, i, v) do { if ((c).ph && ((c).lane == 0)) (c).ph[i] += (unsigned long long)(clock64() - (v)); } while (0)
+#else
+#define OCC_PH_T0(v) do { } while (0)
+#define OCC_PH_T1(c, i, v) do { } while (0)
+#endif
+
 // warp-aggregated event counter (debug statistics only)
 __device__ __forceinline__ void dbg_add(unsigned long long *dbg, int idx, uint32_t n) {
+#ifndef OCC_LINE_STATS
+    return;
+#endif
     if (!dbg) return;
     const uint32_t tot = __reduce_add_sync(__activemask(), n);
     if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && tot) atomicAdd(dbg + idx, (unsigned long long)tot);
@@ -212,6 +224,7 @@ struct LineArgs {
     HardEntry *gq;             // global queue of exhaustive searches (k_hard), capacity gq_cap
     uint32_t *gq_count;
     int32_t gq_cap;
+    int32_t nwork;             // units x frames
 };
 
 // Per-warp context
@@ -390,6 +403,7 @@ struct Blk {
     int32_t tau0;          // block start
     uint32_t Wc;           // candidate bits of [tau0 + h, +31] (+b) / [tau0 - h, +31] (-b)
     int32_t cfall;         // last candidate < tau0 + h (+b) / first candidate >= tau0 + 32 - h (-b)
+    const float *cb;       // the block's staged values, lane column ([r * SP])
     const int16_t *sab;    // filter witness of each survivor, relative to tau0 ([r][lane])
     int32_t T0;
 };
@@ -434,7 +448,7 @@ __device__ __forceinline__ bool pair_far(float vq, float vp, int32_t j, const Vi
 template <int DIR>
 __device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int32_t qn, const ViewK &vk,
                                          const Params &p, uint8_t *Mv, int32_t vid) {
-    const long long tph = clock64();
+    OCC_PH_T0(tph);
     __syncwarp();
     const float NaN = __int_as_float(0x7fc00000);
     // normally the searches go to the global queue, resolved after this
@@ -455,7 +469,7 @@ __device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int3
                 c.gq[base + (uint32_t)e] = he;
             }
             __syncwarp();
-            if (c.ph && c.lane == 0) c.ph[1] += (unsigned long long)(clock64() - tph);
+            OCC_PH_T1(c, 1, tph);
             return;
         }
     }
@@ -480,7 +494,7 @@ __device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int3
         }
     }
     __syncwarp();
-    if (c.ph && c.lane == 0) c.ph[1] += (unsigned long long)(clock64() - tph);
+    OCC_PH_T1(c, 1, tph);
 }
 
 // Appends the survivors of `bits` (bit r <-> tau0 + r) to the deferred queue,
@@ -527,44 +541,82 @@ __device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b,
                                          uint8_t *Mv, uint32_t &left, int32_t vid) {
     const int lane = c.lane;
     const int32_t h = vk.h;
-    const long long tph = clock64();
+    OCC_PH_T0(tph);
     uint32_t hits = 0u, hard = 0u;
     dbg_add(c.dbg, DIR > 0 ? 0 : 1, __popc(S));
-    while (__any_sync(FULL, S != 0u)) {
+    // 1. the line's last far offset jl for every survivor of the block (bands:
+    //    the partner offset moves with the pixel), 4 independent probes per
+    //    round; vp from the staged chunk
+    uint32_t miss = 0u;
+    {
+        const int32_t j = jl;
+        uint32_t T = S;
+        while (__any_sync(FULL, T != 0u)) {
+            int32_t rr[4];
+            float vq[4], vpv[4];
+            int32_t jmv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                rr[u] = -1;
+                if (T) { rr[u] = DIR > 0 ? 31 - __clz(T) : __ffs(T) - 1; T &= ~(1u << rr[u]); }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                vq[u] = __int_as_float(0x7fc00000);
+                vpv[u] = 0.0f;
+                jmv[u] = 0;
+                if (rr[u] >= 0) {
+                    const int32_t tau = b.tau0 + rr[u];
+                    vpv[u] = b.cb[rr[u] * SP];
+                    jmv[u] = min(dcov_of<DIR>(b.Wc, b.cfall, b.tau0, rr[u], h),
+                                 DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
+                    if (j >= 3 && j <= jmv[u]) vq[u] = __ldg(c.Dl + (int64_t)(tau + DIR * j) * c.S);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (rr[u] < 0) continue;
+                if (j >= 3 && j <= jmv[u] && pair_far(vq[u], vpv[u], j, vk, p)) hits |= 1u << rr[u];
+                else miss |= 1u << rr[u];
+            }
+        }
+    }
+    // 2. the rest: the filter witness SA parked by the sweep (past it A falls
+    //    ~1 per step on a flat occluder, so the partner sits near
+    //    jw = max(|SA - tau|, s (v_SA - v_p))); probes jw, jw + 1, jw - 1 in
+    //    parallel, then one secant step from jw
+    while (__any_sync(FULL, miss != 0u)) {
         dbg_add(c.dbg, 9, 1u);
-        if (S) {
-            const int32_t r = DIR > 0 ? 31 - __clz(S) : __ffs(S) - 1;
-            S &= ~(1u << r);
+        if (miss) {
+            const int32_t r = DIR > 0 ? 31 - __clz(miss) : __ffs(miss) - 1;
+            miss &= ~(1u << r);
             const int32_t tau = b.tau0 + r;
-            const float vp = __ldg(c.Dl + (int64_t)tau * c.S);
+            const float vp = b.cb[r * SP];
             int32_t jm = dcov_of<DIR>(b.Wc, b.cfall, b.tau0, r, h);
             jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
-            // 1. the line's last far offset jl (bands: the partner offset moves
-            //    with the pixel, so consecutive survivors share it)
-            bool hit = jl >= 3 && jl <= jm &&
-                       pair_far(probe_b(c, b, lane, tau + DIR * jl, c.elo, c.ehi), vp, jl, vk, p);
-            if (!hit) {
-                // 2. the filter witness SA (parked by the sweep): past it A falls ~1
-                //    per step on a flat occluder, so the partner sits near
-                //    jw = max(|SA - tau|, s (v_SA - v_p)); probe jw, jw + 1, jw - 1
-                //    and one secant step from jw
-                const int32_t SAa = b.tau0 + (int32_t)b.sab[r * 32 + lane];
-                const float vsa = probe_b(c, b, lane, SAa, c.elo, c.ehi);
-                const float g = fminf(fmaxf(__fmul_rn(vk.fs, __fsub_rn(vsa, vp)), 0.0f), 4096.0f);
-                const int32_t jw = max(DIR * (SAa - tau), __float2int_rn(g));
-                float y0 = 0.0f;
+            const int32_t SAa = b.tau0 + (int32_t)b.sab[r * 32 + lane];
+            const float vsa = probe_b(c, b, lane, SAa, c.elo, c.ehi);
+            const float g = fminf(fmaxf(__fmul_rn(vk.fs, __fsub_rn(vsa, vp)), 0.0f), 4096.0f);
+            const int32_t jw = max(DIR * (SAa - tau), __float2int_rn(g));
+            float vq[3];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    int32_t j = q == 0 ? jw : (q == 1 ? jw + 1 : (q == 2 ? jw - 1 : jw + (int32_t)rintf(y0)));
-                    if ((q == 3 && j >= jw - 1 && j <= jw + 1) || j == jl) j = -1;
-                    if (!hit && j >= 3 && j <= jm) {
-                        const float vq = probe_b(c, b, lane, tau + DIR * j, c.elo, c.ehi);
-                        if (q == 0) {
-                            const float yy = __fmaf_rn(vk.fs, __fsub_rn(vq, vp), -(float)j);
-                            y0 = (yy == yy) ? fminf(fmaxf(yy, -64.0f), 64.0f) : 0.0f;
-                        }
-                        if (pair_far(vq, vp, j, vk, p)) { hit = true; jl = j; }
-                    }
+            for (int u = 0; u < 3; ++u) {
+                const int32_t jj = jw + (u == 0 ? 0 : (u == 1 ? 1 : -1));
+                vq[u] = (jj >= 3 && jj <= jm) ? __ldg(c.Dl + (int64_t)(tau + DIR * jj) * c.S)
+                                              : __int_as_float(0x7fc00000);
+            }
+            bool hit = false;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int32_t jj = jw + (u == 0 ? 0 : (u == 1 ? 1 : -1));
+                if (!hit && pair_far(vq[u], vp, jj, vk, p)) { hit = true; jl = jj; }
+            }
+            if (!hit) {
+                const float yy = __fmaf_rn(vk.fs, __fsub_rn(vq[0], vp), -(float)jw);
+                const int32_t js = jw + (yy == yy ? (int32_t)rintf(fminf(fmaxf(yy, -64.0f), 64.0f)) : 0);
+                if ((js < jw - 1 || js > jw + 1) && js >= 3 && js <= jm &&
+                    pair_far(__ldg(c.Dl + (int64_t)(tau + DIR * js) * c.S), vp, js, vk, p)) {
+                    hit = true; jl = js;
                 }
             }
             if (hit) hits |= 1u << r; else hard |= 1u << r;
@@ -585,7 +637,7 @@ __device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b,
         }
         left = queue_bits<DIR>(c, b, h, hard, tot <= QCAP ? 32 : QCAP / 32, qbuf, qn);
     }
-    if (c.ph && lane == 0) c.ph[0] += (unsigned long long)(clock64() - tph);
+    OCC_PH_T1(c, 0, tph);
     return hits;
 }
 
@@ -680,7 +732,15 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     c.dbg = a.dbg;
     c.f = f;
     c.gq = a.gq; c.gq_count = a.gq_count; c.gq_cap = a.gq_cap;
-    c.ph = (a.dbg && blockIdx.x < 32768u) ? a.dbg + 16 + 2 * 32768 + 4 * blockIdx.x : nullptr;
+    {
+        const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+#ifdef OCC_LINE_STATS
+        c.ph = (a.dbg && wid < 32768u) ? a.dbg + 16 + 2 * 32768 + 4 * wid : nullptr;
+#else
+        c.ph = nullptr;
+        (void)wid;
+#endif
+    }
     c.kind = kind;
     c.Df = a.D + (int64_t)f * HW;
     c.H = H; c.W = W; c.l0 = u.l0; c.lane = lane;
@@ -747,9 +807,9 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     const int32_t WB = kB - CMW;
     {
         const unsigned char *codesf = reinterpret_cast<const unsigned char *>(a.codes) + (int64_t)f * HW * CB;
-        const long long tph = clock64();
+        OCC_PH_T0(tph);
         build_cand<CB>(c, codesf, 2 * gd.fam, WB, cw);
-        if (c.ph && lane == 0) c.ph[2] += (unsigned long long)(clock64() - tph);
+        OCC_PH_T1(c, 2, tph);
     }
     const uint32_t *cwP = cw, *cwN = cw + NCW * 32;
     __syncwarp();
@@ -845,7 +905,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 uint32_t left = 0u;
                 Blk b;
                 if (__any_sync(FULL, surv != 0u)) {
-                    b.tau0 = tau0;
+                    b.tau0 = tau0; b.cb = cb;
                     b.Wc = cand_bits32(cwP, tau0 + h, WB, lane); b.cfall = cp.pcl;
                     b.sab = sab; b.T0 = T0;
                     mP |= resolve<1>(c, surv, b, vk, a.p, jl, qbuf, qn, MP, left, vP);
@@ -920,7 +980,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             uint32_t left = 0u;
             Blk b;
             if (__any_sync(FULL, surv != 0u)) {
-                b.tau0 = tau0;
+                b.tau0 = tau0; b.cb = cb;
                 b.Wc = cand_bits32(cwN, tau0 - h, WB, lane); b.cfall = cn.ncl;
                 b.sab = sab; b.T0 = T0;
                 mN |= resolve<-1>(c, surv, b, vk, a.p, jl, qbuf, qn, MN, left, vN);
@@ -944,21 +1004,27 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
 
 // grid: (units, frames); one warp per block
 template <int CB>
-__global__ void __launch_bounds__(32) k_line(LineArgs a) {
+__global__ void __launch_bounds__(128) k_line(LineArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    // frames fastest: co-resident warps work on the same line family (shared
-    // instruction cache footprint) and on neighbouring frames
-    const int32_t f = (int32_t)(blockIdx.x % (unsigned)a.frames);
-    const LineUnit u = a.units[blockIdx.x / (unsigned)a.frames];
+    // one work unit per warp; frames fastest: co-resident warps work on the
+    // same line family and start together (shared instruction-cache footprint)
+    const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (wid >= (uint32_t)a.nwork) return;
+    const int32_t f = (int32_t)(wid % (unsigned)a.frames);
+    const LineUnit u = a.units[wid / (unsigned)a.frames];
     const GroupDesc gd = a.groups[u.group];
     const FamilyDesc fd = a.fams[gd.fam];
+#ifdef OCC_LINE_STATS
     const long long t0 = a.dbg ? clock64() : 0;
-    unit_body<CB>(a, u, gd, fd, f, smem);
-    if (a.dbg && (threadIdx.x & 31) == 0 && blockIdx.x < 32768u) {
-        a.dbg[16 + blockIdx.x] = (unsigned long long)(clock64() - t0);
-        a.dbg[16 + 32768 + blockIdx.x] = ((unsigned long long)fd.kind << 60) | ((unsigned long long)(u.t1 - u.t0) << 40) |
-                                         ((unsigned long long)(u.l0 + 40000) << 20) | (unsigned long long)(u.t0 + 40000);
+#endif
+    unit_body<CB>(a, u, gd, fd, f, smem + (size_t)(threadIdx.x >> 5) * WSMEM);
+#ifdef OCC_LINE_STATS
+    if (a.dbg && (threadIdx.x & 31) == 0 && wid < 32768u) {
+        a.dbg[16 + wid] = (unsigned long long)(clock64() - t0);
+        a.dbg[16 + 32768 + wid] = ((unsigned long long)fd.kind << 60) | ((unsigned long long)(u.t1 - u.t0) << 40) |
+                                  ((unsigned long long)(u.l0 + 40000) << 20) | (unsigned long long)(u.t0 + 40000);
     }
+#endif
 }
 
 // Exhaustive far-partner searches queued by k_line: one thread per entry
@@ -1005,8 +1071,15 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
                         const void *codes, int32_t code_bytes, unsigned long long *dbg, HardEntry *gq,
                         uint32_t *gq_count, int32_t gq_cap, cudaStream_t s) {
     if (nunits <= 0) return cudaSuccess;
-    LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch, gq, gq_count, gq_cap};
-    dim3 grid((unsigned)nunits * (unsigned)batch);
+    LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch, gq, gq_count, gq_cap,
+               nunits * batch};
+    static int nw = 0;
+    if (!nw) {
+        const char *ev = getenv("OCC_LINE_WARPS");
+        nw = ev ? max(1, min(4, atoi(ev))) : 4;
+    }
+    dim3 grid((unsigned)((a.nwork + nw - 1) / nw));
+    const size_t smem = WSMEM * (size_t)nw;
     cudaError_t e;
     // shared memory holds only per-warp bit words / queues; the rest of the
     // SM's 256 KB serves as L1 for the line reads and partner probes
@@ -1016,20 +1089,20 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
         carve = ev ? atoi(ev) : 60;
     }
     if (code_bytes == 1) {
-        e = cudaFuncSetAttribute(k_line<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
+        e = cudaFuncSetAttribute(k_line<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         if (carve >= 0) cudaFuncSetAttribute(k_line<1>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-        k_line<1><<<grid, 32, WSMEM, s>>>(a);
+        k_line<1><<<grid, 32 * nw, smem, s>>>(a);
     } else if (code_bytes == 2) {
-        e = cudaFuncSetAttribute(k_line<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
+        e = cudaFuncSetAttribute(k_line<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         if (carve >= 0) cudaFuncSetAttribute(k_line<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-        k_line<2><<<grid, 32, WSMEM, s>>>(a);
+        k_line<2><<<grid, 32 * nw, smem, s>>>(a);
     } else {
-        e = cudaFuncSetAttribute(k_line<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM);
+        e = cudaFuncSetAttribute(k_line<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         if (carve >= 0) cudaFuncSetAttribute(k_line<4>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-        k_line<4><<<grid, 32, WSMEM, s>>>(a);
+        k_line<4><<<grid, 32 * nw, smem, s>>>(a);
     }
     return cudaGetLastError();
 }

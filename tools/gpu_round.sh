@@ -1,11 +1,14 @@
+# Full measurement pass (run under gpurun): GPU tests, smoke, bench, ncu launch list and
+# one full ncu capture of the dominant kernel.  Outputs land in gpurun_out/.
 set -x
 mkdir -p gpurun_out
 nvidia-smi -L > gpurun_out/smi.txt 2>&1; nproc >> gpurun_out/smi.txt; lscpu | head -20 >> gpurun_out/smi.txt
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
+if grep -q "illegal\|CUDA error\|unspecified launch" gpurun_out/gpu_tests.log; then echo "CUDA fault: stop"; exit 3; fi
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tile -s 20 -c 2 -o gpurun_out/prof_tile python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_prologue -s 20 -c 1 -o gpurun_out/prof_pro python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_line -s 20 -c 1 -o gpurun_out/prof_line python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hard -s 20 -c 1 -o gpurun_out/prof_hard python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full_hard.log 2>&1
 echo done
