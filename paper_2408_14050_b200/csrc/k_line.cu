@@ -257,33 +257,39 @@ __device__ __noinline__ void stage_chunk(const Ctx &c, float *st, int32_t k) {
     const float NaN = __int_as_float(0x7fc00000);
     const int lane = c.lane;
     const int32_t t0 = 32 * k;
+    const float *src;
+    float *dst;
+    int64_t step;
+    int32_t dstep, jlo, jhi;
     if (c.kind == 0) {
-        // rows: lane = position, one row segment per line j
+        // rows: lane = position, one coalesced row segment per line j
         const int32_t x = t0 + lane;
-        const int32_t nrow = (x >= 0 && x < c.W) ? min(32, c.H - c.l0) : 0;
-        const float *src = c.Df + (int64_t)c.l0 * c.W + x;
-        float *dst = st + lane * SP;
-        if (nrow == 32) {
-#pragma unroll 8
-            for (int j = 0; j < 32; ++j) cp_async4(dst + j, src + (int64_t)j * c.W);
-        } else {
-            for (int j = 0; j < 32; ++j) {
-                if (j < nrow) cp_async4(dst + j, src + (int64_t)j * c.W); else dst[j] = NaN;
-            }
-        }
+        src = c.Df + (int64_t)c.l0 * c.W + x;
+        step = c.W;
+        dst = st + lane * SP;
+        dstep = 1;
+        jlo = 0;
+        jhi = (x >= 0 && x < c.W) ? min(32, c.H - c.l0) : 0;
     } else {
-        const float *src = c.Dl + (int64_t)t0 * c.S;
-        float *dst = st + lane;
-        if (t0 >= c.elo && t0 + 32 <= c.ehi) {
+        // lane = line: one coalesced run per tau
+        src = c.Dl + (int64_t)t0 * c.S;
+        step = c.S;
+        dst = st + lane;
+        dstep = SP;
+        jlo = c.elo - t0;
+        jhi = c.ehi - t0;
+    }
+    if (__all_sync(FULL, jlo <= 0 && jhi >= 32)) {
+        // interior chunk: 32 unconditional copies, 32-bit offsets
+        const int32_t st32 = (int32_t)step;
 #pragma unroll 8
-            for (int j = 0; j < 32; ++j) cp_async4(dst + j * SP, src + (int64_t)j * c.S);
-        } else {
-            for (int j = 0; j < 32; ++j) {
-                const int32_t tau = t0 + j;
-                if (tau >= c.elo && tau < c.ehi) cp_async4(dst + j * SP, src + (int64_t)j * c.S);
-                else dst[j * SP] = NaN;
-            }
-        }
+        for (int j = 0; j < 32; ++j) cp_async4(dst + j * dstep, src + j * st32);
+        return;
+    }
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+        if (j >= jlo && j < jhi) cp_async4(dst + j * dstep, src + (int64_t)j * step);
+        else dst[j * dstep] = NaN;
     }
 }
 
@@ -311,12 +317,12 @@ __device__ __forceinline__ uint32_t code_at(const void *codes, int64_t idx) {
 // pass 0: candidate words of both views (bit cb and cb + 1 of the codes)
 template <int CB>
 __device__ __noinline__ void build_cand(const Ctx &c, const void *codesf, int32_t cb, int32_t WB,
-                                           uint32_t *cw) {
+                                           uint32_t *cw, int32_t wlo, int32_t whi) {
     const int lane = c.lane;
     for (int w = 0; w < NCW; ++w) {
         const int32_t t0 = 32 * (WB + w);
         uint32_t wp = 0u, wn = 0u;
-        if (t0 + 31 >= c.elo && t0 < c.ehi) {
+        if (w >= wlo && w <= whi && t0 + 31 >= c.elo && t0 < c.ehi) {
             if (c.kind == 0 && CB == 1 && (c.W & 15) == 0 && t0 >= 0 && t0 + 32 <= c.W) {
                 // rows: 32 consecutive codes of the lane's row in two 16-byte loads
                 const uint8_t *row = reinterpret_cast<const uint8_t *>(codesf) + (int64_t)(c.l0 + lane) * c.W + t0;
@@ -415,8 +421,7 @@ __device__ __forceinline__ float probe_b(const Ctx &c, const Blk &b, int32_t l, 
     return gload(c, l, tau);
 }
 // dcov of the survivor at tau0 + r (largest far offset sharing a scan window, App. A.2)
-template <int DIR>
-__device__ __forceinline__ int32_t dcov_of(uint32_t Wc, int32_t cfall, int32_t tau0, int32_t r, int32_t h) {
+__device__ __forceinline__ int32_t dcov_of(const int DIR, uint32_t Wc, int32_t cfall, int32_t tau0, int32_t r, int32_t h) {
     if (DIR > 0) {
         const uint32_t m = Wc & le_mask(r);
         const int32_t pc = m ? tau0 + h + 31 - __clz(m) : cfall;
@@ -445,8 +450,7 @@ __device__ __forceinline__ bool pair_far(float vq, float vp, int32_t j, const Vi
 // line), scanning offsets 3..dcov of its line in global memory (L2) with 16
 // loads in flight; a confirmed Eq. 5 pair sets the mask byte directly (the
 // block store already wrote 0 there).
-template <int DIR>
-__device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int32_t qn, const ViewK &vk,
+__device__ __noinline__ void flush_queue(const int DIR, const Ctx &c, const int32_t *qbuf, int32_t qn, const ViewK &vk,
                                          const Params &p, uint8_t *Mv, int32_t vid) {
     OCC_PH_T0(tph);
     __syncwarp();
@@ -482,12 +486,11 @@ __device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int3
             const int32_t st = DIR * c.S;
             const float vp = __ldg(Ds);
             bool hit = false;
-            for (int32_t j0 = 3; j0 <= jm && !hit; j0 += 16) {
-                float vq[16];
+            for (int32_t j0 = 3; j0 <= jm && !hit; j0 += 4) {
+                float vq[4];
 #pragma unroll
-                for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * st) : NaN;
-#pragma unroll 4
-                for (int u = 0; u < 16; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
+                for (int u = 0; u < 4; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * st) : NaN;
+                for (int u = 0; u < 4; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
             }
             dbg_add(c.dbg, 4, hit ? 1u : 0u);
             if (hit) Mv[line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S] = 1;
@@ -500,8 +503,7 @@ __device__ __noinline__ void flush_queue(const Ctx &c, const int32_t *qbuf, int3
 // Appends the survivors of `bits` (bit r <-> tau0 + r) to the deferred queue,
 // at most `quota` per lane; returns the bits not queued.  Warp-collective;
 // the caller guarantees room for 32 * quota entries.
-template <int DIR>
-__device__ __forceinline__ uint32_t queue_bits(const Ctx &c, const Blk &b, int32_t h, uint32_t bits,
+__device__ __forceinline__ uint32_t queue_bits(const int DIR, const Ctx &c, const Blk &b, int32_t h, uint32_t bits,
                                                int quota, int32_t *qbuf, int32_t &qn) {
     const int lane = c.lane;
     uint32_t take = 0u, t = bits;
@@ -520,7 +522,7 @@ __device__ __forceinline__ uint32_t queue_bits(const Ctx &c, const Blk &b, int32
         const int32_t r = __ffs(w) - 1;
         w &= w - 1u;
         const int32_t tau = b.tau0 + r;
-        int32_t jm = dcov_of<DIR>(b.Wc, b.cfall, b.tau0, r, h);
+        int32_t jm = dcov_of(DIR, b.Wc, b.cfall, b.tau0, r, h);
         jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
         qbuf[2 * pos] = tau;
         qbuf[2 * pos + 1] = (max(jm, 0) << 5) | lane;
@@ -535,8 +537,7 @@ __device__ __forceinline__ uint32_t queue_bits(const Ctx &c, const Blk &b, int32
 // DIR = +1: partners at tau + j (view +b), -1: at tau - j (view -b).
 // These are the survivors the sweep's witness probe did not confirm: first
 // the line's last far offset -1..+2, then a warp-cooperative exhaustive search.
-template <int DIR>
-__device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b, const ViewK &vk,
+__device__ __noinline__ uint32_t resolve(const int DIR, const Ctx &c, uint32_t S, const Blk &b, const ViewK &vk,
                                          const Params &p, int32_t &jl, int32_t *qbuf, int32_t &qn,
                                          uint8_t *Mv, uint32_t &left, int32_t vid) {
     const int lane = c.lane;
@@ -568,7 +569,7 @@ __device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b,
                 if (rr[u] >= 0) {
                     const int32_t tau = b.tau0 + rr[u];
                     vpv[u] = b.cb[rr[u] * SP];
-                    jmv[u] = min(dcov_of<DIR>(b.Wc, b.cfall, b.tau0, rr[u], h),
+                    jmv[u] = min(dcov_of(DIR, b.Wc, b.cfall, b.tau0, rr[u], h),
                                  DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
                     if (j >= 3 && j <= jmv[u]) vq[u] = __ldg(c.Dl + (int64_t)(tau + DIR * j) * c.S);
                 }
@@ -592,7 +593,7 @@ __device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b,
             miss &= ~(1u << r);
             const int32_t tau = b.tau0 + r;
             const float vp = b.cb[r * SP];
-            int32_t jm = dcov_of<DIR>(b.Wc, b.cfall, b.tau0, r, h);
+            int32_t jm = dcov_of(DIR, b.Wc, b.cfall, b.tau0, r, h);
             jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
             const int32_t SAa = b.tau0 + (int32_t)b.sab[r * 32 + lane];
             const float vsa = probe_b(c, b, lane, SAa, c.elo, c.ehi);
@@ -632,10 +633,10 @@ __device__ __noinline__ uint32_t resolve(const Ctx &c, uint32_t S, const Blk &b,
         const int32_t tot = __reduce_add_sync(FULL, __popc(hard));
         if (lane == 0) dbg_add(c.dbg, 10, tot > QCAP ? 1u : 0u);
         if (qn + tot > QCAP) {
-            flush_queue<DIR>(c, qbuf, qn, vk, p, Mv, vid);
+            flush_queue(DIR, c, qbuf, qn, vk, p, Mv, vid);
             qn = 0;
         }
-        left = queue_bits<DIR>(c, b, h, hard, tot <= QCAP ? 32 : QCAP / 32, qbuf, qn);
+        left = queue_bits(DIR, c, b, h, hard, tot <= QCAP ? 32 : QCAP / 32, qbuf, qn);
     }
     OCC_PH_T1(c, 0, tph);
     return hits;
@@ -808,7 +809,9 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     {
         const unsigned char *codesf = reinterpret_cast<const unsigned char *>(a.codes) + (int64_t)f * HW * CB;
         OCC_PH_T0(tph);
-        build_cand<CB>(c, codesf, 2 * gd.fam, WB, cw);
+        // coverage reads candidates within h + 32 of the segment (S8, App. A.2)
+        const int32_t wlo = ((T0 - h - 32) >> 5) - WB, whi = ((T1 + h + 31) >> 5) - WB;
+        build_cand<CB>(c, codesf, 2 * gd.fam, WB, cw, wlo, whi);
         OCC_PH_T1(c, 2, tph);
     }
     const uint32_t *cwP = cw, *cwN = cw + NCW * 32;
@@ -908,22 +911,22 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                     b.tau0 = tau0; b.cb = cb;
                     b.Wc = cand_bits32(cwP, tau0 + h, WB, lane); b.cfall = cp.pcl;
                     b.sab = sab; b.T0 = T0;
-                    mP |= resolve<1>(c, surv, b, vk, a.p, jl, qbuf, qn, MP, left, vP);
+                    mP |= resolve(1, c, surv, b, vk, a.p, jl, qbuf, qn, MP, left, vP);
                 }
                 store_block(c, MP, mP, k);
                 while (__any_sync(FULL, left != 0u)) {        // queue overflow (rare)
-                    flush_queue<1>(c, qbuf, qn, vk, a.p, MP, vP);
+                    flush_queue(1, c, qbuf, qn, vk, a.p, MP, vP);
                     qn = 0;
-                    left = queue_bits<1>(c, b, h, left, QCAP / 32, qbuf, qn);
+                    left = queue_bits(1, c, b, h, left, QCAP / 32, qbuf, qn);
                 }
                 if (qn >= 32) {          // a full lane batch: search while its lines are L1-hot
-                    flush_queue<1>(c, qbuf, qn, vk, a.p, MP, vP);
+                    flush_queue(1, c, qbuf, qn, vk, a.p, MP, vP);
                     qn = 0;
                 }
             }
         }
         cp_wait<0>();
-        if (vP >= 0 && qn > 0) flush_queue<1>(c, qbuf, qn, vk, a.p, MP, vP);
+        if (vP >= 0 && qn > 0) flush_queue(1, c, qbuf, qn, vk, a.p, MP, vP);
         qn = 0;
     }
     if (vN < 0) return;
@@ -983,22 +986,22 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 b.tau0 = tau0; b.cb = cb;
                 b.Wc = cand_bits32(cwN, tau0 - h, WB, lane); b.cfall = cn.ncl;
                 b.sab = sab; b.T0 = T0;
-                mN |= resolve<-1>(c, surv, b, vk, a.p, jl, qbuf, qn, MN, left, vN);
+                mN |= resolve(-1, c, surv, b, vk, a.p, jl, qbuf, qn, MN, left, vN);
             }
             dbg_add(c.dbg, 7, 32u);
             store_block(c, MN, mN, k);
             while (__any_sync(FULL, left != 0u)) {            // queue overflow (rare)
-                flush_queue<-1>(c, qbuf, qn, vk, a.p, MN, vN);
+                flush_queue(-1, c, qbuf, qn, vk, a.p, MN, vN);
                 qn = 0;
-                left = queue_bits<-1>(c, b, h, left, QCAP / 32, qbuf, qn);
+                left = queue_bits(-1, c, b, h, left, QCAP / 32, qbuf, qn);
             }
             if (qn >= 32) {              // a full lane batch: search while its lines are L1-hot
-                flush_queue<-1>(c, qbuf, qn, vk, a.p, MN, vN);
+                flush_queue(-1, c, qbuf, qn, vk, a.p, MN, vN);
                 qn = 0;
             }
         }
         cp_wait<0>();
-        if (qn > 0) flush_queue<-1>(c, qbuf, qn, vk, a.p, MN, vN);
+        if (qn > 0) flush_queue(-1, c, qbuf, qn, vk, a.p, MN, vN);
     }
 }
 
@@ -1076,7 +1079,7 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
     static int nw = 0;
     if (!nw) {
         const char *ev = getenv("OCC_LINE_WARPS");
-        nw = ev ? max(1, min(4, atoi(ev))) : 4;
+        nw = ev ? max(1, min(4, atoi(ev))) : 2;
     }
     dim3 grid((unsigned)((a.nwork + nw - 1) / nw));
     const size_t smem = WSMEM * (size_t)nw;

@@ -42,6 +42,8 @@ struct occ_ctx {
     float *d_stage_D = nullptr;          // occ_detect_host staging (lazy)
     uint8_t *d_stage_M = nullptr;
     cudaStream_t last_stream = nullptr;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;   // occ_detect_host copy streams
+    std::vector<cudaEvent_t> ev_pipe;
     int32_t last_batch = 0;
     int32_t last_launches = 0;
     // kernel timing (occ_profile)
@@ -422,6 +424,46 @@ int occ_set_path(occ_ctx *c, int32_t path) {
 
 int32_t occ_last_launches(const occ_ctx *c) { return c ? c->last_launches : -1; }
 
+}  // extern "C"
+
+namespace {
+// K0 + K1 for frames [c0, c0 + n) of a batch whose frames start at D / M (device).
+int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, cudaStream_t s, int &launches) {
+    const int64_t HW = (int64_t)c->H * c->W;
+    const float *Dc = D + (int64_t)c0 * HW;
+    uint8_t *Mc = M + (int64_t)c0 * c->V * HW;
+    {
+        ProfScope ps(c, OCC_KERNEL_STATS, s);
+        CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
+                           c->d_stats + c0, c->d_codes, c->code_bytes, s)); ++launches;
+        ps.end();
+    }
+    const bool tiled_only = c->path == OCC_PATH_TILED;
+    if (!tiled_only && !c->units.empty()) {
+        ProfScope pl(c, OCC_KERNEL_LINE, s);
+        CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
+        CK(launch_line(Dc, c->H, c->W, n, c->d_units, (int32_t)c->units.size(), c->d_groups,
+                       c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->d_codes,
+                       c->code_bytes, c->d_dbg, c->d_gq, c->d_gq_count, c->gq_cap, s));
+        CK(launch_hard(Dc, Mc, HW, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count, c->gq_cap,
+                       c->nsm, s));
+        launches += 2;
+        pl.end();
+    }
+    const TileDesc *tl = tiled_only ? c->d_all_tiles : c->d_tiles;
+    const int32_t nt = (int32_t)(tiled_only ? c->all_tiles.size() : c->tiles.size());
+    if (nt > 0) {
+        ProfScope pt(c, OCC_KERNEL_TILE, s);
+        CK(launch_tile(Dc, c->H, c->W, n, tl, nt, c->d_groups, c->d_views, c->V, c->d_fams,
+                       c->d_stats + c0, c->params, Mc, c->d_codes, c->code_bytes, s)); ++launches;
+        pt.end();
+    }
+    return OCC_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stream) {
     if (!c || !D || !M || batch < 1 || batch > c->max_batch) return OCC_ERR_INVALID_ARG;
     const int64_t HW = (int64_t)c->H * c->W;
@@ -452,36 +494,8 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
         // chunks of frames small enough that D and the candidate codes written
         // by K0 are still L2-resident when K1 reads them
         for (int32_t c0 = 0; c0 < batch; c0 += c->chunk) {
-            const int32_t n = std::min(c->chunk, batch - c0);
-            const float *Dc = D + (int64_t)c0 * HW;
-            {
-                ProfScope ps(c, OCC_KERNEL_STATS, s);
-                CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
-                                   c->d_stats + c0, c->d_codes, c->code_bytes, s)); ++launches;
-                ps.end();
-            }
-            const bool tiled_only = c->path == OCC_PATH_TILED;
-            if (!tiled_only && !c->units.empty()) {
-                ProfScope pl(c, OCC_KERNEL_LINE, s);
-                CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
-                CK(launch_line(Dc, c->H, c->W, n, c->d_units, (int32_t)c->units.size(), c->d_groups,
-                               c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params,
-                               M + (int64_t)c0 * c->V * HW, c->d_codes, c->code_bytes, c->d_dbg, c->d_gq,
-                               c->d_gq_count, c->gq_cap, s));
-                CK(launch_hard(Dc, M + (int64_t)c0 * c->V * HW, HW, c->V, c->d_views, c->params, c->d_gq,
-                               c->d_gq_count, c->gq_cap, c->nsm, s));
-                launches += 2;
-                pl.end();
-            }
-            const TileDesc *tl = tiled_only ? c->d_all_tiles : c->d_tiles;
-            const int32_t nt = (int32_t)(tiled_only ? c->all_tiles.size() : c->tiles.size());
-            if (nt > 0) {
-                ProfScope pt(c, OCC_KERNEL_TILE, s);
-                CK(launch_tile(Dc, c->H, c->W, n, tl, nt, c->d_groups, c->d_views, c->V, c->d_fams,
-                               c->d_stats + c0, c->params, M + (int64_t)c0 * c->V * HW, c->d_codes,
-                               c->code_bytes, s)); ++launches;
-                pt.end();
-            }
+            const int rc = detect_chunk(c, D, M, c0, std::min(c->chunk, batch - c0), s, launches);
+            if (rc != OCC_OK) return rc;
         }
     }
     c->last_stream = s;
@@ -490,6 +504,9 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
     return OCC_OK;
 }
 
+// Host-buffer entry point, pipelined per chunk of frames: the H2D copy of
+// chunk i + 1 and the D2H copy of chunk i - 1 run on their own streams while
+// chunk i is detected on the caller's stream (copy engines overlap the kernels).
 int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, void *stream) {
     if (!c || !Dh || !Mh || batch < 1 || batch > c->max_batch) return OCC_ERR_INVALID_ARG;
     CK(cudaSetDevice(c->device));
@@ -501,13 +518,52 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
             return OCC_ERR_OOM;
         }
     }
+    if (!c->s_h2d) {
+        CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    }
     cudaStream_t s = (cudaStream_t)stream;
-    CK(cudaMemcpyAsync(c->d_stage_D, Dh, (size_t)batch * HW * sizeof(float),
-                       cudaMemcpyHostToDevice, s));
-    int rc = occ_detect(c, c->d_stage_D, c->d_stage_M, batch, stream);
-    if (rc != OCC_OK) return rc;
-    CK(cudaMemcpyAsync(Mh, c->d_stage_M, (size_t)batch * c->V * HW, cudaMemcpyDeviceToHost, s));
+    const int32_t chunk = c->path == OCC_PATH_DIRECT ? batch : c->chunk;
+    const int32_t nchunks = (batch + chunk - 1) / chunk;
+    while ((int32_t)c->ev_pipe.size() < 2 * nchunks + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_pipe.push_back(e);
+    }
+    // the copies must not start before the caller's earlier work on s
+    CK(cudaEventRecord(c->ev_pipe[2 * nchunks], s));
+    CK(cudaStreamWaitEvent(c->s_h2d, c->ev_pipe[2 * nchunks], 0));
+    CK(cudaStreamWaitEvent(c->s_d2h, c->ev_pipe[2 * nchunks], 0));
+    int launches = 0;
+    {
+        ProfScope ps(c, OCC_KERNEL_INIT, s);
+        CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
+        ps.end();
+    }
+    for (int32_t i = 0; i < nchunks; ++i) {
+        const int32_t c0 = i * chunk, n = std::min(chunk, batch - c0);
+        CK(cudaMemcpyAsync(c->d_stage_D + (size_t)c0 * HW, Dh + (size_t)c0 * HW, (size_t)n * HW * sizeof(float),
+                           cudaMemcpyHostToDevice, c->s_h2d));
+        CK(cudaEventRecord(c->ev_pipe[2 * i], c->s_h2d));
+        CK(cudaStreamWaitEvent(s, c->ev_pipe[2 * i], 0));
+        if (c->path == OCC_PATH_DIRECT) {
+            int rc = occ_detect(c, c->d_stage_D, c->d_stage_M, batch, stream);
+            if (rc != OCC_OK) return rc;
+            launches += c->last_launches;
+        } else {
+            const int rc = detect_chunk(c, c->d_stage_D, c->d_stage_M, c0, n, s, launches);
+            if (rc != OCC_OK) return rc;
+        }
+        CK(cudaEventRecord(c->ev_pipe[2 * i + 1], s));
+        CK(cudaStreamWaitEvent(c->s_d2h, c->ev_pipe[2 * i + 1], 0));
+        CK(cudaMemcpyAsync(Mh + (size_t)c0 * c->V * HW, c->d_stage_M + (size_t)c0 * c->V * HW,
+                           (size_t)n * c->V * HW, cudaMemcpyDeviceToHost, c->s_d2h));
+    }
+    CK(cudaStreamSynchronize(c->s_d2h));
     CK(cudaStreamSynchronize(s));
+    c->last_stream = s;
+    c->last_batch = batch;
+    c->last_launches = launches;
     return OCC_OK;
 }
 
@@ -606,6 +662,9 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_dbg);
     cudaFree(c->d_gq);
     cudaFree(c->d_gq_count);
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    for (cudaEvent_t e : c->ev_pipe) cudaEventDestroy(e);
     cudaFree(c->d_stage_D);
     cudaFree(c->d_stage_M);
     for (int k = 0; k < OCC_KERNEL_KINDS; ++k)
