@@ -595,10 +595,7 @@ __device__ __noinline__ uint32_t resolve(const int DIR, const Ctx &c, uint32_t S
             const float vp = b.cb[r * SP];
             int32_t jm = dcov_of(DIR, b.Wc, b.cfall, b.tau0, r, h);
             jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
-            const int32_t SAa = b.tau0 + (int32_t)b.sab[r * 32 + lane];
-            const float vsa = probe_b(c, b, lane, SAa, c.elo, c.ehi);
-            const float g = fminf(fmaxf(__fmul_rn(vk.fs, __fsub_rn(vsa, vp)), 0.0f), 4096.0f);
-            const int32_t jw = max(DIR * (SAa - tau), __float2int_rn(g));
+            const int32_t jw = (int32_t)b.sab[r * 32 + lane];    // the sweep's partner guess
             float vq[3];
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
@@ -827,7 +824,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     // seeds the survivor's exact resolution.
     {
         const int32_t kS = max(min(kT + nbr, kEmax), kT);
-        float v1 = NaN, v2 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY;
+        float v1 = NaN, v2 = NaN, v3 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY, VW = NaN;
         int32_t SA = 0, jl = 0;
         int slot = 0;
         stage_chunk(c, stg, kS);
@@ -850,8 +847,8 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 for (int r = 31; r >= 0; --r) {
                     const float v0 = cb[r * SP];
                     const float A0 = __fmaf_rn(fs_, v0, -ip);
-                    if (A3 > SX) { SX = A3; SA = r + 3; }
-                    A3 = A2; A2 = A1; A1 = A0; v2 = v1; v1 = v0;
+                    if (A3 > SX) { SX = A3; SA = r + 3; VW = v3; }
+                    A3 = A2; A2 = A1; A1 = A0; v3 = v2; v2 = v1; v1 = v0;
                     ip = __fsub_rn(ip, 1.0f);
                 }
                 continue;
@@ -872,11 +869,15 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 Xg2 = push(Xg2, __fsub_rn(e2, a2n));
                 Xl2 = push(Xl2, __fsub_rn(e2, bhi1));
                 const float A0 = __fmaf_rn(fs_, v0, -ip);
-                if (A3 > SX) { SX = A3; SA = r + 3; }
+                if (A3 > SX) { SX = A3; SA = r + 3; VW = v3; }
                 const float fr = __fsub_rn(__fsub_rn(A0, vk.T), SX);
                 XFR = push(XFR, fr);
-                if (fr < 0.0f) sab[r * 32 + lane] = (int16_t)SA;     // witness of a survivor
-                A3 = A2; A2 = A1; A1 = A0; v2 = v1; v1 = v0;
+                // partner guess of a survivor: past the filter witness SA, A falls
+                // ~1 per step along a flat occluder, so the partner sits near
+                // jw = max(SA - i, s (v_SA - v_i))
+                if (fr < 0.0f)
+                    sab[r * 32 + lane] = (int16_t)max(SA - r, __float2int_rn(fminf(__fmul_rn(fs_, __fsub_rn(VW, v0)), 30000.0f)));
+                A3 = A2; A2 = A1; A1 = A0; v3 = v2; v2 = v1; v1 = v0;
                 ip = __fsub_rn(ip, 1.0f);
             }
             // tails: delta1 at 32k - 1, delta2 at 32k - 1 and 32k - 2 (chunk k - 1)
@@ -904,9 +905,27 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 const uint32_t C3 = cov_p_k(cp, tau0, h, 3);
                 uint32_t mP = ((T1 & ~Xs1) & cov_p_k(cp, tau0, h, 1)) | ((T2 & ~Xs2) & cov_p_k(cp, tau0, h, 2));
                 if (NFWD) mP |= (((TF & Xs1) << 1) | (tfm & s1m)) & cov_p_f(cp, tau0, h);
-                const uint32_t surv = XFR & C3 & ~mP;
+                uint32_t surv = XFR & C3 & ~mP;
                 uint32_t left = 0u;
                 Blk b;
+                if (__any_sync(FULL, surv != 0u)) {
+                    // witness probes of the block's survivors, branch-free, 8 loads in
+                    // flight; offsets clamped to dcov(i) >= pc(tau0 + h) + h - i (a hit
+                    // at any covered offset >= 3 is a far mark) and to the line
+                    const int32_t pc0 = (cand_bits32(cwP, tau0 + h, WB, lane) & 1u) ? tau0 + h : cp.pcl;
+                    const int32_t jcb = min(pc0 + h - tau0, c.ehi - 1 - tau0);
+                    uint32_t XH = 0u;
+#pragma unroll 8
+                    for (int r = 31; r >= 0; --r) {
+                        const int32_t jv = min((int32_t)sab[r * 32 + lane], jcb - r);
+                        const bool ok = jv >= 3 && tau0 + r >= c.elo;
+                        const float vq = ok ? __ldg(c.Dl + (int64_t)(tau0 + r + jv) * c.S) : NaN;
+                        const float x = __fsub_rn(fabsf(__fmaf_rn(fs_, __fsub_rn(vq, cb[r * SP]), -(float)jv)), vk.tlo);
+                        XH = push(XH, x);
+                    }
+                    mP |= XH & surv;
+                    surv &= ~XH;
+                }
                 if (__any_sync(FULL, surv != 0u)) {
                     b.tau0 = tau0; b.cb = cb;
                     b.Wc = cand_bits32(cwP, tau0 + h, WB, lane); b.cfall = cp.pcl;
@@ -937,7 +956,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     // with its witness SA parked for every survivor.
     {
         const int32_t kS = min(max(kB - nbr, kEmin), kB);
-        float A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY;
+        float v1 = NaN, v2 = NaN, v3 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY, VW = NaN;
         int32_t SA = 0, jl = 0;
         int slot = 0;
         stage_chunk(c, stg, kS);
@@ -956,9 +975,10 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             if (k < kB) {
 #pragma unroll 8
                 for (int r = 0; r < 32; ++r) {
-                    const float A0 = __fmaf_rn(fs_, cb[r * SP], ip);
-                    if (A3 > SX) { SX = A3; SA = r - 3; }
-                    A3 = A2; A2 = A1; A1 = A0;
+                    const float v0 = cb[r * SP];
+                    const float A0 = __fmaf_rn(fs_, v0, ip);
+                    if (A3 > SX) { SX = A3; SA = r - 3; VW = v3; }
+                    A3 = A2; A2 = A1; A1 = A0; v3 = v2; v2 = v1; v1 = v0;
                     ip = __fadd_rn(ip, 1.0f);
                 }
                 continue;
@@ -968,20 +988,38 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             uint32_t XFR = 0;
 #pragma unroll 8
             for (int r = 0; r < 32; ++r) {
-                const float A0 = __fmaf_rn(fs_, cb[r * SP], ip);
-                if (A3 > SX) { SX = A3; SA = r - 3; }
+                const float v0 = cb[r * SP];
+                const float A0 = __fmaf_rn(fs_, v0, ip);
+                if (A3 > SX) { SX = A3; SA = r - 3; VW = v3; }
                 const float fr = __fsub_rn(__fsub_rn(A0, vk.T), SX);
                 XFR = push(XFR, fr);
-                if (fr < 0.0f) sab[r * 32 + lane] = (int16_t)SA;     // witness of a survivor
-                A3 = A2; A2 = A1; A1 = A0;
+                if (fr < 0.0f)
+                    sab[r * 32 + lane] = (int16_t)max(r - SA, __float2int_rn(fminf(__fmul_rn(fs_, __fsub_rn(VW, v0)), 30000.0f)));
+                A3 = A2; A2 = A1; A1 = A0; v3 = v2; v2 = v1; v1 = v0;
                 ip = __fadd_rn(ip, 1.0f);
             }
             XFR = __brev(XFR);                     // bit r <-> tau0 + r
             const uint32_t C3 = cov_n_k(cn, tau0, h, 3);
             uint32_t mN = nn[(k - kB) * 32 + lane];
-            const uint32_t surv = XFR & C3 & ~mN;
+            uint32_t surv = XFR & C3 & ~mN;
             uint32_t left = 0u;
             Blk b;
+            if (__any_sync(FULL, surv != 0u)) {
+                // witness probes toward lower tau; dcov(i) >= i + h - nc(tau0 + 31 - h)
+                const int32_t nc0 = (cand_bits32(cwN, tau0 + 31 - h, WB, lane) & 1u) ? tau0 + 31 - h : cn.ncl;
+                const int32_t jcb = min(tau0 + h - nc0, tau0 - c.elo);
+                uint32_t XH = 0u;
+#pragma unroll 8
+                for (int r = 31; r >= 0; --r) {
+                    const int32_t jv = min((int32_t)sab[r * 32 + lane], jcb + r);
+                    const bool ok = jv >= 3 && tau0 + r < c.ehi;
+                    const float vq = ok ? __ldg(c.Dl + (int64_t)(tau0 + r - jv) * c.S) : NaN;
+                    const float x = __fsub_rn(fabsf(__fmaf_rn(fs_, __fsub_rn(vq, cb[r * SP]), -(float)jv)), vk.tlo);
+                    XH = push(XH, x);
+                }
+                mN |= XH & surv;
+                surv &= ~XH;
+            }
             if (__any_sync(FULL, surv != 0u)) {
                 b.tau0 = tau0; b.cb = cb;
                 b.Wc = cand_bits32(cwN, tau0 - h, WB, lane); b.cfall = cn.ncl;

@@ -14,7 +14,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libocc.so")
+LIB_PATH = os.environ.get("OCC_LIB") or os.path.join(_HERE, "libocc.so")   # OCC_LIB: A/B builds
 
 OCC_OK = 0
 OCC_ERR_INVALID_ARG = -1

@@ -16,7 +16,7 @@ L = lib()
 L.occ_debug_line_stats.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_ulonglong)]
 names = ["survP", "survN", "stage1_hits", "hard", "exh_found", "exh_steps", "global_probes",
          "blocks(x32)", "direct_units", "resolve_iters(x32)"]
-names2 = ["q_overflow", "q_tot", "q_n"]
+names2 = ["q_overflow", "q_tot", "q_n", "after_stage1"]
 nf = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 D = torch.from_numpy(scenes.make_batch(3, nf)).cuda()
 H, W = D.shape[1:]
@@ -33,7 +33,7 @@ for fam, views in [("rows", [(1, 0), (-1, 0)]), ("cols", [(0, 1), (0, -1)]),
     vals = list(out)[:10]
     print(fam, " ".join(f"{n}={v / pv:.5f}" if i not in (7, 9) else f"{n}={v / 32 / pv:.5f}"
                         for i, (n, v) in enumerate(zip(names, vals))))
-    print("   raw:", {n: int(v) for n, v in zip(names2, list(out)[10:13])}, "steps", int(out[5]))
+    print("   raw:", {n: int(v) for n, v in zip(names2, list(out)[10:14])}, "steps", int(out[5]))
     allv = np.array(list(out)[16:16 + 65536], dtype=np.uint64)
     phs = np.array(list(out)[16 + 65536:16 + 65536 + 4 * 32768], dtype=np.float64).reshape(-1, 4)
     print("   phase totals / CTA-cycles: resolve %.3f flush %.3f pass0 %.3f" % tuple(
