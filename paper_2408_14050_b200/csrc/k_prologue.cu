@@ -15,6 +15,7 @@ namespace occ {
 
 struct FamDirs {
     int32_t n;
+    int32_t small;      // all components in {-2..2}: fp32 products are exact
     int32_t bx[kMaxFamilies], by[kMaxFamilies];
 };
 
@@ -29,11 +30,20 @@ __device__ __forceinline__ CodeT pixel_code(float c, float right, float below, b
     uint32_t code = 0;
     if (e2 > e2_thresh) {
         for (int k = 0; k < fd.n; ++k) {
-            // Eq. 2 <=> b0 . (E_x, E_y) > 0, exact sign in binary64
-            const double dot = __dadd_rn(__dmul_rn((double)fd.bx[k], (double)ex),
-                                         __dmul_rn((double)fd.by[k], (double)ey));
-            code |= ((dot > 0.0) ? 1u : 0u) << (2 * k);
-            code |= ((dot < 0.0) ? 1u : 0u) << (2 * k + 1);
+            // Eq. 2 <=> b0 . (E_x, E_y) > 0, exact sign: with |b0| components
+            // in {0, 1, 2} both products are exact in fp32 and the sign of a
+            // correctly rounded sum is the sign of the exact sum; otherwise binary64
+            bool pos, neg;
+            if (fd.small) {
+                const float dot = __fadd_rn(__fmul_rn((float)fd.bx[k], ex), __fmul_rn((float)fd.by[k], ey));
+                pos = dot > 0.0f; neg = dot < 0.0f;
+            } else {
+                const double dot = __dadd_rn(__dmul_rn((double)fd.bx[k], (double)ex),
+                                             __dmul_rn((double)fd.by[k], (double)ey));
+                pos = dot > 0.0; neg = dot < 0.0;
+            }
+            code |= (pos ? 1u : 0u) << (2 * k);
+            code |= (neg ? 1u : 0u) << (2 * k + 1);
         }
     }
     return (CodeT)code;
@@ -122,7 +132,11 @@ cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames
                             FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s) {
     FamDirs fd{};
     fd.n = nfam;
-    for (int k = 0; k < nfam; ++k) { fd.bx[k] = fams_host[k].b0x; fd.by[k] = fams_host[k].b0y; }
+    fd.small = 1;
+    for (int k = 0; k < nfam; ++k) {
+        fd.bx[k] = fams_host[k].b0x; fd.by[k] = fams_host[k].b0y;
+        if (fd.bx[k] < -2 || fd.bx[k] > 2 || fd.by[k] < -2 || fd.by[k] > 2) fd.small = 0;
+    }
     const int64_t HW = (int64_t)H * W;
     const int64_t per_block = 256 * 4 * 4;
     int bx = (int)((HW + per_block - 1) / per_block);
