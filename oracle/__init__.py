@@ -63,6 +63,7 @@ def lib() -> ctypes.CDLL:
             "orc_detect": (ctypes.c_int, [f32p, i32, i32, i32p, i32, f32, f32, f32, i32, u8p, i32p]),
             "bf1_detect": (ctypes.c_int, [f32p, i32, i32, i32p, i32, f32, f32, f32, i32, u8p]),
             "bf2_zbuffer": (ctypes.c_int, [f32p, i32, i32, i32, i32, f32, u8p]),
+            "orc_fuse_median": (ctypes.c_int, [f32p, i32, ctypes.c_int64, f32p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -198,3 +199,17 @@ def count(g, v, w, idx, s=1, t_dist=2.0, t_disp=0.5, eps=1e-6) -> np.ndarray:
     lib().orc_count(_p(g, ctypes.c_int32), _p(v, ctypes.c_float), _p(w, ctypes.c_double),
                     _p(idx, ctypes.c_int32), len(g), s, t_dist, t_disp, eps, _p(O, ctypes.c_int32))
     return O
+
+
+def fuse_median(stack: np.ndarray) -> np.ndarray:
+    """Pixel-wise median of K fp32 estimates:
+    stack [K, ...] -> [...]; even K: fl32(fl32(a + b) * 0.5) of the middle pair;
+    NaN where any estimate is non-finite."""
+    st = np.ascontiguousarray(stack, dtype=np.float32)
+    K = st.shape[0]
+    n = int(np.prod(st.shape[1:])) if st.ndim > 1 else 1
+    out = np.empty(st.shape[1:], dtype=np.float32)
+    rc = lib().orc_fuse_median(_p(st, ctypes.c_float), K, n, _p(out, ctypes.c_float))
+    if rc != OK:
+        raise ValueError(f"orc_fuse_median rc={rc}")
+    return out

@@ -307,3 +307,36 @@ int orc_detect(const float *D, int32_t H, int32_t W, const int32_t *baselines, i
     free(Ex); free(Ey); free(E); free(cand);
     return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------------
+ * NEXT #3: pixel-wise median fusion.
+ * Per pixel: copy the K values, insertion-sort them (plain, O(K^2)), take the
+ * middle one (odd K) or the fp32 mean of the two middle ones (even K).
+ * ------------------------------------------------------------------------- */
+int orc_fuse_median(const float *stack, int32_t K, int64_t n, float *out)
+{
+    if (K < 1 || K > 1024) return ORC_ERR_INVALID_ARG;
+    float *v = (float *)malloc(sizeof(float) * (size_t)K);
+    if (!v) return ORC_ERR_INVALID_ARG;
+    for (int64_t p = 0; p < n; ++p) {
+        int bad = 0;
+        for (int32_t k = 0; k < K; ++k) {
+            const float x = stack[(int64_t)k * n + p];
+            if (!isfinite(x)) bad = 1;
+            /* insertion into the sorted prefix v[0..k-1] */
+            int32_t j = k;
+            while (j > 0 && v[j - 1] > x) { v[j] = v[j - 1]; --j; }
+            v[j] = x;
+        }
+        if (bad) { out[p] = NAN; continue; }
+        if (K & 1) {
+            out[p] = v[K / 2];
+        } else {
+            const float a = v[K / 2 - 1], b = v[K / 2];
+            const float sum = a + b;          /* one fp32 rounding */
+            out[p] = sum * 0.5f;              /* exact halving (normal range) */
+        }
+    }
+    free(v);
+    return ORC_OK;
+}

@@ -95,6 +95,17 @@ int bf1_detect(const float *D, int32_t H, int32_t W, const int32_t *baselines, i
 int bf2_zbuffer(const float *D, int32_t H, int32_t W, int32_t bx, int32_t by,
                 float t_disp, uint8_t *mask);
 
+/* Pixel-wise median fusion of K disparity estimates.
+ * PAPER.md:238 (§4.2, "fused to a single disparity map by pixel-wise median
+ * filtering"); SPEC.md:51-58 (fuse_median: for even counts the arithmetic
+ * mean of the two middle values).  stack is K planes of n values
+ * ([K][n], plane k = estimate k); out[p] = median of stack[0..K-1][p].
+ * fp32 reading (Q22): odd K -> the middle value; even K ->
+ * fl32(fl32(a + b) * 0.5) of the two middle values a <= b; any non-finite
+ * input at p -> out[p] = NaN (the detector then rejects the frame, Q18).
+ * Returns ORC_OK, or ORC_ERR_INVALID_ARG for K < 1. */
+int orc_fuse_median(const float *stack, int32_t K, int64_t n, float *out);
+
 #ifdef __cplusplus
 }
 #endif
