@@ -123,6 +123,19 @@ enum { OCC_KERNEL_INIT = 0, OCC_KERNEL_STATS = 1, OCC_KERNEL_TILE = 2, OCC_KERNE
 int occ_profile(occ_ctx *ctx, int32_t enable);
 int occ_profile_read(occ_ctx *ctx, int32_t kind, double *total_ms, int32_t *launches);
 
+/* Pixel-wise median fusion of K disparity estimates into the fused map the
+ * detector consumes (§4.2: "fused to a single disparity map by
+ * pixel-wise median filtering").  No context needed.
+ *   stack: device, K planes of n fp32 values back to back ([K][n]; plane k =
+ *          estimate k, n = frames * H * W for a batch), caller-owned;
+ *   out:   device, n fp32 values, caller-owned, must not overlap stack.
+ * out[p] = the middle value of {stack[k][p]} for odd K; for even K the fp32
+ * mean fl(fl(a + b) * 0.5) of the two middle values a <= b; NaN where any
+ * estimate is non-finite (occ_detect then reports OCC_ERR_NONFINITE for the
+ * frame).  Stream ordered; returns OCC_OK, OCC_ERR_INVALID_ARG (null
+ * pointers, K < 1 or K > 64, n < 1, overlap) or OCC_ERR_CUDA. */
+int occ_fuse_median(const float *stack, int32_t K, int64_t n, float *out, void *cuda_stream);
+
 /* Releases the context and its device scratch (synchronises first). */
 int occ_destroy(occ_ctx *ctx);
 

@@ -647,6 +647,20 @@ int occ_debug_line_stats(occ_ctx *c, int32_t enable, unsigned long long *out) {
     return OCC_OK;
 }
 
+int occ_fuse_median(const float *stack, int32_t K, int64_t n, float *out, void *stream) {
+    if (!stack || !out || K < 1 || K > kFuseMaxK || n < 1) return OCC_ERR_INVALID_ARG;
+    {
+        const char *s0 = (const char *)stack, *s1 = s0 + (size_t)K * (size_t)n * sizeof(float);
+        const char *o0 = (const char *)out, *o1 = o0 + (size_t)n * sizeof(float);
+        if (o0 < s1 && s0 < o1) return OCC_ERR_INVALID_ARG;
+    }
+    int dev = 0, nsm = 148;
+    CK(cudaGetDevice(&dev));
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+    CK(launch_fuse_median(stack, K, n, out, nsm, (cudaStream_t)stream));
+    return OCC_OK;
+}
+
 int occ_destroy(occ_ctx *c) {
     if (!c) return OCC_ERR_INVALID_ARG;
     cudaSetDevice(c->device);

@@ -27,7 +27,7 @@ PATHS = {"auto": 0, "tiled": 1, "direct": 2}
 # every function include/occ.h declares (checked against the header by tests)
 EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", "occ_status",
            "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
-           "occ_version", "occ_profile", "occ_profile_read"]
+           "occ_version", "occ_profile", "occ_profile_read", "occ_fuse_median"]
 KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5}
 
 
@@ -86,6 +86,8 @@ def lib() -> ctypes.CDLL:
         L.occ_profile_read.restype = ctypes.c_int
         L.occ_version.argtypes = []
         L.occ_version.restype = i32
+        L.occ_fuse_median.argtypes = [vp, i32, ctypes.c_int64, vp, vp]
+        L.occ_fuse_median.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -235,3 +237,22 @@ class Detector:
             self.close()
         except Exception:
             pass
+
+
+def fuse_median(stack, out=None, stream=None):
+    """Pixel-wise median of K disparity estimates (occ_fuse_median).
+
+    stack: contiguous fp32 CUDA tensor [K, ...]; returns fp32 [...] (or fills
+    ``out``).  Marshalling only: the median runs in libocc's k_fuse kernel."""
+    import torch
+    if not (stack.is_cuda and stack.dtype == torch.float32 and stack.is_contiguous()):
+        raise ValueError("stack must be a contiguous float32 CUDA tensor [K, ...]")
+    K = int(stack.shape[0])
+    n = stack.numel() // max(1, K)
+    if out is None:
+        out = torch.empty(stack.shape[1:], dtype=torch.float32, device=stack.device)
+    s = stream or torch.cuda.current_stream(stack.device)
+    rc = lib().occ_fuse_median(stack.data_ptr(), K, n, out.data_ptr(), s.cuda_stream)
+    if rc != OCC_OK:
+        raise OccError(rc, "occ_fuse_median")
+    return out
