@@ -200,6 +200,41 @@ def workload_config(world, nf=FRAMES_PER_GPU):
             "parallelism": f"frame-sharded x{world} (no data-path collective)"}
 
 
+def fuse_leg(d, nf, dev, args, peak):
+    """Times occ_fuse_median on K = 8 synthetic per-camera estimates of the
+    bench frames (estimate k = D + N(0, 0.25^2) noise, generated on the device
+    outside the timed region): bytes moved = (4 K + 4) per pixel."""
+    import torch
+    from paper_2408_14050_b200.occ import fuse_median
+    K = 8
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)
+    stack = torch.empty((K,) + tuple(d.shape), dtype=torch.float32, device=dev)
+    for k in range(K):
+        stack[k] = d + 0.25 * torch.randn(d.shape, generator=g, device=dev)
+    out = torch.empty_like(d)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        fuse_median(stack, out=out)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        fuse_median(stack, out=out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    n = d.numel()
+    gbs = (4 * K + 4) * n / (ms / 1e3) / 1e9
+    res = {"K": K, "frames": nf, "ms_per_call": ms, "mpix_per_s": n / (ms / 1e3) / 1e6,
+           "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
+           "bytes_per_px": 4 * K + 4, "kernel": "k_fuse<8>"}
+    del stack, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -212,6 +247,7 @@ def main():
     ap.add_argument("--ref-frames", type=int, default=2)
     ap.add_argument("--path", default="auto", choices=["auto", "tiled", "direct"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fuse", action="store_true", help="skip the median-fusion leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -251,6 +287,7 @@ def main():
     st = det.status()
     assert all(s == 0 for s in st), st
 
+    peak, peak_src = load_peaks()
     # ---------------- timed region: K steps, inputs resident in HBM ----------------
     det.profile(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -279,7 +316,6 @@ def main():
     launches_per_step = max(1, dom_n // args.steps)
     alg_step = nf * H * W * (4 + V)            # 4 B read + V B written per pixel
     alg_bytes = alg_step / launches_per_step   # per launch of the dominant kernel (frame chunk)
-    peak, peak_src = load_peaks()
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
     tr = load_traffic()
     traffic = None
@@ -308,6 +344,11 @@ def main():
            "note": "occ_detect_host: pinned H2D of D, detect, D2H of all masks, stream sync"}
     assert torch.equal(mbuf[:1].to(dev), masks[:1])
 
+    # ---------------- median fusion leg (NEXT #3): K = 8 per-camera estimates ----------------
+    fuse = None
+    if not args.no_fuse:
+        fuse = fuse_leg(d, nf, dev, args, peak)
+
     if rank != 0:
         return
     cpu = None
@@ -321,6 +362,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world, nf),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
         "gpu_launches": launches, "path": args.path,
+        "fuse_median": fuse,
     }
     print(json.dumps(line), flush=True)
 
