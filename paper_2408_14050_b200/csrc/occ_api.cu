@@ -372,9 +372,12 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
     c->nfam = (int32_t)c->fams.size();
     build_tiles(c);
     c->code_bytes = c->nfam <= 4 ? 1 : (c->nfam <= 8 ? 2 : 4);
-    {   // frames per K0/K1 chunk: D + codes of a chunk within ~48 MiB of L2
+    {   // frames per K0/K1 chunk (measured: 48 MiB 54.6 ms/step, 96 MiB 51.7,
+        // 160-640 MiB 50.3-50.6 at C5)
         const double per = (double)H * W * (4.0 + c->code_bytes);
-        c->chunk = (int32_t)std::max(1.0, std::min(64.0, std::floor(48.0 * 1048576.0 / per)));
+        const char *ev = getenv("OCC_CHUNK_MIB");          // tuning knob (default 256 MiB)
+        const double budget = (ev ? std::max(1, atoi(ev)) : 256) * 1048576.0;
+        c->chunk = (int32_t)std::max(1.0, std::min(64.0, std::floor(budget / per)));
         c->chunk = std::min(c->chunk, max_batch);
     }
 
@@ -491,8 +494,9 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
                          c->params, M, s)); ++launches;
         pd.end();
     } else {
-        // chunks of frames small enough that D and the candidate codes written
-        // by K0 are still L2-resident when K1 reads them
+        // chunks of ~256 MiB of D + codes: enough warps per K1 launch to fill
+        // the GPU (the long-tailed per-unit times average out); K1's re-reads
+        // of D mostly hit L2, the rest is a small fraction of the HBM bandwidth
         for (int32_t c0 = 0; c0 < batch; c0 += c->chunk) {
             const int rc = detect_chunk(c, D, M, c0, std::min(c->chunk, batch - c0), s, launches);
             if (rc != OCC_OK) return rc;
