@@ -104,9 +104,10 @@ def test_line_vs_tiled_paths(torch_cuda):
     assert_same(a[0], oracle.detect(D[0], views), "C3 crop")
 
 
-def test_host_pipeline_multiple_chunks(torch_cuda):
-    # 1080p frames: 4 frames per chunk, so 7 frames = two chunks (4 + 3)
+def test_host_pipeline_multiple_chunks(torch_cuda, monkeypatch):
+    # 48 MiB chunks of 1080p frames hold 4 frames, so 7 frames = two chunks (4 + 3)
     from paper_2408_14050_b200.occ import Detector
+    monkeypatch.setenv("OCC_CHUNK_MIB", "48")
     D = scenes.make_batch(5, 7)
     views = scenes.config_views(5)
     det = Detector(1080, 1920, views, max_batch=7)
