@@ -918,7 +918,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
 #pragma unroll 8
                     for (int r = 31; r >= 0; --r) {
                         const int32_t jv = min((int32_t)sab[r * 32 + lane], jcb - r);
-                        const bool ok = jv >= 3 && tau0 + r >= c.elo;
+                        const bool ok = jv >= 3 && tau0 + r >= c.elo && ((surv >> r) & 1u);
                         const float vq = ok ? __ldg(c.Dl + (int64_t)(tau0 + r + jv) * c.S) : NaN;
                         const float x = __fsub_rn(fabsf(__fmaf_rn(fs_, __fsub_rn(vq, cb[r * SP]), -(float)jv)), vk.tlo);
                         XH = push(XH, x);
@@ -1012,7 +1012,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
 #pragma unroll 8
                 for (int r = 31; r >= 0; --r) {
                     const int32_t jv = min((int32_t)sab[r * 32 + lane], jcb + r);
-                    const bool ok = jv >= 3 && tau0 + r < c.ehi;
+                    const bool ok = jv >= 3 && tau0 + r < c.ehi && ((surv >> r) & 1u);
                     const float vq = ok ? __ldg(c.Dl + (int64_t)(tau0 + r - jv) * c.S) : NaN;
                     const float x = __fsub_rn(fabsf(__fmaf_rn(fs_, __fsub_rn(vq, cb[r * SP]), -(float)jv)), vk.tlo);
                     XH = push(XH, x);
