@@ -527,7 +527,10 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
         CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
     }
     cudaStream_t s = (cudaStream_t)stream;
-    const int32_t chunk = c->path == OCC_PATH_DIRECT ? batch : c->chunk;
+    // pipeline granularity: ~64 MiB of D per copy (finer than the device-side
+    // chunk, so the first H2D and the last D2H expose little of the step)
+    const int32_t pipe = (int32_t)std::max<int64_t>(1, ((int64_t)64 << 20) / (int64_t)(HW * sizeof(float)));
+    const int32_t chunk = c->path == OCC_PATH_DIRECT ? batch : std::min(c->chunk, pipe);
     const int32_t nchunks = (batch + chunk - 1) / chunk;
     while ((int32_t)c->ev_pipe.size() < 2 * nchunks + 1) {
         cudaEvent_t e;
