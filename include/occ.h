@@ -107,6 +107,20 @@ int occ_status(occ_ctx *ctx, int32_t *frame_status);
  * h_per_view has n_views entries.  Any output pointer may be NULL. */
 int occ_frame_info(occ_ctx *ctx, int32_t frame, float *dmin, float *dmax, int32_t *h_per_view);
 
+/* Mask output format (occ_set_mask_format), NEXT #4 of SURVEY §8(f):
+ *   OCC_MASK_U8   (default) uint8 [batch][n_views][H][W], each byte 0 or 1;
+ *   OCC_MASK_BITS bit-packed uint32 words [batch][n_views][H][ceil(W/32)]:
+ *                 bit (x & 31) of word (y, x >> 5) is the mask of pixel
+ *                 (x, y); padding bits are 0.  8x fewer bytes to move.
+ * The buffers passed to occ_detect / occ_detect_host must hold
+ * occ_mask_bytes(ctx, batch) bytes.  Returns OCC_OK or OCC_ERR_INVALID_ARG. */
+enum { OCC_MASK_U8 = 0, OCC_MASK_BITS = 1 };
+int occ_set_mask_format(occ_ctx *ctx, int32_t format);
+
+/* Bytes of the mask buffer for `batch` frames in the current format (-1 on
+ * a null context or negative batch). */
+int64_t occ_mask_bytes(const occ_ctx *ctx, int32_t batch);
+
 /* Selects the kernel path for subsequent calls (OCC_PATH_*). */
 int occ_set_path(occ_ctx *ctx, int32_t path);
 

@@ -225,6 +225,7 @@ struct LineArgs {
     uint32_t *gq_count;
     int32_t gq_cap;
     int32_t nwork;             // units x frames
+    MaskFmt mf;
 };
 
 // Per-warp context
@@ -240,6 +241,7 @@ struct Ctx {
     int64_t B;                 // lane's line: pixel index = B + tau * S
     int32_t S;
     int32_t f;                 // frame
+    MaskFmt mf;
     HardEntry *gq;
     uint32_t *gq_count;
     int32_t gq_cap;
@@ -493,7 +495,11 @@ __device__ __noinline__ void flush_queue(const int DIR, const Ctx &c, const int3
                 for (int u = 0; u < 4; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
             }
             dbg_add(c.dbg, 4, hit ? 1u : 0u);
-            if (hit) Mv[line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S] = 1;
+            if (hit) {
+                int32_t x, y;
+                lg_px(c.kind, c.l0, src, tau, x, y);
+                mask_put(Mv, c.mf, c.W, x, y, true);
+            }
         }
     }
     __syncwarp();
@@ -651,6 +657,38 @@ __device__ __forceinline__ uint32_t cand_bits32(const uint32_t *cw, int32_t x, i
 __device__ __noinline__ void store_block(const Ctx &c, uint8_t *Mv, uint32_t word, int32_t k) {
     const int lane = c.lane;
     const int32_t H = c.H, W = c.W;
+    if (c.mf.packed) {
+        // bit-packed planes (pre-zeroed): rows and columns own whole words;
+        // a diagonal row run straddles two words shared with the neighbouring
+        // line block (atomicOr)
+        uint32_t *P = reinterpret_cast<uint32_t *>(Mv);
+        const int32_t Wb = c.mf.Wb;
+        if (c.kind == 0) {
+            const int32_t y = c.l0 + lane;
+            if (y >= 0 && y < H && 32 * k >= 0 && 32 * k < W) P[(int64_t)y * Wb + k] = word;
+        } else if (c.kind == 1) {
+            const uint32_t t = transpose32(word, lane);          // lane r: row 32k + r, bit l = column l0 + l
+            const int32_t y = 32 * k + lane;
+            if (y >= 0 && y < H && c.l0 >= 0 && c.l0 < W) P[(int64_t)y * Wb + (c.l0 >> 5)] = t;
+        } else {
+            // tau = 32k + r is one image row; its 32 lanes form the run x0 .. x0 + 31
+            uint32_t mine = 0u;
+            for (int r = 0; r < 32; ++r) {
+                const uint32_t b = __ballot_sync(0xffffffffu, (word >> r) & 1u);
+                if (r == lane) mine = b;
+            }
+            const int32_t tau = 32 * k + lane;
+            const int32_t y = c.kind == 2 ? c.l0 + tau : c.l0 + 31 - tau;
+            const uint32_t run = c.kind == 2 ? __brev(mine) : mine;      // bit m <-> x = tau - 31 + m
+            if (run && y >= 0 && y < H) {
+                const int32_t x0 = tau - 31, w0 = x0 >> 5, sh = x0 & 31;
+                const uint32_t lo = run << sh, hi = sh ? (run >> (32 - sh)) : 0u;
+                if (lo && w0 >= 0 && w0 < Wb) atomicOr(P + (int64_t)y * Wb + w0, lo);
+                if (hi && w0 + 1 >= 0 && w0 + 1 < Wb) atomicOr(P + (int64_t)y * Wb + w0 + 1, hi);
+            }
+        }
+        return;
+    }
     if (c.kind == 0) {
         const int32_t y = c.l0 + lane, x0 = 32 * k;
         if (y < 0 || y >= H) return;
@@ -708,12 +746,12 @@ __device__ __noinline__ void unit_direct(const Ctx &c, const LineArgs &a, const 
     for (int g = 0; g < gd.nv; ++g) {
         const ViewDesc &vd = a.views[gd.view[g]];
         const int32_t h = view_h(R, vd.s, a.p.max_scan);
-        uint8_t *Mv = a.masks + ((int64_t)f * a.nviews + gd.view[g]) * HW;
+        uint8_t *Mv = a.masks + ((int64_t)f * a.nviews + gd.view[g]) * a.mf.vbytes;
         for (int32_t tau = max(T0, c.elo); tau < min(T1, c.ehi); ++tau) {
             int32_t x, y;
             lg_px(c.kind, c.l0, c.lane, tau, x, y);
             const bool m = !zero && direct_pixel<false>(c.Df, c.H, c.W, vd, fd, a.p, h, x, y);
-            Mv[(int64_t)y * c.W + x] = (uint8_t)m;
+            mask_put(Mv, a.mf, c.W, x, y, m);
         }
     }
 }
@@ -729,6 +767,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     Ctx c;
     c.dbg = a.dbg;
     c.f = f;
+    c.mf = a.mf;
     c.gq = a.gq; c.gq_count = a.gq_count; c.gq_cap = a.gq_cap;
     {
         const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -815,8 +854,8 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     __syncwarp();
 
     const float NaN = __int_as_float(0x7fc00000);
-    uint8_t *MP = vP >= 0 ? a.masks + ((int64_t)f * a.nviews + vP) * HW : nullptr;
-    uint8_t *MN = vN >= 0 ? a.masks + ((int64_t)f * a.nviews + vN) * HW : nullptr;
+    uint8_t *MP = vP >= 0 ? a.masks + ((int64_t)f * a.nviews + vP) * a.mf.vbytes : nullptr;
+    uint8_t *MN = vN >= 0 ? a.masks + ((int64_t)f * a.nviews + vN) * a.mf.vbytes : nullptr;
 
     // ---------------------------------------------------- pass A (descending)
     // Far filter of view +b: SX = max A(q) over q >= i + 3, A = s v - pos, with
@@ -1072,7 +1111,8 @@ __global__ void __launch_bounds__(128) k_line(LineArgs a) {
 // (survivor p of view v in frame f), offsets 3..dcov(p) along its line, 16
 // loads in flight; a confirmed Eq. 5 pair sets the mask byte.
 __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
-                                              int64_t HW, int32_t nviews, const ViewDesc *__restrict__ views,
+                                              MaskFmt mf, int32_t W, int64_t HW, int32_t nviews,
+                                              const ViewDesc *__restrict__ views,
                                               Params p, const HardEntry *__restrict__ gq,
                                               const uint32_t *__restrict__ gq_count, int32_t gq_cap) {
     const uint32_t n = min(*gq_count, (uint32_t)gq_cap);
@@ -1095,25 +1135,26 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
 #pragma unroll 4
             for (int u = 0; u < 16; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
         }
-        if (hit) masks[((int64_t)f * nviews + v) * HW + he.pix] = 1;
+        if (hit) mask_put(masks + ((int64_t)f * nviews + v) * mf.vbytes, mf, W, he.pix % W, he.pix / W, true);
     }
 }
 
-cudaError_t launch_hard(const float *D, uint8_t *masks, int64_t HW, int32_t nviews, const ViewDesc *views,
+cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW,
+                        int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
                         int32_t nsm, cudaStream_t s) {
-    k_hard<<<nsm * 8, 256, 0, s>>>(D, masks, HW, nviews, views, p, gq, gq_count, gq_cap);
+    k_hard<<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, nviews, views, p, gq, gq_count, gq_cap);
     return cudaGetLastError();
 }
 
 cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
                         const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
-                        const void *codes, int32_t code_bytes, unsigned long long *dbg, HardEntry *gq,
-                        uint32_t *gq_count, int32_t gq_cap, cudaStream_t s) {
+                        const MaskFmt &mf, const void *codes, int32_t code_bytes, unsigned long long *dbg,
+                        HardEntry *gq, uint32_t *gq_count, int32_t gq_cap, cudaStream_t s) {
     if (nunits <= 0) return cudaSuccess;
     LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch, gq, gq_count, gq_cap,
-               nunits * batch};
+               nunits * batch, mf};
     static int nw = 0;
     if (!nw) {
         const char *ev = getenv("OCC_LINE_WARPS");

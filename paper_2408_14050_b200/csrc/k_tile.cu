@@ -330,6 +330,7 @@ struct TileArgs {
     Params p;
     uint8_t *masks;
     const void *codes;
+    MaskFmt mf;
 };
 
 template <class G, int CB, int VP>
@@ -568,7 +569,20 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
 #pragma unroll 1
     for (int g = 0; g < gd.nv; ++g) {
         const uint32_t *ow = outw + g * NOB * 32;
-        uint8_t *Mv = a.masks + ((int64_t)f * a.nviews + gd.view[g]) * HW;
+        uint8_t *Mv = a.masks + ((int64_t)f * a.nviews + gd.view[g]) * a.mf.vbytes;
+        if (a.mf.packed) {
+            // bit-packed masks (pre-zeroed): set the marked pixels of the tile
+            for (int k = tid; k < TPe * 32; k += NT) {
+                const int32_t kk = k >> 5, l = k & 31;
+                if (!bit_at(ow, kk, l)) continue;
+                const int32_t pos = P0 + kk, ln = l0 + l;
+                int32_t x, y;
+                if (xm) { x = pos; y = ln + geo.fl(pos); }
+                else { y = pos; x = ln + geo.fl(pos); }
+                if (x >= 0 && x < W && y >= 0 && y < H) mask_put(Mv, a.mf, W, x, y, true);
+            }
+            continue;
+        }
         const bool al4 = ((W & 3) == 0) && ((l0 & 3) == 0) && ((P0 & 3) == 0) && geo.num() == 0;
         if (!xm && al4) {
             // columns: output row y = P0 + k holds lanes l0..l0+31 -> 4 lanes per thread
@@ -669,9 +683,9 @@ __global__ void __launch_bounds__(NT, 3) k_tile(TileArgs a) {
 cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
                         const TileDesc *tiles, int32_t ntiles, const GroupDesc *groups,
                         const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
-                        const FrameStats *st, const Params &p, uint8_t *masks, const void *codes,
-                        int32_t code_bytes, cudaStream_t s) {
-    TileArgs a{D, H, W, tiles, groups, views, nviews, fams, st, p, masks, codes};
+                        const FrameStats *st, const Params &p, uint8_t *masks, const MaskFmt &mf,
+                        const void *codes, int32_t code_bytes, cudaStream_t s) {
+    TileArgs a{D, H, W, tiles, groups, views, nviews, fams, st, p, masks, codes, mf};
     dim3 grid((unsigned)ntiles, (unsigned)batch);
     cudaError_t e;
     if (code_bytes == 1) {

@@ -19,6 +19,7 @@ using namespace occ;
 struct occ_ctx {
     int32_t H = 0, W = 0, V = 0, nfam = 0, max_batch = 0, device = 0;
     int32_t path = OCC_PATH_AUTO;
+    MaskFmt mf{0, 0, 0};                 // occ_set_mask_format
     Params params{};
     std::vector<ViewDesc> views;
     std::vector<FamilyDesc> fams;
@@ -326,6 +327,7 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
     occ_ctx *c = new (std::nothrow) occ_ctx();
     if (!c) return OCC_ERR_OOM;
     c->H = H; c->W = W; c->V = n_views; c->max_batch = max_batch;
+    c->mf.packed = 0; c->mf.Wb = (W + 31) / 32; c->mf.vbytes = (int64_t)H * W;
     c->params.t_edge = p.t_edge;
     c->params.t_dist = p.t_dist;
     c->params.t_disp = p.t_disp;
@@ -419,6 +421,19 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
     return OCC_OK;
 }
 
+int occ_set_mask_format(occ_ctx *c, int32_t format) {
+    if (!c || (format != OCC_MASK_U8 && format != OCC_MASK_BITS)) return OCC_ERR_INVALID_ARG;
+    c->mf.packed = format == OCC_MASK_BITS;
+    c->mf.Wb = (c->W + 31) / 32;
+    c->mf.vbytes = c->mf.packed ? (int64_t)c->H * c->mf.Wb * 4 : (int64_t)c->H * c->W;
+    return OCC_OK;
+}
+
+int64_t occ_mask_bytes(const occ_ctx *c, int32_t batch) {
+    if (!c || batch < 0) return -1;
+    return (int64_t)batch * c->V * c->mf.vbytes;
+}
+
 int occ_set_path(occ_ctx *c, int32_t path) {
     if (!c || path < OCC_PATH_AUTO || path > OCC_PATH_DIRECT) return OCC_ERR_INVALID_ARG;
     c->path = path;
@@ -434,7 +449,7 @@ namespace {
 int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, cudaStream_t s, int &launches) {
     const int64_t HW = (int64_t)c->H * c->W;
     const float *Dc = D + (int64_t)c0 * HW;
-    uint8_t *Mc = M + (int64_t)c0 * c->V * HW;
+    uint8_t *Mc = M + (int64_t)c0 * c->V * c->mf.vbytes;
     {
         ProfScope ps(c, OCC_KERNEL_STATS, s);
         CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
@@ -446,10 +461,10 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
         CK(launch_line(Dc, c->H, c->W, n, c->d_units, (int32_t)c->units.size(), c->d_groups,
-                       c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->d_codes,
+                       c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_codes,
                        c->code_bytes, c->d_dbg, c->d_gq, c->d_gq_count, c->gq_cap, s));
-        CK(launch_hard(Dc, Mc, HW, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count, c->gq_cap,
-                       c->nsm, s));
+        CK(launch_hard(Dc, Mc, c->mf, c->W, HW, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
+                       c->gq_cap, c->nsm, s));
         launches += 2;
         pl.end();
     }
@@ -458,7 +473,7 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
     if (nt > 0) {
         ProfScope pt(c, OCC_KERNEL_TILE, s);
         CK(launch_tile(Dc, c->H, c->W, n, tl, nt, c->d_groups, c->d_views, c->V, c->d_fams,
-                       c->d_stats + c0, c->params, Mc, c->d_codes, c->code_bytes, s)); ++launches;
+                       c->d_stats + c0, c->params, Mc, c->mf, c->d_codes, c->code_bytes, s)); ++launches;
         pt.end();
     }
     return OCC_OK;
@@ -472,12 +487,14 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
     const int64_t HW = (int64_t)c->H * c->W;
     {   // masks must not alias the input
         const char *d0 = (const char *)D, *d1 = d0 + (size_t)batch * HW * sizeof(float);
-        const char *m0 = (const char *)M, *m1 = m0 + (size_t)batch * c->V * HW;
+        const char *m0 = (const char *)M, *m1 = m0 + (size_t)batch * c->V * c->mf.vbytes;
         if (m0 < d1 && d0 < m1) return OCC_ERR_INVALID_ARG;
     }
     CK(cudaSetDevice(c->device));
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
+    if (c->mf.packed)       // packed planes: kernels set bits only
+        CK(cudaMemsetAsync(M, 0, (size_t)batch * c->V * c->mf.vbytes, s));
     {
         ProfScope ps(c, OCC_KERNEL_INIT, s);
         CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
@@ -491,7 +508,7 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
         }
         ProfScope pd(c, OCC_KERNEL_DIRECT, s);
         CK(launch_direct(D, c->H, c->W, batch, c->d_views, c->V, c->d_fams, c->d_stats,
-                         c->params, M, s)); ++launches;
+                         c->params, M, c->mf, s)); ++launches;
         pd.end();
     } else {
         // chunks of ~256 MiB of D + codes: enough warps per K1 launch to fill
@@ -547,6 +564,8 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
         CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
         ps.end();
     }
+    if (c->mf.packed && c->path != OCC_PATH_DIRECT)
+        CK(cudaMemsetAsync(c->d_stage_M, 0, (size_t)batch * c->V * c->mf.vbytes, s));
     for (int32_t i = 0; i < nchunks; ++i) {
         const int32_t c0 = i * chunk, n = std::min(chunk, batch - c0);
         CK(cudaMemcpyAsync(c->d_stage_D + (size_t)c0 * HW, Dh + (size_t)c0 * HW, (size_t)n * HW * sizeof(float),
@@ -563,8 +582,8 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
         }
         CK(cudaEventRecord(c->ev_pipe[2 * i + 1], s));
         CK(cudaStreamWaitEvent(c->s_d2h, c->ev_pipe[2 * i + 1], 0));
-        CK(cudaMemcpyAsync(Mh + (size_t)c0 * c->V * HW, c->d_stage_M + (size_t)c0 * c->V * HW,
-                           (size_t)n * c->V * HW, cudaMemcpyDeviceToHost, c->s_d2h));
+        CK(cudaMemcpyAsync(Mh + (size_t)c0 * c->V * c->mf.vbytes, c->d_stage_M + (size_t)c0 * c->V * c->mf.vbytes,
+                           (size_t)n * c->V * c->mf.vbytes, cudaMemcpyDeviceToHost, c->s_d2h));
     }
     CK(cudaStreamSynchronize(c->s_d2h));
     CK(cudaStreamSynchronize(s));

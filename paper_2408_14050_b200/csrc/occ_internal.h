@@ -58,6 +58,25 @@ struct Params {
     float e2_thresh;    // largest fp32 x with sqrt_rn(x) <= t_edge: E > t_e <=> e2 > e2_thresh
 };
 
+// Mask output format (occ_set_mask_format): uint8 [H][W] per (frame, view),
+// or bit-packed: [H][Wb] 32-bit words, Wb = ceil(W / 32), bit x & 31 of word
+// (y, x >> 5) = mask of pixel (x, y), padding bits 0.  vbytes = bytes per
+// (frame, view) plane.  Packed planes are zeroed before the kernels run and
+// only set bits are written (atomicOr where two writers share a word).
+struct MaskFmt {
+    int32_t packed, Wb;
+    int64_t vbytes;
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ void mask_put(uint8_t *Mv, const MaskFmt &m, int32_t W, int32_t x, int32_t y, bool v) {
+    if (m.packed) {
+        if (v) atomicOr(reinterpret_cast<unsigned int *>(Mv) + (int64_t)y * m.Wb + (x >> 5), 1u << (x & 31));
+    } else {
+        Mv[(int64_t)y * W + x] = (uint8_t)v;
+    }
+}
+#endif
+
 // Per-frame statistics written by k_stats (S1) -- ordered-int keys so that
 // atomicMin/atomicMax give the exact fp32 min/max.
 struct FrameStats {
@@ -94,15 +113,16 @@ cudaError_t launch_stats_init(FrameStats *st, int32_t batch, cudaStream_t s);
 cudaError_t launch_stats(const float *D, int64_t HW, int32_t batch, FrameStats *st, cudaStream_t s);
 cudaError_t launch_direct(const float *D, int32_t H, int32_t W, int32_t batch,
                           const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
-                          const FrameStats *st, const Params &p, uint8_t *masks, cudaStream_t s);
+                          const FrameStats *st, const Params &p, uint8_t *masks, const MaskFmt &mf,
+                          cudaStream_t s);
 size_t tile_smem_bytes();
 constexpr int kTilePositions = 224;    // TP (7 blocks of 32: smem for 3 CTAs per SM)
 constexpr int kTileHaloMax = 96;       // staged halo per side (multiple of 32)
 cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
                         const TileDesc *tiles, int32_t ntiles, const GroupDesc *groups,
                         const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
-                        const FrameStats *st, const Params &p, uint8_t *masks, const void *codes,
-                        int32_t code_bytes, cudaStream_t s);
+                        const FrameStats *st, const Params &p, uint8_t *masks, const MaskFmt &mf,
+                        const void *codes, int32_t code_bytes, cudaStream_t s);
 // Line-sweep kernel (k_line.cu) for the four line families of |b| <= 1
 // arrays: one warp per unit = 32 consecutive lines x [t0, t1) in the lane's
 // time coordinate (t0, t1 multiples of 32, t1 - t0 <= kLineSeg).
@@ -122,9 +142,10 @@ size_t line_smem_bytes();
 cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
                         const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
-                        const void *codes, int32_t code_bytes, unsigned long long *dbg, HardEntry *gq,
-                        uint32_t *gq_count, int32_t gq_cap, cudaStream_t s);
-cudaError_t launch_hard(const float *D, uint8_t *masks, int64_t HW, int32_t nviews, const ViewDesc *views,
+                        const MaskFmt &mf, const void *codes, int32_t code_bytes, unsigned long long *dbg,
+                        HardEntry *gq, uint32_t *gq_count, int32_t gq_cap, cudaStream_t s);
+cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW,
+                        int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
                         int32_t nsm, cudaStream_t s);
 // Pixel-wise median fusion (k_fuse.cu): stack [K][n] -> out [n].

@@ -27,7 +27,9 @@ PATHS = {"auto": 0, "tiled": 1, "direct": 2}
 # every function include/occ.h declares (checked against the header by tests)
 EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", "occ_status",
            "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
-           "occ_version", "occ_profile", "occ_profile_read", "occ_fuse_median"]
+           "occ_version", "occ_profile", "occ_profile_read", "occ_fuse_median", "occ_set_mask_format",
+           "occ_mask_bytes"]
+MASK_FORMATS = {"u8": 0, "bits": 1}
 KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5}
 
 
@@ -88,6 +90,10 @@ def lib() -> ctypes.CDLL:
         L.occ_version.restype = i32
         L.occ_fuse_median.argtypes = [vp, i32, ctypes.c_int64, vp, vp]
         L.occ_fuse_median.restype = ctypes.c_int
+        L.occ_set_mask_format.argtypes = [vp, i32]
+        L.occ_set_mask_format.restype = ctypes.c_int
+        L.occ_mask_bytes.argtypes = [vp, i32]
+        L.occ_mask_bytes.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -125,7 +131,7 @@ class Detector:
 
     def __init__(self, H: int, W: int, baselines: Sequence[Tuple[int, int]], t_edge: float = 1.0,
                  t_dist: float = 2.0, t_disp: float = 0.5, max_scan: int = 4096, max_batch: int = 1,
-                 path: str = "auto"):
+                 path: str = "auto", mask_format: str = "u8"):
         self.H, self.W = int(H), int(W)
         self.baselines: List[Tuple[int, int]] = [(int(a), int(b)) for a, b in baselines]
         self.V = len(self.baselines)
@@ -137,6 +143,11 @@ class Detector:
         self._h = h
         self._last_batch = 0
         self.set_path(path)
+        self.mask_format = mask_format
+        rc = lib().occ_set_mask_format(self._h, MASK_FORMATS[mask_format])
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_set_mask_format")
+        self.Wb = (self.W + 31) // 32
 
     def set_path(self, path: str) -> None:
         rc = lib().occ_set_path(self._h, PATHS[path])
@@ -153,9 +164,10 @@ class Detector:
         if tuple(D.shape[1:]) != (self.H, self.W):
             raise ValueError(f"expected [B, {self.H}, {self.W}], got {tuple(D.shape)}")
         if out is None:
-            out = torch.empty((B, self.V, self.H, self.W), dtype=torch.uint8, device=D.device)
-        elif out.dtype != torch.uint8 or not out.is_contiguous() or out.numel() < B * self.V * self.H * self.W:
-            raise ValueError("out must be a contiguous uint8 CUDA tensor [B, V, H, W]")
+            out = torch.empty(self.mask_shape(B), dtype=self.mask_dtype(torch), device=D.device)
+        elif (out.dtype != self.mask_dtype(torch) or not out.is_contiguous()
+              or out.numel() * out.element_size() < lib().occ_mask_bytes(self._h, B)):
+            raise ValueError(f"out must be a contiguous {self.mask_dtype(torch)} CUDA tensor {self.mask_shape(B)}")
         s = stream if stream is not None else torch.cuda.current_stream(D.device)
         rc = lib().occ_detect(self._h, D.data_ptr(), out.data_ptr(), B, s.cuda_stream)
         if rc != OCC_OK:
@@ -170,7 +182,7 @@ class Detector:
             D = D[None]
         B = D.shape[0]
         if out is None:
-            out = np.empty((B, self.V, self.H, self.W), dtype=np.uint8)
+            out = np.empty(self.mask_shape(B), dtype=np.uint8 if self.mask_format == "u8" else np.uint32)
         sp = 0
         if stream is not None:
             sp = stream.cuda_stream
@@ -185,6 +197,13 @@ class Detector:
             raise OccError(rc, "occ_detect_host")
         self._last_batch = B
         return out
+
+    def mask_shape(self, B: int):
+        """[B, V, H, W] for uint8 masks, [B, V, H, ceil(W/32)] words for bit-packed ones."""
+        return (B, self.V, self.H, self.W if self.mask_format == "u8" else self.Wb)
+
+    def mask_dtype(self, torch):
+        return torch.uint8 if self.mask_format == "u8" else torch.int32
 
     def detect_host_ptr(self, d_ptr: int, m_ptr: int, batch: int, stream_ptr: int = 0) -> None:
         rc = lib().occ_detect_host(self._h, d_ptr, m_ptr, batch, stream_ptr)
@@ -256,3 +275,11 @@ def fuse_median(stack, out=None, stream=None):
     if rc != OCC_OK:
         raise OccError(rc, "occ_fuse_median")
     return out
+
+
+def unpack_masks(words: np.ndarray, W: int) -> np.ndarray:
+    """Bit-packed masks (OCC_MASK_BITS: [..., H, ceil(W/32)] 32-bit words, bit
+    x & 31 of word x >> 5) -> uint8 0/1 masks [..., H, W] (host-side view helper)."""
+    w = np.ascontiguousarray(words).view(np.uint32)
+    b = np.unpackbits(w.view(np.uint8), axis=-1, bitorder="little")
+    return b[..., :W]
