@@ -64,6 +64,8 @@ def lib() -> ctypes.CDLL:
             "bf1_detect": (ctypes.c_int, [f32p, i32, i32, i32p, i32, f32, f32, f32, i32, u8p]),
             "bf2_zbuffer": (ctypes.c_int, [f32p, i32, i32, i32, i32, f32, u8p]),
             "orc_fuse_median": (ctypes.c_int, [f32p, i32, ctypes.c_int64, f32p]),
+            "orc_count_n": (None, [i32p, f32p, i32p, i32, i32, f32, f32, i32, i32p]),
+            "orc_detect_n": (ctypes.c_int, [f32p, i32, i32, i32p, i32, f32, f32, f32, i32, i32, u8p, i32p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -83,7 +85,7 @@ def _baselines(views: Sequence[Tuple[int, int]]) -> np.ndarray:
 
 def detect(D: np.ndarray, views: Sequence[Tuple[int, int]], t_edge: float = 1.0,
            t_dist: float = 2.0, t_disp: float = 0.5, max_scan: int = 4096,
-           return_info: bool = False):
+           return_info: bool = False, neighbors: int = 0):
     """Oracle masks uint8 [V, H, W] for one fp32 [H, W] map; raises on error codes
     other than NONFINITE (which returns zero masks and rc)."""
     D = np.ascontiguousarray(D, dtype=np.float32)
@@ -92,9 +94,9 @@ def detect(D: np.ndarray, views: Sequence[Tuple[int, int]], t_edge: float = 1.0,
     V = b.shape[0]
     masks = np.zeros((V, H, W), dtype=np.uint8)
     info = np.zeros((V, 4), dtype=np.int32)
-    rc = lib().orc_detect(_p(D, ctypes.c_float), H, W, _p(b, ctypes.c_int32), V,
-                          t_edge, t_dist, t_disp, max_scan,
-                          _p(masks, ctypes.c_uint8), _p(info, ctypes.c_int32))
+    rc = lib().orc_detect_n(_p(D, ctypes.c_float), H, W, _p(b, ctypes.c_int32), V,
+                            t_edge, t_dist, t_disp, max_scan, int(neighbors),
+                            _p(masks, ctypes.c_uint8), _p(info, ctypes.c_int32))
     if rc not in (OK, ERR_NONFINITE):
         raise ValueError(f"orc_detect rc={rc}")
     if return_info:
@@ -213,3 +215,14 @@ def fuse_median(stack: np.ndarray) -> np.ndarray:
     if rc != OK:
         raise ValueError(f"orc_fuse_median rc={rc}")
     return out
+
+
+def count_n(g, v, idx, N, s=1, t_dist=2.0, t_disp=0.5) -> np.ndarray:
+    """O10 with a finite neighbour count N over a sorted line (orc_count_n)."""
+    g = np.ascontiguousarray(g, np.int32)
+    v = np.ascontiguousarray(v, np.float32)
+    idx = np.ascontiguousarray(idx, np.int32)
+    O = np.zeros(len(g), np.int32)
+    lib().orc_count_n(_p(g, ctypes.c_int32), _p(v, ctypes.c_float), _p(idx, ctypes.c_int32), len(g), s,
+                      t_dist, t_disp, int(N), _p(O, ctypes.c_int32))
+    return O

@@ -240,10 +240,54 @@ void orc_count(const int32_t *g, const float *v, const double *w, const int32_t 
     }
 }
 
+/* ----------------------------------------------- O10 with finite N */
+void orc_count_n(const int32_t *g, const float *v, const int32_t *idx, int32_t n, int32_t s,
+                 float t_dist, float t_disp, int32_t N, int32_t *O)
+{
+    /* PAPER.md:131-142 (Eq. 5) literally: each entry i of the sorted warped
+     * line is compared with the entries at sorted offsets d in
+     * {-N/2..-1, 1..N/2}; offsets beyond the line are skipped (SPEC.md:197,
+     * 244).  The pair test is the exact S7 predicate (reading Q14), so the
+     * warped distance is |dk + s delta| with delta rounded once. */
+    for (int32_t i = 0; i < n; ++i) O[i] = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        int32_t p = idx[i];
+        for (int32_t d = 1; d <= N / 2; ++d) {
+            if (i + d < n) {
+                int32_t q = idx[i + d];
+                if (orc_pair(v[q], v[p], g[q] - g[p], s, t_dist, t_disp)) O[p]++;
+            }
+            if (i - d >= 0) {
+                int32_t q = idx[i - d];
+                if (orc_pair(v[q], v[p], g[q] - g[p], s, t_dist, t_disp)) O[p]++;
+            }
+        }
+    }
+}
+
 /* --------------------------------------------------------- O1-O11 */
+static int detect_impl(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
+                       float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t Nnb,
+                       uint8_t *masks, int32_t *info);
+
 int orc_detect(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
                float t_edge, float t_dist, float t_disp, int32_t max_scan,
                uint8_t *masks, int32_t *info)
+{
+    return detect_impl(D, H, W, baselines, V, t_edge, t_dist, t_disp, max_scan, 0, masks, info);
+}
+
+int orc_detect_n(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
+                 float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t N,
+                 uint8_t *masks, int32_t *info)
+{
+    if (N < 0 || (N > 0 && (N < 2 || (N & 1)))) return ORC_ERR_INVALID_ARG;
+    return detect_impl(D, H, W, baselines, V, t_edge, t_dist, t_disp, max_scan, N, masks, info);
+}
+
+static int detect_impl(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
+                       float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t Nnb,
+                       uint8_t *masks, int32_t *info)
 {
     int rc = orc_validate(H, W, baselines, V, t_edge, t_dist, t_disp, max_scan);
     if (rc != ORC_OK) return rc;
@@ -289,7 +333,8 @@ int orc_detect(const float *D, int32_t H, int32_t W, const int32_t *baselines, i
                     for (int32_t i = 0; i < n; ++i)                      /* O8: W = G + V */
                         w[i] = (double)g[i] + (double)s * (double)v[i];
                     orc_sort(w, n, idx);                                 /* O9 */
-                    orc_count(g, v, w, idx, n, s, t_dist, t_disp, eps, O); /* O10 */
+                    if (Nnb > 0) orc_count_n(g, v, idx, n, s, t_dist, t_disp, Nnb, O);   /* O10, finite N */
+                    else orc_count(g, v, w, idx, n, s, t_dist, t_disp, eps, O);     /* O10, N = inf */
                     for (int32_t i = 0; i < n; ++i)                      /* O11: Eq. 6, OR */
                         if (O[i] > 0) mask[(int64_t)ys[i] * W + xs[i]] = 1;
                 }

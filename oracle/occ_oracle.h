@@ -95,6 +95,19 @@ int bf1_detect(const float *D, int32_t H, int32_t W, const int32_t *baselines, i
 int bf2_zbuffer(const float *D, int32_t H, int32_t W, int32_t bx, int32_t by,
                 float t_disp, uint8_t *mask);
 
+/* O10 with a finite neighbour count N (SPEC.md:197,
+ * 244): each sorted entry is compared with the entries at sorted offsets
+ * d in {-N/2..-1, 1..N/2} (skipped beyond the line) with the exact pair
+ * predicate (orc_pair); O[p] counts the pairs.  N even >= 2. */
+void orc_count_n(const int32_t *g, const float *v, const int32_t *idx, int32_t n, int32_t s,
+                 float t_dist, float t_disp, int32_t N, int32_t *O);
+
+/* O1-O11 with a finite neighbour count N (N = 0: N = infinity, identical to
+ * orc_detect).  Returns ORC_ERR_INVALID_ARG for odd N or N < 2 (N != 0). */
+int orc_detect_n(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
+                 float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t N,
+                 uint8_t *masks, int32_t *info);
+
 /* Pixel-wise median fusion of K disparity estimates.
  * PAPER.md:238 (§4.2, "fused to a single disparity map by pixel-wise median
  * filtering"); SPEC.md:51-58 (fuse_median: for even counts the arithmetic
