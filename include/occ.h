@@ -121,6 +121,24 @@ int occ_set_mask_format(occ_ctx *ctx, int32_t format);
  * a null context or negative batch). */
 int64_t occ_mask_bytes(const occ_ctx *ctx, int32_t batch);
 
+/* Neighbour count N of Eq. 5:
+ * each entry of a sorted warped scan line is compared with the entries at
+ * sorted offsets d in {-N/2..-1, 1..N/2} only (offsets beyond
+ * the line skipped; SPEC.md:155's default is N = 8).  N = 0 (the context's
+ * default) selects N = infinity, the per-pixel form every other path
+ * computes.  With N > 0 subsequent calls run the per-window kernel k_nwin
+ * (one warp per candidate window: sort by (W, scan index), then the +-N/2
+ * neighbour tests) whatever occ_set_path selected; the output is
+ * bit-identical to the oracle's orc_detect_n.  Longer windows than the
+ * kernel's shared-memory capacity (h > 159) use device scratch allocated on
+ * first use (about nsm * 8 * (max_scan + 1) * 16 bytes).
+ * Returns OCC_OK, OCC_ERR_INVALID_ARG (N odd, N < 0, N > 65536, NULL ctx)
+ * or OCC_ERR_OOM. */
+int occ_set_neighbors(occ_ctx *ctx, int32_t N);
+
+/* Current N (0 = infinity), -1 on a NULL context. */
+int32_t occ_get_neighbors(const occ_ctx *ctx);
+
 /* Selects the kernel path for subsequent calls (OCC_PATH_*). */
 int occ_set_path(occ_ctx *ctx, int32_t path);
 
@@ -133,7 +151,7 @@ int32_t occ_last_launches(const occ_ctx *ctx);
  * synchronises and returns, for one kernel kind, the summed device time in
  * milliseconds and the number of launches since the last reset. */
 enum { OCC_KERNEL_INIT = 0, OCC_KERNEL_STATS = 1, OCC_KERNEL_TILE = 2, OCC_KERNEL_DIRECT = 3,
-       OCC_KERNEL_CAND = 4, OCC_KERNEL_LINE = 5, OCC_KERNEL_KINDS = 6 };
+       OCC_KERNEL_CAND = 4, OCC_KERNEL_LINE = 5, OCC_KERNEL_NWIN = 6, OCC_KERNEL_KINDS = 7 };
 int occ_profile(occ_ctx *ctx, int32_t enable);
 int occ_profile_read(occ_ctx *ctx, int32_t kind, double *total_ms, int32_t *launches);
 

@@ -28,7 +28,7 @@ def sources():
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "occ.h")]
+    deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.h")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "occ.h")]
     newest = max(os.path.getmtime(p) for p in deps)
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= newest:
         return SO

@@ -19,6 +19,9 @@ using namespace occ;
 struct occ_ctx {
     int32_t H = 0, W = 0, V = 0, nfam = 0, max_batch = 0, device = 0;
     int32_t path = OCC_PATH_AUTO;
+    int32_t neighbors = 0;               // occ_set_neighbors: N (0 = infinity)
+    uint32_t *d_nwin_work = nullptr;     // k_nwin granule counters (lazy)
+    NwinScratch nwin_big;                // k_nwin scratch for windows > kNwinCap (lazy)
     MaskFmt mf{0, 0, 0};                 // occ_set_mask_format
     Params params{};
     std::vector<ViewDesc> views;
@@ -442,6 +445,21 @@ int occ_set_path(occ_ctx *c, int32_t path) {
 
 int32_t occ_last_launches(const occ_ctx *c) { return c ? c->last_launches : -1; }
 
+int occ_set_neighbors(occ_ctx *c, int32_t N) {
+    if (!c || N < 0 || N == 1 || (N & 1) || N > 65536) return OCC_ERR_INVALID_ARG;
+    if (N > 0 && !c->d_nwin_work) {
+        CK(cudaSetDevice(c->device));
+        if (cudaMalloc(&c->d_nwin_work, 2 * sizeof(uint32_t)) != cudaSuccess) {
+            cudaGetLastError();
+            return OCC_ERR_OOM;
+        }
+    }
+    c->neighbors = N;
+    return OCC_OK;
+}
+
+int32_t occ_get_neighbors(const occ_ctx *c) { return c ? c->neighbors : -1; }
+
 }  // extern "C"
 
 namespace {
@@ -455,6 +473,14 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
                            c->d_stats + c0, c->d_codes, c->code_bytes, s)); ++launches;
         ps.end();
+    }
+    if (c->neighbors > 0) {         // finite N: per-window kernel (masks pre-zeroed)
+        ProfScope pn(c, OCC_KERNEL_NWIN, s);
+        CK(launch_nwin(Dc, c->H, c->W, n, c->d_views, c->V, c->d_stats + c0, c->params, c->neighbors, Mc,
+                       c->mf, c->d_codes, c->code_bytes, c->d_nwin_work, c->nwin_big, c->nsm, s));
+        launches += 2 * c->params.max_scan / 2 + 1 > kNwinCap ? 2 : 1;
+        pn.end();
+        return OCC_OK;
     }
     const bool tiled_only = c->path == OCC_PATH_TILED;
     if (!tiled_only && !c->units.empty()) {
@@ -493,14 +519,14 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
     CK(cudaSetDevice(c->device));
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
-    if (c->mf.packed)       // packed planes: kernels set bits only
+    if (c->mf.packed || c->neighbors > 0)   // packed planes / finite N: kernels set marks only
         CK(cudaMemsetAsync(M, 0, (size_t)batch * c->V * c->mf.vbytes, s));
     {
         ProfScope ps(c, OCC_KERNEL_INIT, s);
         CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
         ps.end();
     }
-    if (c->path == OCC_PATH_DIRECT) {
+    if (c->path == OCC_PATH_DIRECT && c->neighbors == 0) {
         {
             ProfScope ps(c, OCC_KERNEL_STATS, s);
             CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
@@ -547,7 +573,8 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
     // pipeline granularity: ~64 MiB of D per copy (finer than the device-side
     // chunk, so the first H2D and the last D2H expose little of the step)
     const int32_t pipe = (int32_t)std::max<int64_t>(1, ((int64_t)64 << 20) / (int64_t)(HW * sizeof(float)));
-    const int32_t chunk = c->path == OCC_PATH_DIRECT ? batch : std::min(c->chunk, pipe);
+    const bool direct = c->path == OCC_PATH_DIRECT && c->neighbors == 0;
+    const int32_t chunk = direct ? batch : std::min(c->chunk, pipe);
     const int32_t nchunks = (batch + chunk - 1) / chunk;
     while ((int32_t)c->ev_pipe.size() < 2 * nchunks + 1) {
         cudaEvent_t e;
@@ -564,7 +591,7 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
         CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
         ps.end();
     }
-    if (c->mf.packed && c->path != OCC_PATH_DIRECT)
+    if ((c->mf.packed || c->neighbors > 0) && !direct)
         CK(cudaMemsetAsync(c->d_stage_M, 0, (size_t)batch * c->V * c->mf.vbytes, s));
     for (int32_t i = 0; i < nchunks; ++i) {
         const int32_t c0 = i * chunk, n = std::min(chunk, batch - c0);
@@ -572,7 +599,7 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
                            cudaMemcpyHostToDevice, c->s_h2d));
         CK(cudaEventRecord(c->ev_pipe[2 * i], c->s_h2d));
         CK(cudaStreamWaitEvent(s, c->ev_pipe[2 * i], 0));
-        if (c->path == OCC_PATH_DIRECT) {
+        if (direct) {
             int rc = occ_detect(c, c->d_stage_D, c->d_stage_M, batch, stream);
             if (rc != OCC_OK) return rc;
             launches += c->last_launches;
@@ -702,6 +729,10 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_dbg);
     cudaFree(c->d_gq);
     cudaFree(c->d_gq_count);
+    cudaFree(c->d_nwin_work);
+    cudaFree(c->nwin_big.w);
+    cudaFree(c->nwin_big.v);
+    cudaFree(c->nwin_big.s);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     for (cudaEvent_t e : c->ev_pipe) cudaEventDestroy(e);

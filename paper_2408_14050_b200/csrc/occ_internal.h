@@ -151,6 +151,21 @@ cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32
 // Pixel-wise median fusion (k_fuse.cu): stack [K][n] -> out [n].
 constexpr int kFuseMaxK = 64;
 cudaError_t launch_fuse_median(const float *stack, int32_t K, int64_t n, float *out, int nsm, cudaStream_t s);
+// Finite-N detector (k_nwin.cu, occ_set_neighbors): one warp per candidate
+// window; windows of up to kNwinCap entries in shared memory, longer ones in
+// lazily allocated global scratch.
+constexpr int kNwinCap = 320;
+struct NwinScratch {
+    double *w = nullptr;
+    float *v = nullptr;
+    int32_t *s = nullptr;
+    size_t entries = 0;
+};
+size_t nwin_smem_bytes();
+cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, const ViewDesc *views,
+                        int32_t nviews, const FrameStats *st, const Params &p, int32_t N, uint8_t *masks,
+                        const MaskFmt &mf, const void *codes, int32_t code_bytes, uint32_t *work,
+                        NwinScratch &big, int32_t nsm, cudaStream_t s);
 cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
                             const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
                             FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s);

@@ -28,9 +28,9 @@ PATHS = {"auto": 0, "tiled": 1, "direct": 2}
 EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", "occ_status",
            "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
            "occ_version", "occ_profile", "occ_profile_read", "occ_fuse_median", "occ_set_mask_format",
-           "occ_mask_bytes"]
+           "occ_mask_bytes", "occ_set_neighbors", "occ_get_neighbors"]
 MASK_FORMATS = {"u8": 0, "bits": 1}
-KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5}
+KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5, "nwin": 6}
 
 
 class occ_baseline(ctypes.Structure):
@@ -94,6 +94,10 @@ def lib() -> ctypes.CDLL:
         L.occ_set_mask_format.restype = ctypes.c_int
         L.occ_mask_bytes.argtypes = [vp, i32]
         L.occ_mask_bytes.restype = ctypes.c_int64
+        L.occ_set_neighbors.argtypes = [vp, i32]
+        L.occ_set_neighbors.restype = ctypes.c_int
+        L.occ_get_neighbors.argtypes = [vp]
+        L.occ_get_neighbors.restype = i32
         _lib = L
     return _lib
 
@@ -131,7 +135,7 @@ class Detector:
 
     def __init__(self, H: int, W: int, baselines: Sequence[Tuple[int, int]], t_edge: float = 1.0,
                  t_dist: float = 2.0, t_disp: float = 0.5, max_scan: int = 4096, max_batch: int = 1,
-                 path: str = "auto", mask_format: str = "u8"):
+                 path: str = "auto", mask_format: str = "u8", neighbors: int = 0):
         self.H, self.W = int(H), int(W)
         self.baselines: List[Tuple[int, int]] = [(int(a), int(b)) for a, b in baselines]
         self.V = len(self.baselines)
@@ -148,6 +152,14 @@ class Detector:
         if rc != OCC_OK:
             raise OccError(rc, "occ_set_mask_format")
         self.Wb = (self.W + 31) // 32
+        self.set_neighbors(neighbors)
+
+    def set_neighbors(self, N: int) -> None:
+        """Eq. 5's neighbour count N (0 = infinity; see occ_set_neighbors)."""
+        rc = lib().occ_set_neighbors(self._h, int(N))
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_set_neighbors")
+        self.neighbors = int(N)
 
     def set_path(self, path: str) -> None:
         rc = lib().occ_set_path(self._h, PATHS[path])
