@@ -14,13 +14,15 @@
 //   1. the window's valid extent [glo, ghi] (the digital line clipped to the
 //      image is one interval of g), v = D on it, w = fl64(g + s v) -- the
 //      same binary64 value the oracle sorts;
-//   2. rank of every entry by counting smaller keys (w, index).  An entry q
-//      with g_q - g_i > s (v_i - vmin) >= s (v_i - v_q) has exact w_q > w_i,
-//      so (rounding is monotone, ties go by index) key_q > key_i without a
-//      comparison, and symmetrically below; the count only visits
-//      [i - ceil(s (vmax - v_i)), i + ceil(s (v_i - vmin))];
-//   3. sorted[rank] = i; each sorted position r tests the pairs (r, r +- d),
-//      d = 1..N/2, with pair_exact and marks the entry's pixel.
+//   2. rank of every entry under (w, index): the window splits into runs of
+//      non-decreasing w; an entry's rank sums, over the runs, the entries
+//      below it (own run: its offset; other runs: all, none, or one binary
+//      search).  Windows with many runs count directly over the g-range
+//      outside which the order is fixed by g alone;
+//   3. sorted[rank] = i; every unordered pair of sorted positions
+//      {r, r + d}, d = 1..N/2, gets one Eq. 5 test serving both orientations
+//      (the d loop stops once the warped distances exceed t_dist + eps), and
+//      the flagged entries' pixels are marked.
 // Masks are zeroed before the launch; the kernel only sets 1s (u8 byte
 // stores or atomicOr on packed words), so overlapping windows OR their marks.
 //
@@ -37,6 +39,7 @@ namespace {
 
 constexpr int kNwinWarps = 8;
 constexpr int kGran = 256;     // pixels per work granule
+constexpr int kMaxRuns = 24;   // run-merge ranking up to this many runs per window
 
 struct NwinArgs {
     const float *D;
@@ -53,10 +56,25 @@ struct NwinArgs {
     uint32_t *work;            // granule counter (zeroed before the launch)
     int64_t ngran, gpf;        // granules total / per frame
     int32_t cap;               // window capacity of the storage this launch uses
-    double *gw;                // global scratch (big launch): [warp][cap] doubles
-    float *gv;                 //                              [warp][cap] floats
-    int32_t *gs;               //                              [warp][cap] ints
+    unsigned char *gbuf;       // global scratch (big launch): [warp][cap * kNwinEntryBytes]
 };
+
+// Per-warp window storage, kNwinEntryBytes per entry: w (binary64), v,
+// sorted index, run starts.  cap is even, so every warp's slice stays
+// 8-byte aligned.
+struct WinBuf {
+    double *w;
+    float *v;
+    int32_t *s, *run;
+};
+__device__ __forceinline__ WinBuf carve(unsigned char *base, int32_t cap) {
+    WinBuf b;
+    b.w = reinterpret_cast<double *>(base);
+    b.v = reinterpret_cast<float *>(base + (size_t)cap * 8);
+    b.s = reinterpret_cast<int32_t *>(base + (size_t)cap * 12);
+    b.run = reinterpret_cast<int32_t *>(base + (size_t)cap * 16);
+    return b;
+}
 
 __device__ __forceinline__ uint32_t load_code(const void *codes, int32_t cb, int64_t i) {
     if (cb == 1) return reinterpret_cast<const uint8_t *>(codes)[i];
@@ -64,35 +82,41 @@ __device__ __forceinline__ uint32_t load_code(const void *codes, int32_t cb, int
     return reinterpret_cast<const uint32_t *>(codes)[i];
 }
 
-// One candidate window (warp-cooperative).  sw / sv / ss: this warp's
-// storage (shared or global), at least n entries.
+__device__ __forceinline__ int32_t fdiv(int32_t a, int32_t den) {   // floor(a / den), den > 0
+    return den == 1 ? a : (den == 2 ? (a >> 1) : floordiv(a, den));
+}
+
+// One candidate window (warp-cooperative).
 __device__ __forceinline__ void window(const NwinArgs &a, const float *__restrict__ Df, uint8_t *Mv,
-                                   const ViewDesc &vd, int32_t h, int32_t cx, int32_t cy,
-                                   double *sw, float *sv, int32_t *ss) {
+                                       const ViewDesc &vd, int32_t h, int32_t cx, int32_t cy,
+                                       const WinBuf &B) {
     const int lane = threadIdx.x & 31;
-    LineGeom lg;
-    lg.init(vd, a.H, a.W, cx, cy);
-    const int32_t uc = vd.sg * (vd.xmajor ? cx : cy);
-    const int32_t s = vd.s;
-    // 1. valid extent: sample g sits at u = uc - g (orc_scanline: x = cx - sg g)
+    // digital line through the candidate (S6): sample g has major coordinate
+    // pc - sg g (orc_scanline: x = cx - sg g) and minor line + floor(major num / den)
+    const int32_t X = vd.xmajor, sg = vd.sg, num = vd.num, den = vd.den, s = vd.s;
+    const int32_t pc = X ? cx : cy;
+    const int32_t line = X ? cy - fdiv(cx * num, den) : cx - fdiv(cy * num, den);
+    const int32_t nmaj = X ? a.W : a.H, nmin = X ? a.H : a.W;
+    // 1. valid extent (the clipped line is one interval of g)
     int32_t glo = INT_MAX, ghi = INT_MIN;
     for (int32_t g0 = -h; g0 <= h; g0 += 32) {
         const int32_t g = g0 + lane;
-        int32_t xx, yy;
-        const bool ok = g <= h && lg.at(uc - g, xx, yy);
-        if (ok) { glo = min(glo, g); ghi = max(ghi, g); }
+        const int32_t mj = pc - sg * g;
+        const int32_t mn = line + fdiv(mj * num, den);
+        if (g <= h && mj >= 0 && mj < nmaj && mn >= 0 && mn < nmin) { glo = min(glo, g); ghi = max(ghi, g); }
     }
     glo = __reduce_min_sync(0xffffffffu, glo);
     ghi = __reduce_max_sync(0xffffffffu, ghi);
     const int32_t n = ghi - glo + 1;        // >= 1: the candidate itself
+    // 2. V = D on the window, W = fl64(G + s V)
     float vmin = INFINITY, vmax = -INFINITY;
     for (int32_t i = lane; i < n; i += 32) {
         const int32_t g = glo + i;
-        int32_t xx, yy;
-        lg.at(uc - g, xx, yy);
-        const float v = __ldg(Df + (int64_t)yy * a.W + xx);
-        sv[i] = v;
-        sw[i] = __dadd_rn((double)g, __dmul_rn((double)s, (double)v));   // PAPER.md:127, W = G + s V
+        const int32_t mj = pc - sg * g;
+        const int32_t mn = line + fdiv(mj * num, den);
+        const float v = __ldg(Df + (X ? (int64_t)mn * a.W + mj : (int64_t)mj * a.W + mn));
+        B.v[i] = v;
+        B.w[i] = __dadd_rn((double)g, __dmul_rn((double)s, (double)v));
         vmin = fminf(vmin, v);
         vmax = fmaxf(vmax, v);
     }
@@ -102,67 +126,126 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
         vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     }
     __syncwarp();
-    // 2. ranks by counting (ties by index), 3. scatter
-    for (int32_t i = lane; i < n; i += 32) {
-        const double wi = sw[i];
-        const float vi = sv[i];
-        // kd >= s (vmax - v_i): q < i - kd has w_q < w_i; ku >= s (v_i - vmin):
-        // q > i + ku has w_q > w_i (rounded up: only >= is needed)
-        const double kd = ceil(__dmul_ru((double)s, __dsub_ru((double)vmax, (double)vi)));
-        const double ku = ceil(__dmul_ru((double)s, __dsub_ru((double)vi, (double)vmin)));
-        const int32_t lo = kd >= (double)i ? 0 : i - (int32_t)kd;
-        const int32_t hi = ku >= (double)(n - 1 - i) ? n - 1 : i + (int32_t)ku;
-        int32_t rank = lo;
-        for (int32_t q = lo; q < i; ++q) rank += sw[q] <= wi ? 1 : 0;   // ties: q < i counts
-        for (int32_t q = i + 1; q <= hi; ++q) rank += sw[q] < wi ? 1 : 0;
-        ss[rank] = i;
+    // 3. rank of every entry under the key (w, index).  The window splits
+    // into maximal runs of non-decreasing w (keys increasing); the rank of
+    // w_i is the sum over runs of the entries below it: the run holding i
+    // contributes i - start, a run wholly below / above contributes all / none,
+    // the rest one binary search.  Inside smooth regions w grows by about 1
+    // per sample, so a window has a few runs (one more per depth edge whose
+    // near side comes first).  Windows with more than kMaxRuns runs (noise
+    // at s >= 2, random maps) count directly: q with g_q - g_i > s (v_i -
+    // vmin) >= s (v_i - v_q) has exact w_q > w_i, so (rounding is monotone,
+    // ties go by index) key_q > key_i without a comparison; symmetrically below.
+    int32_t m = 0;
+    for (int32_t b0 = 0; b0 < n; b0 += 32) {
+        const int32_t i = b0 + lane;
+        const bool st = i < n && (i == 0 || B.w[i] < B.w[i - 1]);
+        const uint32_t bal = __ballot_sync(0xffffffffu, st);
+        if (st) B.run[m + __popc(bal & ((1u << lane) - 1u))] = i;
+        m += __popc(bal);
     }
     __syncwarp();
+    if (m <= kMaxRuns) {
+        for (int32_t i = lane; i < n; i += 32) {
+            const double wi = B.w[i];
+            int32_t rank = 0;
+            for (int32_t k = 0; k < m; ++k) {
+                const int32_t ra = B.run[k], rb = (k + 1 < m ? B.run[k + 1] : n) - 1;
+                if (i >= ra && i <= rb) { rank += i - ra; continue; }
+                const double wa = B.w[ra], wb = B.w[rb];
+                if (rb < i) {                     // keys below w_i: w_q <= w_i
+                    if (wb <= wi) { rank += rb - ra + 1; continue; }
+                    if (!(wa <= wi)) continue;
+                    int32_t lo = ra + 1, hi = rb;     // first q in (ra, rb] with w_q > w_i
+                    while (lo < hi) { const int32_t md = (lo + hi) >> 1; if (B.w[md] > wi) hi = md; else lo = md + 1; }
+                    rank += lo - ra;
+                } else {                          // keys below w_i: w_q < w_i
+                    if (wb < wi) { rank += rb - ra + 1; continue; }
+                    if (!(wa < wi)) continue;
+                    int32_t lo = ra + 1, hi = rb;     // first q in (ra, rb] with w_q >= w_i
+                    while (lo < hi) { const int32_t md = (lo + hi) >> 1; if (B.w[md] >= wi) hi = md; else lo = md + 1; }
+                    rank += lo - ra;
+                }
+            }
+            B.s[rank] = i;
+        }
+    } else {
+        for (int32_t i = lane; i < n; i += 32) {
+            const double wi = B.w[i];
+            const float vi = B.v[i];
+            const double kd = ceil(__dmul_ru((double)s, __dsub_ru((double)vmax, (double)vi)));
+            const double ku = ceil(__dmul_ru((double)s, __dsub_ru((double)vi, (double)vmin)));
+            const int32_t lo = kd >= (double)i ? 0 : i - (int32_t)kd;
+            const int32_t hi = ku >= (double)(n - 1 - i) ? n - 1 : i + (int32_t)ku;
+            int32_t rank = lo;
+            for (int32_t q = lo; q < i; ++q) rank += B.w[q] <= wi ? 1 : 0;   // ties: q < i counts
+            for (int32_t q = i + 1; q <= hi; ++q) rank += B.w[q] < wi ? 1 : 0;
+            B.s[rank] = i;
+        }
+    }
+    __syncwarp();
+    // 4. Eq. 5 over the sorted neighbours d = 1..N/2, one test
+    // per unordered pair {r, r + d}: with delta = fl32(v_hi - v_lo) the
+    // reversed orientation has delta' = -delta exactly and the same warped
+    // distance |dk + s delta|, so one distance test serves both; the entry
+    // with the smaller disparity is marked when |delta| > t_disp.  Per chunk
+    // of 32 sorted positions the d loop ends once no lane's pair is within
+    // t_dist + eps in w (sorted: further d are further in w; eps bounds every
+    // rounding of w and of s delta vs s (v_q - v_p), the oracle's bound of
+    // DESIGN.md §2.3 with the window's max |v|).  Flags in the run slots.
     const int32_t half = a.half;
     const float t_dist = a.p.t_dist, t_disp = a.p.t_disp;
+    const double M = fmax(fabs((double)vmin), fabs((double)vmax));
+    const double lim = __dadd_rn((double)t_dist, __dmul_rn(0x1p-16, __dadd_rn(__dmul_rn((double)s, M), 1.0)));
+    int32_t *hit = B.run;
+    for (int32_t r = lane; r < n; r += 32) hit[r] = 0;
+    __syncwarp();
+    for (int32_t r0 = 0; r0 < n - 1; r0 += 32) {
+        const int32_t r = r0 + lane;
+        const int32_t ip = r < n ? B.s[r] : 0;
+        const float vp = B.v[ip];
+        const double wp = B.w[ip];
+        bool hp = false;
+        for (int32_t d = 1; d <= half; ++d) {
+            const int32_t rq = r + d;
+            bool near = false;
+            if (rq < n) {
+                const int32_t iq = B.s[rq];
+                near = __dsub_rn(B.w[iq], wp) < lim;
+                if (near) {
+                    const float delta = __fsub_rn(B.v[iq], vp);
+                    const int32_t dk = iq - ip;                        // g_q - g_p
+                    const double x = __dmul_rn((double)s, (double)delta);
+                    if (x > __dsub_rn(-(double)t_dist, (double)dk) && x < __dsub_rn((double)t_dist, (double)dk)) {
+                        if (delta > t_disp) hp = true;                 // p behind q
+                        else if (-delta > t_disp) hit[rq] = 1;         // q behind p
+                    }
+                }
+            }
+            if (!__any_sync(0xffffffffu, near)) break;
+        }
+        __syncwarp();
+        if (hp) hit[r] = 1;
+    }
+    __syncwarp();
     for (int32_t r = lane; r < n; r += 32) {
-        const int32_t ip = ss[r];
-        const float vp = sv[ip];
-        bool hit = false;
-        for (int32_t d = 1; d <= half && !hit; ++d) {
-            if (r + d < n) {
-                const int32_t iq = ss[r + d];
-                hit = pair_exact(sv[iq], vp, iq - ip, s, t_dist, t_disp);   // dk = g_q - g_p
-            }
-            if (!hit && r - d >= 0) {
-                const int32_t iq = ss[r - d];
-                hit = pair_exact(sv[iq], vp, iq - ip, s, t_dist, t_disp);
-            }
-        }
-        if (hit) {                                                       // Eq. 6
-            int32_t xx, yy;
-            lg.at(uc - (glo + ip), xx, yy);
-            mask_put(Mv, a.mf, a.W, xx, yy, true);
-        }
+        if (!hit[r]) continue;                                           // Eq. 6
+        const int32_t mj = pc - sg * (glo + B.s[r]);
+        const int32_t mn = line + fdiv(mj * num, den);
+        mask_put(Mv, a.mf, a.W, X ? mj : mn, X ? mn : mj, true);
     }
     __syncwarp();
 }
 
-// kBig = false: windows of 2h + 1 <= cap entries, shared-memory storage;
-// kBig = true: the longer ones, global scratch.
+// kBig = false: windows of 2h + 1 <= kNwinCap entries, shared-memory
+// storage; kBig = true: the longer ones, global scratch.
 template <bool kBig>
 __global__ void __launch_bounds__(32 * kNwinWarps) k_nwin(NwinArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double *sw;
-    float *sv;
-    int32_t *ss;
-    if (kBig) {
-        const int64_t gw = (int64_t)blockIdx.x * kNwinWarps + wid;
-        sw = a.gw + gw * a.cap;
-        sv = a.gv + gw * a.cap;
-        ss = a.gs + gw * a.cap;
-    } else {
-        unsigned char *base = smem + (size_t)wid * a.cap * 16;
-        sw = reinterpret_cast<double *>(base);
-        sv = reinterpret_cast<float *>(base + (size_t)a.cap * 8);
-        ss = reinterpret_cast<int32_t *>(base + (size_t)a.cap * 12);
-    }
+    const size_t wbytes = (size_t)a.cap * kNwinEntryBytes;
+    const WinBuf B = kBig ? carve(a.gbuf + ((size_t)blockIdx.x * kNwinWarps + wid) * wbytes, a.cap)
+                          : carve(smem + (size_t)wid * wbytes, a.cap);
     const int64_t HW = (int64_t)a.H * a.W;
     for (;;) {
         int64_t gi = 0;
@@ -175,10 +258,9 @@ __global__ void __launch_bounds__(32 * kNwinWarps) k_nwin(NwinArgs a) {
         if (fs.nonfinite) continue;                     // masks stay zero
         const float R = frame_range(fs);
         const float *Df = a.D + (int64_t)f * HW;
-        const void *cf = a.codes;
         for (int32_t sub = 0; sub < kGran; sub += 32) {
             const int64_t pix = p0 + sub + lane;
-            const uint32_t code = pix < HW ? load_code(cf, a.code_bytes, (int64_t)f * HW + pix) : 0u;
+            const uint32_t code = pix < HW ? load_code(a.codes, a.code_bytes, (int64_t)f * HW + pix) : 0u;
             if (__ballot_sync(0xffffffffu, code != 0u) == 0u) continue;
             for (int32_t vi = 0; vi < a.nviews; ++vi) {
                 const ViewDesc &vd = a.views[vi];
@@ -192,7 +274,7 @@ __global__ void __launch_bounds__(32 * kNwinWarps) k_nwin(NwinArgs a) {
                     cand &= cand - 1;
                     const int64_t pc = p0 + sub + b;
                     const int32_t cy = (int32_t)(pc / a.W), cx = (int32_t)(pc - (int64_t)cy * a.W);
-                    window(a, Df, Mv, vd, h, cx, cy, sw, sv, ss);
+                    window(a, Df, Mv, vd, h, cx, cy, B);
                 }
             }
         }
@@ -201,7 +283,7 @@ __global__ void __launch_bounds__(32 * kNwinWarps) k_nwin(NwinArgs a) {
 
 }  // namespace
 
-size_t nwin_smem_bytes() { return (size_t)kNwinWarps * kNwinCap * 16; }
+size_t nwin_smem_bytes() { return (size_t)kNwinWarps * kNwinCap * kNwinEntryBytes; }
 
 cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, const ViewDesc *views,
                         int32_t nviews, const FrameStats *st, const Params &p, int32_t N, uint8_t *masks,
@@ -231,21 +313,20 @@ cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, co
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // windows longer than kNwinCap (h > (kNwinCap - 1) / 2): global scratch
     // sized for the largest window max_scan allows
-    const int32_t capbig = 2 * (p.max_scan / 2) + 1;
+    const int32_t capbig = 2 * (p.max_scan / 2) + 2;   // even: 8-byte aligned slices
     if (capbig <= kNwinCap) return cudaSuccess;
     const int32_t blocks = nsm;
-    const size_t need = (size_t)blocks * kNwinWarps * capbig;
-    if (big.entries < need) {
-        cudaFree(big.w); cudaFree(big.v); cudaFree(big.s);
-        big.w = nullptr; big.v = nullptr; big.s = nullptr; big.entries = 0;
-        if ((e = cudaMalloc(&big.w, need * sizeof(double))) != cudaSuccess) return e;
-        if ((e = cudaMalloc(&big.v, need * sizeof(float))) != cudaSuccess) return e;
-        if ((e = cudaMalloc(&big.s, need * sizeof(int32_t))) != cudaSuccess) return e;
-        big.entries = need;
+    const size_t need = (size_t)blocks * kNwinWarps * capbig * kNwinEntryBytes;
+    if (big.bytes < need) {
+        cudaFree(big.buf);
+        big.buf = nullptr;
+        big.bytes = 0;
+        if ((e = cudaMalloc(&big.buf, need)) != cudaSuccess) return e;
+        big.bytes = need;
     }
     a.work = work + 1;
     a.cap = capbig;
-    a.gw = big.w; a.gv = big.v; a.gs = big.s;
+    a.gbuf = big.buf;
     k_nwin<true><<<blocks, 32 * kNwinWarps, 0, s>>>(a);
     return cudaGetLastError();
 }

@@ -730,9 +730,7 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_gq);
     cudaFree(c->d_gq_count);
     cudaFree(c->d_nwin_work);
-    cudaFree(c->nwin_big.w);
-    cudaFree(c->nwin_big.v);
-    cudaFree(c->nwin_big.s);
+    cudaFree(c->nwin_big.buf);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     for (cudaEvent_t e : c->ev_pipe) cudaEventDestroy(e);

@@ -155,11 +155,10 @@ cudaError_t launch_fuse_median(const float *stack, int32_t K, int64_t n, float *
 // window; windows of up to kNwinCap entries in shared memory, longer ones in
 // lazily allocated global scratch.
 constexpr int kNwinCap = 320;
+constexpr int kNwinEntryBytes = 20;
 struct NwinScratch {
-    double *w = nullptr;
-    float *v = nullptr;
-    int32_t *s = nullptr;
-    size_t entries = 0;
+    unsigned char *buf = nullptr;
+    size_t bytes = 0;
 };
 size_t nwin_smem_bytes();
 cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, const ViewDesc *views,
