@@ -235,6 +235,38 @@ def fuse_leg(d, nf, dev, args, peak):
     return res
 
 
+def nwin_leg(d, masks, nf, views, args, peak):
+    """Times the finite-N detector (occ_set_neighbors, NEXT #1; SPEC.md:155's
+    N = 8) on the same resident frames and mask buffer, device-timed with
+    CUDA events; per-launch time of k_nwin from occ_profile."""
+    import torch
+    from paper_2408_14050_b200.occ import Detector
+    N = args.nwin
+    det = Detector(H, W, views, max_batch=nf, neighbors=N)
+    stream = torch.cuda.current_stream(d.device)
+    for _ in range(3):
+        det.detect(d, out=masks)
+    reps = max(3, min(args.steps, 5))
+    det.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        det.detect(d, out=masks)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    kt = det.profile_read()
+    det.profile(False)
+    det.close()
+    pv = nf * H * W * len(views)
+    kms, kn = kt["nwin"]
+    return {"N": N, "frames": nf, "ms_per_step": ms, "value": pv / (ms / 1e3) / 1e6, "unit": "MPV/s",
+            "kernel": "k_nwin", "kernel_ms_per_step": kms / reps, "launches_per_step": kn // reps,
+            "hbm_frac": nf * H * W * (4 + len(views)) / (ms / 1e3) / 1e9 / peak,
+            "note": "one warp per candidate window: sort by (W, index), +-N/2 sorted-neighbour tests"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -248,6 +280,7 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "tiled", "direct"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fuse", action="store_true", help="skip the median-fusion leg")
+    ap.add_argument("--nwin", type=int, default=8, help="finite-N leg's N (0: skip the leg)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -365,6 +398,9 @@ def main():
     if not args.no_fuse:
         fuse = fuse_leg(d, nf, dev, args, peak)
 
+    # ---------------- finite-N leg (NEXT #1): N = 8 per-window sort ----------------
+    nwin = nwin_leg(d, masks, nf, views, args, peak) if args.nwin > 0 else None
+
     if rank != 0:
         return
     cpu = None
@@ -378,7 +414,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world, nf),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_u8": e2e_u8, "clocks": clk.summary(),
         "gpu_launches": launches, "path": args.path,
-        "fuse_median": fuse,
+        "fuse_median": fuse, "finite_n": nwin,
     }
     print(json.dumps(line), flush=True)
 

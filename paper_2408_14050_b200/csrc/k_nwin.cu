@@ -38,7 +38,10 @@ namespace occ {
 namespace {
 
 constexpr int kNwinWarps = 8;
-constexpr int kGran = 256;     // pixels per work granule
+#ifndef NWIN_GRAN
+#define NWIN_GRAN 32
+#endif
+constexpr int kGran = NWIN_GRAN;   // pixels per work granule
 constexpr int kMaxRuns = 24;   // run-merge ranking up to this many runs per window
 
 struct NwinArgs {
@@ -110,15 +113,25 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
     const int32_t n = ghi - glo + 1;        // >= 1: the candidate itself
     // 2. V = D on the window, W = fl64(G + s V)
     float vmin = INFINITY, vmax = -INFINITY;
-    for (int32_t i = lane; i < n; i += 32) {
-        const int32_t g = glo + i;
-        const int32_t mj = pc - sg * g;
-        const int32_t mn = line + fdiv(mj * num, den);
-        const float v = __ldg(Df + (X ? (int64_t)mn * a.W + mj : (int64_t)mj * a.W + mn));
-        B.v[i] = v;
-        B.w[i] = __dadd_rn((double)g, __dmul_rn((double)s, (double)v));
-        vmin = fminf(vmin, v);
-        vmax = fmaxf(vmax, v);
+    for (int32_t i0 = 0; i0 < n; i0 += 128) {      // 4 gathers in flight per lane
+        float vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int32_t i = i0 + 32 * u + lane;
+            const int32_t mj = pc - sg * (glo + i);
+            const int32_t mn = line + fdiv(mj * num, den);
+            vv[u] = i < n ? __ldg(Df + (X ? (int64_t)mn * a.W + mj : (int64_t)mj * a.W + mn)) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int32_t i = i0 + 32 * u + lane;
+            if (i < n) {
+                B.v[i] = vv[u];
+                B.w[i] = __dadd_rn((double)(glo + i), __dmul_rn((double)s, (double)vv[u]));
+                vmin = fminf(vmin, vv[u]);
+                vmax = fmaxf(vmax, vv[u]);
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
