@@ -226,6 +226,7 @@ struct LineArgs {
     int32_t gq_cap;
     int32_t nwork;             // units x frames
     MaskFmt mf;
+    int32_t frame_major;       // work order: 0 frames fastest, 1 units fastest (frame-major)
 };
 
 // Per-warp context
@@ -1086,12 +1087,12 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
 template <int CB>
 __global__ void __launch_bounds__(128) k_line(LineArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    // one work unit per warp; frames fastest: co-resident warps work on the
-    // same line family and start together (shared instruction-cache footprint)
+    // one work unit per warp, frame-major (units fastest, longest first)
     const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (wid >= (uint32_t)a.nwork) return;
-    const int32_t f = (int32_t)(wid % (unsigned)a.frames);
-    const LineUnit u = a.units[wid / (unsigned)a.frames];
+    const uint32_t nu = (uint32_t)a.nwork / (uint32_t)a.frames;
+    const int32_t f = a.frame_major ? (int32_t)(wid / nu) : (int32_t)(wid % (unsigned)a.frames);
+    const LineUnit u = a.units[a.frame_major ? wid % nu : wid / (unsigned)a.frames];
     const GroupDesc gd = a.groups[u.group];
     const FamilyDesc fd = a.fams[gd.fam];
 #ifdef OCC_LINE_STATS
@@ -1154,7 +1155,16 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
                         HardEntry *gq, uint32_t *gq_count, int32_t gq_cap, cudaStream_t s) {
     if (nunits <= 0) return cudaSuccess;
     LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch, gq, gq_count, gq_cap,
-               nunits * batch, mf};
+               nunits * batch, mf, 0};
+    static int order = -1;
+    if (order < 0) {
+        const char *ev = getenv("OCC_LINE_ORDER");
+        // frame-major by default: the warps in flight cover about one frame,
+        // whose D and codes stay in L2 for all four families (measured: k_line
+        // DRAM reads per 25-frame chunk 1.34 GB -> 0.26 GB, same time)
+        order = ev ? atoi(ev) : 1;
+    }
+    a.frame_major = order;
     static int nw = 0;
     if (!nw) {
         const char *ev = getenv("OCC_LINE_WARPS");
