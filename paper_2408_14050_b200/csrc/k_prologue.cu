@@ -9,6 +9,8 @@
 // D is read once from HBM (16-byte loads); the row below is an L2 hit (the
 // neighbouring block reads it at the same time); codes stay L2-resident for
 // K1, which runs on the same chunk right after.
+#include <algorithm>
+
 #include "occ_internal.h"
 
 namespace occ {
@@ -17,9 +19,11 @@ struct FamDirs {
     int32_t n;
     int32_t small;      // all components in {-2..2}: fp32 products are exact
     int32_t bx[kMaxFamilies], by[kMaxFamilies];
+    float fbx[kMaxFamilies], fby[kMaxFamilies];
 };
 
-template <typename CodeT>
+// NF > 0: compile-time family count (unrolled); NF = 0: fd.n at run time
+template <typename CodeT, int NF>
 __device__ __forceinline__ CodeT pixel_code(float c, float right, float below, bool has_r, bool has_b,
                                             const FamDirs &fd, float e2_thresh) {
     // Eq. 1 forward differences (0 on the last column / row), E^2 vs the exact
@@ -29,13 +33,16 @@ __device__ __forceinline__ CodeT pixel_code(float c, float right, float below, b
     const float e2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
     uint32_t code = 0;
     if (e2 > e2_thresh) {
-        for (int k = 0; k < fd.n; ++k) {
+        const int nf = NF > 0 ? NF : fd.n;
+#pragma unroll
+        for (int k = 0; k < (NF > 0 ? NF : kMaxFamilies); ++k) {
+            if (k >= nf) break;
             // Eq. 2 <=> b0 . (E_x, E_y) > 0, exact sign: with |b0| components
             // in {0, 1, 2} both products are exact in fp32 and the sign of a
             // correctly rounded sum is the sign of the exact sum; otherwise binary64
             bool pos, neg;
             if (fd.small) {
-                const float dot = __fadd_rn(__fmul_rn((float)fd.bx[k], ex), __fmul_rn((float)fd.by[k], ey));
+                const float dot = __fadd_rn(__fmul_rn(fd.fbx[k], ex), __fmul_rn(fd.fby[k], ey));
                 pos = dot > 0.0f; neg = dot < 0.0f;
             } else {
                 const double dot = __dadd_rn(__dmul_rn((double)fd.bx[k], (double)ex),
@@ -71,7 +78,7 @@ __device__ __forceinline__ void stat_acc(float d, int32_t &lo, int32_t &hi, uint
 }
 
 // grid: (blocks per frame, frames); block 256
-template <typename CodeT>
+template <typename CodeT, int NF>
 __global__ void __launch_bounds__(256) k_prologue(const float *__restrict__ D, int32_t H, int32_t W,
                                                   FamDirs fd, float e2_thresh, FrameStats *st,
                                                   CodeT *__restrict__ codes) {
@@ -81,14 +88,15 @@ __global__ void __launch_bounds__(256) k_prologue(const float *__restrict__ D, i
     CodeT *Cf = codes + (int64_t)f * HW;
     int32_t lo = 0x7FFFFFFF, hi = (int32_t)0x80000000;
     uint32_t bad = 0;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     if ((W & 3) == 0 && (reinterpret_cast<uintptr_t>(Df) & 15) == 0) {
+        // rows are block-strided, float4 columns thread-strided (no 64-bit
+        // index division per element)
         const float4 *D4 = reinterpret_cast<const float4 *>(Df);
         const int32_t W4 = W >> 2;
-        const int64_t n4 = HW >> 2;
-        for (int64_t t = tid; t < n4; t += nth) {
-            const int32_t y = (int32_t)(t / W4), x = (int32_t)(t - (int64_t)y * W4) * 4;
+        for (int32_t y = blockIdx.x; y < H; y += gridDim.x)
+        for (int32_t xq = threadIdx.x; xq < W4; xq += blockDim.x) {
+            const int64_t t = (int64_t)y * W4 + xq;
+            const int32_t x = xq * 4;
             const float4 c = __ldg(D4 + t);
             const bool has_b = y + 1 < H;
             const float4 b = has_b ? __ldg(D4 + t + W4) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -98,19 +106,21 @@ __global__ void __launch_bounds__(256) k_prologue(const float *__restrict__ D, i
             stat_acc(c.y, lo, hi, bad);
             stat_acc(c.z, lo, hi, bad);
             stat_acc(c.w, lo, hi, bad);
-            CodeT k0 = pixel_code<CodeT>(c.x, c.y, b.x, true, has_b, fd, e2_thresh);
-            CodeT k1 = pixel_code<CodeT>(c.y, c.z, b.y, true, has_b, fd, e2_thresh);
-            CodeT k2 = pixel_code<CodeT>(c.z, c.w, b.z, true, has_b, fd, e2_thresh);
-            CodeT k3 = pixel_code<CodeT>(c.w, r4, b.w, has_r4, has_b, fd, e2_thresh);
+            CodeT k0 = pixel_code<CodeT, NF>(c.x, c.y, b.x, true, has_b, fd, e2_thresh);
+            CodeT k1 = pixel_code<CodeT, NF>(c.y, c.z, b.y, true, has_b, fd, e2_thresh);
+            CodeT k2 = pixel_code<CodeT, NF>(c.z, c.w, b.z, true, has_b, fd, e2_thresh);
+            CodeT k3 = pixel_code<CodeT, NF>(c.w, r4, b.w, has_r4, has_b, fd, e2_thresh);
             store4(Cf + (int64_t)t * 4, k0, k1, k2, k3);
         }
     } else {
+        const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const int64_t nth = (int64_t)gridDim.x * blockDim.x;
         for (int64_t i = tid; i < HW; i += nth) {
             const int32_t y = (int32_t)(i / W), x = (int32_t)(i - (int64_t)y * W);
             const float c = Df[i];
             stat_acc(c, lo, hi, bad);
             const bool has_r = x + 1 < W, has_b = y + 1 < H;
-            Cf[i] = pixel_code<CodeT>(c, has_r ? Df[i + 1] : 0.0f, has_b ? Df[i + W] : 0.0f, has_r,
+            Cf[i] = pixel_code<CodeT, NF>(c, has_r ? Df[i + 1] : 0.0f, has_b ? Df[i + W] : 0.0f, has_r,
                                       has_b, fd, e2_thresh);
         }
     }
@@ -120,10 +130,28 @@ __global__ void __launch_bounds__(256) k_prologue(const float *__restrict__ D, i
         hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
         bad += __shfl_xor_sync(0xffffffffu, bad, o);
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&st[f].minkey, lo);
-        atomicMax(&st[f].maxkey, hi);
-        if (bad) atomicAdd(&st[f].nonfinite, bad);
+    // block reduction, then one set of atomics per block
+    __shared__ int32_t r_lo[8], r_hi[8];
+    __shared__ uint32_t r_bad[8];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { r_lo[w] = lo; r_hi[w] = hi; r_bad[w] = bad; }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        lo = l < nw ? r_lo[l] : 0x7FFFFFFF;
+        hi = l < nw ? r_hi[l] : (int32_t)0x80000000;
+        bad = l < nw ? r_bad[l] : 0u;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            bad += __shfl_xor_sync(0xffffffffu, bad, o);
+        }
+        if (l == 0) {
+            atomicMin(&st[f].minkey, lo);
+            atomicMax(&st[f].maxkey, hi);
+            if (bad) atomicAdd(&st[f].nonfinite, bad);
+        }
     }
 }
 
@@ -135,20 +163,23 @@ cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames
     fd.small = 1;
     for (int k = 0; k < nfam; ++k) {
         fd.bx[k] = fams_host[k].b0x; fd.by[k] = fams_host[k].b0y;
+        fd.fbx[k] = (float)fd.bx[k]; fd.fby[k] = (float)fd.by[k];
         if (fd.bx[k] < -2 || fd.bx[k] > 2 || fd.by[k] < -2 || fd.by[k] > 2) fd.small = 0;
     }
-    const int64_t HW = (int64_t)H * W;
-    const int64_t per_block = 256 * 4 * 4;
-    int bx = (int)((HW + per_block - 1) / per_block);
-    if (bx < 1) bx = 1;
-    if (bx > 2048) bx = 2048;
+    // vector path: blocks stride over rows (about 2 float4 per thread per row
+    // at 1920 wide); scalar path: grid-stride over the pixels
+    const int bx = std::max(1, std::min(H, 256));
     dim3 grid(bx, frames);
-    if (code_bytes == 1)
-        k_prologue<uint8_t><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
-    else if (code_bytes == 2)
-        k_prologue<uint16_t><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint16_t *)codes);
-    else
-        k_prologue<uint32_t><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint32_t *)codes);
+    if (code_bytes == 1) {
+        if (nfam == 4) k_prologue<uint8_t, 4><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
+        else if (nfam == 1) k_prologue<uint8_t, 1><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
+        else k_prologue<uint8_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
+    } else if (code_bytes == 2) {
+        if (nfam == 8) k_prologue<uint16_t, 8><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint16_t *)codes);
+        else k_prologue<uint16_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint16_t *)codes);
+    } else {
+        k_prologue<uint32_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint32_t *)codes);
+    }
     return cudaGetLastError();
 }
 
