@@ -352,10 +352,14 @@ def main():
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
     tr = load_traffic()
     traffic = None
-    if tr and tr.get("kernel") == dom_name and abs(tr.get("alg_bytes_per_launch", -1) - alg_bytes) < 1:
-        traffic = tr.get("bytes_per_launch")
+    traffic_src = None
+    if tr and tr.get("kernel") == dom_name and tr.get("alg_bytes_per_launch"):
+        # DRAM bytes of one full 25-frame chunk (ncu), scaled per algorithmic
+        # byte to this run's average launch (the last chunk is shorter)
+        traffic = tr["bytes_per_launch"] / tr["alg_bytes_per_launch"] * alg_bytes
+        traffic_src = tr.get("source")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "kernel": dom_name,
                 "kernel_ms_per_launch": per_launch_ms, "launches_per_step": launches_per_step,
                 "kernel_share_of_step": dom_ms / ms if ms else None,
                 "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,

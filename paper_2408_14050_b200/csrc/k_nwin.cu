@@ -60,6 +60,7 @@ struct NwinArgs {
     int64_t ngran, gpf;        // granules total / per frame
     int32_t cap;               // window capacity of the storage this launch uses
     unsigned char *gbuf;       // global scratch (big launch): [warp][cap * kNwinEntryBytes]
+    int32_t smax;              // largest ||b||_inf of the views (longest windows)
 };
 
 // Per-warp window storage, kNwinEntryBytes per entry: w (binary64), v,
@@ -260,6 +261,14 @@ __global__ void __launch_bounds__(32 * kNwinWarps) k_nwin(NwinArgs a) {
     const WinBuf B = kBig ? carve(a.gbuf + ((size_t)blockIdx.x * kNwinWarps + wid) * wbytes, a.cap)
                           : carve(smem + (size_t)wid * wbytes, a.cap);
     const int64_t HW = (int64_t)a.H * a.W;
+    if (kBig) {     // nothing to do unless some frame has a window longer than kNwinCap
+        bool need = false;
+        for (int32_t f = lane; f < a.frames; f += 32) {
+            const FrameStats fs = a.st[f];
+            need |= !fs.nonfinite && 2 * view_h(frame_range(fs), a.smax, a.p.max_scan) + 1 > kNwinCap;
+        }
+        if (!__any_sync(0xffffffffu, need)) return;
+    }
     for (;;) {
         int64_t gi = 0;
         if (lane == 0) gi = atomicAdd(a.work, 1u);
@@ -270,6 +279,7 @@ __global__ void __launch_bounds__(32 * kNwinWarps) k_nwin(NwinArgs a) {
         const FrameStats fs = a.st[f];
         if (fs.nonfinite) continue;                     // masks stay zero
         const float R = frame_range(fs);
+        if (kBig && 2 * view_h(R, a.smax, a.p.max_scan) + 1 <= kNwinCap) continue;
         const float *Df = a.D + (int64_t)f * HW;
         for (int32_t sub = 0; sub < kGran; sub += 32) {
             const int64_t pix = p0 + sub + lane;
@@ -301,8 +311,9 @@ size_t nwin_smem_bytes() { return (size_t)kNwinWarps * kNwinCap * kNwinEntryByte
 cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, const ViewDesc *views,
                         int32_t nviews, const FrameStats *st, const Params &p, int32_t N, uint8_t *masks,
                         const MaskFmt &mf, const void *codes, int32_t code_bytes, uint32_t *work,
-                        NwinScratch &big, int32_t nsm, cudaStream_t s) {
+                        NwinScratch &big, int32_t smax, int32_t nsm, cudaStream_t s) {
     NwinArgs a{};
+    a.smax = smax;
     a.D = D; a.H = H; a.W = W; a.frames = frames;
     a.codes = codes; a.code_bytes = code_bytes;
     a.views = views; a.nviews = nviews; a.st = st; a.p = p; a.half = N / 2;

@@ -463,6 +463,12 @@ int32_t occ_get_neighbors(const occ_ctx *c) { return c ? c->neighbors : -1; }
 }  // extern "C"
 
 namespace {
+int32_t smax_of(const occ_ctx *c) {
+    int32_t m = 1;
+    for (const ViewDesc &v : c->views) m = std::max(m, v.s);
+    return m;
+}
+
 // K0 + K1 for frames [c0, c0 + n) of a batch whose frames start at D / M (device).
 int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, cudaStream_t s, int &launches) {
     const int64_t HW = (int64_t)c->H * c->W;
@@ -477,7 +483,7 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
     if (c->neighbors > 0) {         // finite N: per-window kernel (masks pre-zeroed)
         ProfScope pn(c, OCC_KERNEL_NWIN, s);
         CK(launch_nwin(Dc, c->H, c->W, n, c->d_views, c->V, c->d_stats + c0, c->params, c->neighbors, Mc,
-                       c->mf, c->d_codes, c->code_bytes, c->d_nwin_work, c->nwin_big, c->nsm, s));
+                       c->mf, c->d_codes, c->code_bytes, c->d_nwin_work, c->nwin_big, smax_of(c), c->nsm, s));
         launches += 2 * c->params.max_scan / 2 + 1 > kNwinCap ? 2 : 1;
         pn.end();
         return OCC_OK;

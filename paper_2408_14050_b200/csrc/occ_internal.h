@@ -164,7 +164,7 @@ size_t nwin_smem_bytes();
 cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, const ViewDesc *views,
                         int32_t nviews, const FrameStats *st, const Params &p, int32_t N, uint8_t *masks,
                         const MaskFmt &mf, const void *codes, int32_t code_bytes, uint32_t *work,
-                        NwinScratch &big, int32_t nsm, cudaStream_t s);
+                        NwinScratch &big, int32_t smax, int32_t nsm, cudaStream_t s);
 cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
                             const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
                             FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s);
