@@ -267,6 +267,37 @@ def nwin_leg(d, masks, nf, views, args, peak):
             "note": "one warp per candidate window: sort by (W, index), +-N/2 sorted-neighbour tests"}
 
 
+def gather_leg(d, nf, views, dev, world, rank, steps):
+    """N > 1 only: NCCL gather of every rank's bit-packed masks to rank 0
+    (off the hot path, reported separately).  Device-timed with
+    CUDA events around `steps` gathers, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2408_14050_b200 import shard
+    from paper_2408_14050_b200.occ import Detector
+    det = Detector(H, W, views, max_batch=nf, mask_format="bits")
+    mk = det.detect(d)
+    torch.cuda.synchronize()
+    recv = [torch.empty_like(mk) for _ in range(world)] if rank == 0 else None
+    dist.gather(mk, recv, dst=0)                       # warm-up (NCCL channels)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        dist.gather(mk, recv, dst=0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = shard.max_over_ranks(e0.elapsed_time(e1) / steps, dev)
+    per_rank = mk.numel() * mk.element_size()
+    det.close()
+    del recv
+    return {"ms": ms, "bytes_per_rank": per_rank, "bytes_into_rank0": per_rank * (world - 1),
+            "gbs_into_rank0": per_rank * (world - 1) / (ms / 1e3) / 1e9, "mask_format": "bits",
+            "note": "torch.distributed.gather (NCCL) of the packed masks of all frames; not in value"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -402,6 +433,14 @@ def main():
     if not args.no_fuse:
         fuse = fuse_leg(d, nf, dev, args, peak)
 
+    # ---------------- N > 1: NCCL gather of the packed masks to rank 0 ----------------
+    gather = None
+    if world > 1:
+        try:
+            gather = gather_leg(d, nf, views, dev, world, rank, max(1, min(args.steps, 3)))
+        except Exception as ex:   # reported, never fatal: the gather is not part of value
+            gather = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+
     # ---------------- finite-N leg (NEXT #1): N = 8 per-window sort ----------------
     nwin = nwin_leg(d, masks, nf, views, args, peak) if args.nwin > 0 else None
 
@@ -418,7 +457,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world, nf),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_u8": e2e_u8, "clocks": clk.summary(),
         "gpu_launches": launches, "path": args.path,
-        "fuse_median": fuse, "finite_n": nwin,
+        "fuse_median": fuse, "finite_n": nwin, "mask_gather": gather,
     }
     print(json.dumps(line), flush=True)
 

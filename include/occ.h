@@ -139,6 +139,29 @@ int occ_set_neighbors(occ_ctx *ctx, int32_t N);
 /* Current N (0 = infinity), -1 on a NULL context. */
 int32_t occ_get_neighbors(const occ_ctx *ctx);
 
+/* Spatial sharding: a frame too large for one GPU is
+ * split into row bands, each processed with halo rows on its own rank.  The
+ * scan half-length h (Eq. 3) depends on the WHOLE frame's
+ * min/max, so the ranks all-reduce their band statistics and impose the
+ * result on their band:
+ *   occ_frame_stats: exact per-frame min / max / non-finite count of `batch`
+ *     device frames [batch][H][W] (this context's H, W); writes host arrays
+ *     dmin[batch], dmax[batch], nonfinite[batch] (any may be NULL; a frame
+ *     without finite values reports dmin = +inf, dmax = -inf).  Synchronises
+ *     the stream.  Errors: OCC_ERR_INVALID_ARG, OCC_ERR_CUDA.
+ *   occ_set_frame_stats: subsequent occ_detect / occ_detect_host calls use
+ *     dmin[f], dmax[f], nonfinite[f] (host arrays, copied) for frame f < n
+ *     instead of the statistics of the data passed (n = 0 disables the
+ *     override).  Candidates, windows and pairs still come from the data, so
+ *     a band extended by 2 h + 2 halo rows on each side (clipped to the
+ *     frame) yields the whole frame's masks on its interior rows.
+ *     Errors: OCC_ERR_INVALID_ARG (n < 0, n > max_batch, NULL arrays with
+ *     n > 0, dmin > dmax with a zero non-finite count), OCC_ERR_CUDA. */
+int occ_frame_stats(occ_ctx *ctx, const float *disparity, int32_t batch, float *dmin, float *dmax,
+                    int32_t *nonfinite, void *cuda_stream);
+int occ_set_frame_stats(occ_ctx *ctx, const float *dmin, const float *dmax, const int32_t *nonfinite,
+                        int32_t n);
+
 /* Selects the kernel path for subsequent calls (OCC_PATH_*). */
 int occ_set_path(occ_ctx *ctx, int32_t path);
 

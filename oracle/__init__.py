@@ -65,6 +65,8 @@ def lib() -> ctypes.CDLL:
             "bf2_zbuffer": (ctypes.c_int, [f32p, i32, i32, i32, i32, f32, u8p]),
             "orc_fuse_median": (ctypes.c_int, [f32p, i32, ctypes.c_int64, f32p]),
             "orc_count_n": (None, [i32p, f32p, i32p, i32, i32, f32, f32, i32, i32p]),
+            "orc_detect_range": (ctypes.c_int, [f32p, i32, i32, i32p, i32, f32, f32, f32, i32, i32, f32, f32,
+                                                u8p, i32p]),
             "orc_detect_n": (ctypes.c_int, [f32p, i32, i32, i32p, i32, f32, f32, f32, i32, i32, u8p, i32p]),
         }
         for name, (res, args) in sig.items():
@@ -226,3 +228,20 @@ def count_n(g, v, idx, N, s=1, t_dist=2.0, t_disp=0.5) -> np.ndarray:
     lib().orc_count_n(_p(g, ctypes.c_int32), _p(v, ctypes.c_float), _p(idx, ctypes.c_int32), len(g), s,
                       t_dist, t_disp, int(N), _p(O, ctypes.c_int32))
     return O
+
+
+def detect_range(D: np.ndarray, views, dmin: float, dmax: float, t_edge: float = 1.0, t_dist: float = 2.0,
+                 t_disp: float = 0.5, max_scan: int = 4096, neighbors: int = 0) -> np.ndarray:
+    """orc_detect_range: masks of D with Eq. 3's min / max imposed (a band of a
+    larger frame whose statistics are dmin, dmax)."""
+    D = np.ascontiguousarray(D, dtype=np.float32)
+    H, W = D.shape
+    b = _baselines(views)
+    masks = np.zeros((b.shape[0], H, W), dtype=np.uint8)
+    info = np.zeros((b.shape[0], 4), dtype=np.int32)
+    rc = lib().orc_detect_range(_p(D, ctypes.c_float), H, W, _p(b, ctypes.c_int32), b.shape[0], t_edge, t_dist,
+                                t_disp, max_scan, int(neighbors), float(dmin), float(dmax),
+                                _p(masks, ctypes.c_uint8), _p(info, ctypes.c_int32))
+    if rc != OK:
+        raise ValueError(f"orc_detect_range rc={rc}")
+    return masks

@@ -268,13 +268,13 @@ void orc_count_n(const int32_t *g, const float *v, const int32_t *idx, int32_t n
 /* --------------------------------------------------------- O1-O11 */
 static int detect_impl(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
                        float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t Nnb,
-                       uint8_t *masks, int32_t *info);
+                       const float *range, uint8_t *masks, int32_t *info);
 
 int orc_detect(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
                float t_edge, float t_dist, float t_disp, int32_t max_scan,
                uint8_t *masks, int32_t *info)
 {
-    return detect_impl(D, H, W, baselines, V, t_edge, t_dist, t_disp, max_scan, 0, masks, info);
+    return detect_impl(D, H, W, baselines, V, t_edge, t_dist, t_disp, max_scan, 0, NULL, masks, info);
 }
 
 int orc_detect_n(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
@@ -282,12 +282,25 @@ int orc_detect_n(const float *D, int32_t H, int32_t W, const int32_t *baselines,
                  uint8_t *masks, int32_t *info)
 {
     if (N < 0 || (N > 0 && (N < 2 || (N & 1)))) return ORC_ERR_INVALID_ARG;   /* SPEC.md:155 */
-    return detect_impl(D, H, W, baselines, V, t_edge, t_dist, t_disp, max_scan, N, masks, info);
+    return detect_impl(D, H, W, baselines, V, t_edge, t_dist, t_disp, max_scan, N, NULL, masks, info);
+}
+
+int orc_detect_range(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
+                     float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t N,
+                     float dmin, float dmax, uint8_t *masks, int32_t *info)
+{
+    /* O1-O11 with Eq. 3's "minimum and maximum occurring disparity"
+     * (PAPER.md:113-115) supplied by the caller: the statistics of a whole
+     * frame of which D is a band (spatial sharding, SURVEY §8(f) NEXT #4). */
+    if (N < 0 || (N > 0 && (N < 2 || (N & 1)))) return ORC_ERR_INVALID_ARG;
+    if (!(dmin <= dmax)) return ORC_ERR_INVALID_ARG;
+    const float range[2] = {dmin, dmax};
+    return detect_impl(D, H, W, baselines, V, t_edge, t_dist, t_disp, max_scan, N, range, masks, info);
 }
 
 static int detect_impl(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
                        float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t Nnb,
-                       uint8_t *masks, int32_t *info)
+                       const float *range, uint8_t *masks, int32_t *info)
 {
     int rc = orc_validate(H, W, baselines, V, t_edge, t_dist, t_disp, max_scan);
     if (rc != ORC_OK) return rc;
@@ -297,6 +310,7 @@ static int detect_impl(const float *D, int32_t H, int32_t W, const int32_t *base
 
     float dmin, dmax;
     if (orc_stats(D, H, W, &dmin, &dmax) > 0) return ORC_ERR_NONFINITE;   /* O1, Q18 */
+    if (range) { dmin = range[0]; dmax = range[1]; }                     /* whole-frame stats */
 
     float *Ex = (float *)malloc(sizeof(float) * (size_t)N);
     float *Ey = (float *)malloc(sizeof(float) * (size_t)N);

@@ -108,6 +108,12 @@ int orc_detect_n(const float *D, int32_t H, int32_t W, const int32_t *baselines,
                  float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t N,
                  uint8_t *masks, int32_t *info);
 
+/* orc_detect_n with Eq. 3's min / max supplied by the caller (dmin <= dmax):
+ * the statistics of the whole frame a band D belongs to (spatial sharding). */
+int orc_detect_range(const float *D, int32_t H, int32_t W, const int32_t *baselines, int32_t V,
+                     float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t N,
+                     float dmin, float dmax, uint8_t *masks, int32_t *info);
+
 /* Pixel-wise median fusion of K disparity estimates.
  * PAPER.md:238 (§4.2, "fused to a single disparity map by pixel-wise median
  * filtering"); SPEC.md:51-58 (fuse_median: for even counts the arithmetic

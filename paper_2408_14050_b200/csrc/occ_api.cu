@@ -22,6 +22,8 @@ struct occ_ctx {
     int32_t neighbors = 0;               // occ_set_neighbors: N (0 = infinity)
     uint32_t *d_nwin_work = nullptr;     // k_nwin granule counters (lazy)
     NwinScratch nwin_big;                // k_nwin scratch for windows > kNwinCap (lazy)
+    FrameStats *d_override = nullptr;    // occ_set_frame_stats (lazy), n_override frames
+    int32_t n_override = 0;
     MaskFmt mf{0, 0, 0};                 // occ_set_mask_format
     Params params{};
     std::vector<ViewDesc> views;
@@ -460,6 +462,54 @@ int occ_set_neighbors(occ_ctx *c, int32_t N) {
 
 int32_t occ_get_neighbors(const occ_ctx *c) { return c ? c->neighbors : -1; }
 
+int occ_frame_stats(occ_ctx *c, const float *D, int32_t batch, float *dmin, float *dmax, int32_t *nonfinite,
+                    void *stream) {
+    if (!c || !D || batch < 1 || batch > c->max_batch) return OCC_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    // own scratch: the context's d_stats belong to the last occ_detect (occ_status)
+    FrameStats *st = nullptr;
+    if (cudaMalloc(&st, sizeof(FrameStats) * (size_t)batch) != cudaSuccess) { cudaGetLastError(); return OCC_ERR_OOM; }
+    std::vector<FrameStats> h((size_t)batch);
+    cudaError_t e = launch_stats_init(st, batch, s);
+    if (e == cudaSuccess) e = launch_stats(D, (int64_t)c->H * c->W, batch, st, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), st, sizeof(FrameStats) * h.size(), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(st);
+    if (e != cudaSuccess) return OCC_ERR_CUDA;
+    for (int32_t f = 0; f < batch; ++f) {
+        if (dmin) dmin[f] = key_float(h[(size_t)f].minkey);
+        if (dmax) dmax[f] = key_float(h[(size_t)f].maxkey);
+        if (nonfinite) nonfinite[f] = (int32_t)h[(size_t)f].nonfinite;
+    }
+    return OCC_OK;
+}
+
+int occ_set_frame_stats(occ_ctx *c, const float *dmin, const float *dmax, const int32_t *nonfinite, int32_t n) {
+    if (!c || n < 0 || n > c->max_batch || (n > 0 && (!dmin || !dmax || !nonfinite))) return OCC_ERR_INVALID_ARG;
+    std::vector<FrameStats> h((size_t)n);
+    for (int32_t f = 0; f < n; ++f) {
+        if (!nonfinite[f] && !(dmin[f] <= dmax[f])) return OCC_ERR_INVALID_ARG;
+        h[(size_t)f].minkey = float_key(dmin[f]);
+        h[(size_t)f].maxkey = float_key(dmax[f]);
+        h[(size_t)f].nonfinite = (uint32_t)std::max(0, nonfinite[f]);
+        h[(size_t)f].pad = 0;
+    }
+    CK(cudaSetDevice(c->device));
+    if (n > 0) {
+        if (!c->d_override) {
+            if (cudaMalloc(&c->d_override, sizeof(FrameStats) * (size_t)c->max_batch) != cudaSuccess) {
+                cudaGetLastError();
+                return OCC_ERR_OOM;
+            }
+        }
+        CK(cudaDeviceSynchronize());     // no call in flight may still read the old values
+        CK(cudaMemcpy(c->d_override, h.data(), sizeof(FrameStats) * (size_t)n, cudaMemcpyHostToDevice));
+    }
+    c->n_override = n;
+    return OCC_OK;
+}
+
 }  // extern "C"
 
 namespace {
@@ -478,6 +528,10 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         ProfScope ps(c, OCC_KERNEL_STATS, s);
         CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
                            c->d_stats + c0, c->d_codes, c->code_bytes, s)); ++launches;
+        if (c->n_override > c0)    // imposed whole-frame statistics (spatial sharding)
+            CK(cudaMemcpyAsync(c->d_stats + c0, c->d_override + c0,
+                               sizeof(FrameStats) * (size_t)std::min(n, c->n_override - c0),
+                               cudaMemcpyDeviceToDevice, s));
         ps.end();
     }
     if (c->neighbors > 0) {         // finite N: per-window kernel (masks pre-zeroed)
@@ -536,6 +590,9 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
         {
             ProfScope ps(c, OCC_KERNEL_STATS, s);
             CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
+            if (c->n_override > 0)
+                CK(cudaMemcpyAsync(c->d_stats, c->d_override, sizeof(FrameStats) * (size_t)std::min(batch, c->n_override),
+                                   cudaMemcpyDeviceToDevice, s));
             ps.end();
         }
         ProfScope pd(c, OCC_KERNEL_DIRECT, s);
@@ -736,6 +793,7 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_gq);
     cudaFree(c->d_gq_count);
     cudaFree(c->d_nwin_work);
+    cudaFree(c->d_override);
     cudaFree(c->nwin_big.buf);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);

@@ -28,7 +28,8 @@ PATHS = {"auto": 0, "tiled": 1, "direct": 2}
 EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", "occ_status",
            "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
            "occ_version", "occ_profile", "occ_profile_read", "occ_fuse_median", "occ_set_mask_format",
-           "occ_mask_bytes", "occ_set_neighbors", "occ_get_neighbors"]
+           "occ_mask_bytes", "occ_set_neighbors", "occ_get_neighbors", "occ_frame_stats",
+           "occ_set_frame_stats"]
 MASK_FORMATS = {"u8": 0, "bits": 1}
 KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5, "nwin": 6}
 
@@ -98,6 +99,10 @@ def lib() -> ctypes.CDLL:
         L.occ_set_neighbors.restype = ctypes.c_int
         L.occ_get_neighbors.argtypes = [vp]
         L.occ_get_neighbors.restype = i32
+        L.occ_frame_stats.argtypes = [vp, vp, i32, vp, vp, vp, vp]
+        L.occ_frame_stats.restype = ctypes.c_int
+        L.occ_set_frame_stats.argtypes = [vp, vp, vp, vp, i32]
+        L.occ_set_frame_stats.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -153,6 +158,35 @@ class Detector:
             raise OccError(rc, "occ_set_mask_format")
         self.Wb = (self.W + 31) // 32
         self.set_neighbors(neighbors)
+
+    def frame_stats(self, D, stream=None):
+        """Exact per-frame (dmin, dmax, nonfinite) numpy arrays of device frames
+        D [B, H, W] (occ_frame_stats; synchronises)."""
+        import torch
+        if D.dim() == 2:
+            D = D.unsqueeze(0)
+        assert D.is_cuda and D.dtype == torch.float32 and D.is_contiguous()
+        B = D.shape[0]
+        lo, hi = np.empty(B, np.float32), np.empty(B, np.float32)
+        bad = np.empty(B, np.int32)
+        s = stream if stream is not None else torch.cuda.current_stream(D.device).cuda_stream
+        rc = lib().occ_frame_stats(self._h, D.data_ptr(), B, lo.ctypes.data, hi.ctypes.data, bad.ctypes.data, s)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_frame_stats")
+        return lo, hi, bad
+
+    def set_frame_stats(self, dmin=None, dmax=None, nonfinite=None) -> None:
+        """Impose whole-frame statistics on subsequent calls (occ_set_frame_stats);
+        no arguments: back to the data's own statistics."""
+        if dmin is None:
+            rc = lib().occ_set_frame_stats(self._h, None, None, None, 0)
+        else:
+            lo = np.ascontiguousarray(dmin, np.float32).ravel()
+            hi = np.ascontiguousarray(dmax, np.float32).ravel()
+            bad = np.ascontiguousarray(nonfinite if nonfinite is not None else np.zeros(len(lo)), np.int32).ravel()
+            rc = lib().occ_set_frame_stats(self._h, lo.ctypes.data, hi.ctypes.data, bad.ctypes.data, len(lo))
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_set_frame_stats")
 
     def set_neighbors(self, N: int) -> None:
         """Eq. 5's neighbour count N (0 = infinity; see occ_set_neighbors)."""

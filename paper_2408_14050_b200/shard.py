@@ -29,6 +29,15 @@ def strong_shard(total: int, world: int, rank: int) -> Tuple[int, int]:
     return first, base + (1 if rank < extra else 0)
 
 
+def view_shard(views, world: int, rank: int):
+    """Shard by peripheral view (24 views over 8 GPUs): views
+    are independent once each rank has the whole frame (it recomputes the
+    frame statistics itself, so h is identical everywhere).  Returns rank r's
+    contiguous near-equal block of (index, baseline) pairs."""
+    first, n = strong_shard(len(views), world, rank)
+    return [(i, tuple(views[i])) for i in range(first, first + n)]
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """All-reduce MAX of a per-rank scalar (identity when not distributed)."""
     import torch

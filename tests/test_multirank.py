@@ -76,3 +76,42 @@ def test_two_rank_gloo_shard_gather(tmp_path):
                     for f in range(5)])
     assert got.shape == ref.shape and (got == ref).all()
     assert float((tmp_path / "t.txt").read_text()) == 2.0    # max over ranks
+
+
+def _view_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2408_14050_b200 import scenes
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    views = scenes.config_views(4)                      # 24 views of the 5x5 array
+    D = scenes.make_scene(4)[:64, :96].copy()
+    mine = shard.view_shard(views, world, rank)
+    m = oracle.detect(D, [b for _, b in mine])
+    pad = np.zeros((8, 64, 96), np.uint8)                # 24 views / 3 ranks
+    pad[:len(mine)] = m
+    got = shard.gather_to_rank0(torch.from_numpy(pad))
+    if rank == 0:
+        allm = [g.numpy()[:len(shard.view_shard(views, world, r))] for r, g in enumerate(got)]
+        np.save(os.path.join(out_dir, "views.npy"), np.concatenate(allm))
+    dist.destroy_process_group()
+
+
+def test_view_shards_cover_all_views():
+    from paper_2408_14050_b200 import scenes
+    views = scenes.config_views(4)
+    for world in (1, 2, 3, 8, 24):
+        got = [i for r in range(world) for i, _ in shard.view_shard(views, world, r)]
+        assert got == list(range(24))
+
+
+def test_three_rank_gloo_view_shards(tmp_path):
+    import oracle
+    from paper_2408_14050_b200 import scenes
+    mp.spawn(_view_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    D = scenes.make_scene(4)[:64, :96].copy()
+    ref = oracle.detect(D, scenes.config_views(4))
+    assert (np.load(tmp_path / "views.npy") == ref).all()
