@@ -65,6 +65,8 @@ def lib() -> ctypes.CDLL:
             "bf2_zbuffer": (ctypes.c_int, [f32p, i32, i32, i32, i32, f32, u8p]),
             "orc_fuse_median": (ctypes.c_int, [f32p, i32, ctypes.c_int64, f32p]),
             "orc_count_n": (None, [i32p, f32p, i32p, i32, i32, f32, f32, i32, i32p]),
+            "orc_detect_dirs": (ctypes.c_int, [f32p, i32, i32, f64p, f64p, i32, f32, f32, f32, i32, i32, u8p, i32p]),
+            "orc_dir_offsets": (ctypes.c_int, [ctypes.c_double, i32, i32p, i32p]),
             "orc_detect_range": (ctypes.c_int, [f32p, i32, i32, i32p, i32, f32, f32, f32, i32, i32, f32, f32,
                                                 u8p, i32p]),
             "orc_detect_n": (ctypes.c_int, [f32p, i32, i32, i32p, i32, f32, f32, f32, i32, i32, u8p, i32p]),
@@ -245,3 +247,30 @@ def detect_range(D: np.ndarray, views, dmin: float, dmax: float, t_edge: float =
     if rc != OK:
         raise ValueError(f"orc_detect_range rc={rc}")
     return masks
+
+
+def detect_dirs(D: np.ndarray, dirs, t_edge: float = 1.0, t_dist: float = 2.0, t_disp: float = 0.5,
+                max_scan: int = 4096, neighbors: int = 0, return_info: bool = False):
+    """NEXT #2 (reading Q23): dirs = [(baseline_angle_rad, baseline_length), ...]."""
+    D = np.ascontiguousarray(D, dtype=np.float32)
+    H, W = D.shape
+    phi = np.ascontiguousarray([float(a) for a, _ in dirs], np.float64)
+    rho = np.ascontiguousarray([float(r) for _, r in dirs], np.float64)
+    V = len(dirs)
+    masks = np.zeros((V, H, W), dtype=np.uint8)
+    info = np.zeros((V, 4), dtype=np.int32)
+    rc = lib().orc_detect_dirs(_p(D, ctypes.c_float), H, W, _p(phi, ctypes.c_double), _p(rho, ctypes.c_double), V,
+                               t_edge, t_dist, t_disp, max_scan, int(neighbors), _p(masks, ctypes.c_uint8),
+                               _p(info, ctypes.c_int32))
+    if rc not in (OK, ERR_NONFINITE):
+        raise ValueError(f"orc_detect_dirs rc={rc}")
+    return (masks, info, rc) if return_info else masks
+
+
+def dir_offsets(phi: float, h: int):
+    dx = np.zeros(2 * h + 1, np.int32)
+    dy = np.zeros(2 * h + 1, np.int32)
+    rc = lib().orc_dir_offsets(float(phi), int(h), _p(dx, ctypes.c_int32), _p(dy, ctypes.c_int32))
+    if rc != OK:
+        raise ValueError(f"orc_dir_offsets rc={rc}")
+    return dx, dy

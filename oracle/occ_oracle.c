@@ -368,6 +368,136 @@ static int detect_impl(const float *D, int32_t H, int32_t W, const int32_t *base
 }
 
 /* ---------------------------------------------------------------------------
+ * NEXT #2: real-valued baseline directions (calibrated, non-grid arrays).
+ * A view is a baseline angle phi (radians, image coordinates) and a baseline
+ * length rho (grid units).  Reading Q23:
+ *   Eq. 2: E > t_e (literal fp32, Q4) and the circular
+ *     |Theta - phi| < pi/2, i.e. cos(phi) E_x + sin(phi) E_y > 0, evaluated as
+ *     fl64(fl64(c E_x) + fl64(s E_y)) > 0 with c = cos(phi), s = sin(phi);
+ *   Eq. 4: sample g of candidate C sits at
+ *     C + g u, u = (-c, -s) (displacement = baseline + pi),
+ *     each coordinate rounded half away from zero; samples
+ *     outside the image are dropped, coinciding samples kept;
+ *   Eq. 3: L = min(cap, ceil(fl64(fl64(2 rho) R))), h = floor(L / 2);
+ *   W = g + rho V: w = fl64(g + fl64(rho v)) (Euclidean
+ *     major-axis-free scaling: samples are one pixel apart along u);
+ *   Eq. 5 (prose sign, Q13): delta = fl32(v_q - v_p) > t_disp and
+ *     |dg + fl64(rho delta)| < t_dist, exact on these values;
+ *   sort by (w, index), N = infinity walk or finite N, Eq. 6 OR-marks.
+ * ------------------------------------------------------------------------- */
+static int pair_rho(float vq, float vp, int32_t dg, double rho, float t_dist, float t_disp)
+{
+    float delta = vq - vp;
+    if (!(delta > t_disp)) return 0;
+    double x = rho * (double)delta;                      /* one binary64 rounding */
+    return (x > -(double)t_dist - (double)dg) && (x < (double)t_dist - (double)dg);
+}
+
+int orc_dir_offsets(double phi, int32_t h, int32_t *dx, int32_t *dy)
+{
+    /* offsets of samples g = -h..h (index g + h): round half away from zero
+     * of g u, u = (-cos phi, -sin phi) */
+    if (!isfinite(phi) || h < 0) return ORC_ERR_INVALID_ARG;
+    double ux = -cos(phi), uy = -sin(phi);
+    for (int32_t g = -h; g <= h; ++g) {
+        dx[g + h] = (int32_t)round((double)g * ux);
+        dy[g + h] = (int32_t)round((double)g * uy);
+    }
+    return ORC_OK;
+}
+
+int orc_detect_dirs(const float *D, int32_t H, int32_t W, const double *phi, const double *rho, int32_t V,
+                    float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t N,
+                    uint8_t *masks, int32_t *info)
+{
+    if (H < 2 || W < 2 || H > 32768 || W > 32768 || V < 1 || V > 64 || !phi || !rho) return ORC_ERR_INVALID_ARG;
+    if (!(isfinite(t_edge) && t_edge > 0.0f)) return ORC_ERR_INVALID_ARG;
+    if (!(t_dist >= 0x1p-12f && t_dist <= 0x1p16f)) return ORC_ERR_INVALID_ARG;
+    if (!(t_disp >= 0.0f && t_disp <= 0x1p16f)) return ORC_ERR_INVALID_ARG;
+    if (max_scan < 1 || max_scan > 65536) return ORC_ERR_INVALID_ARG;
+    if (N < 0 || (N > 0 && (N < 2 || (N & 1)))) return ORC_ERR_INVALID_ARG;
+    for (int32_t i = 0; i < V; ++i)
+        if (!isfinite(phi[i]) || !(rho[i] > 0.0 && rho[i] <= 8.0)) return ORC_ERR_INVALID_ARG;
+    const int64_t P = (int64_t)H * W;
+    memset(masks, 0, (size_t)(P * V));
+    if (info) memset(info, 0, sizeof(int32_t) * 4 * (size_t)V);
+    float dmin, dmax;
+    if (orc_stats(D, H, W, &dmin, &dmax) > 0) return ORC_ERR_NONFINITE;   /* O1, Q18 */
+    float *Ex = (float *)malloc(sizeof(float) * (size_t)P);
+    float *Ey = (float *)malloc(sizeof(float) * (size_t)P);
+    float *E = (float *)malloc(sizeof(float) * (size_t)P);
+    orc_edges(D, H, W, Ex, Ey, E);                                     /* O3, O4 */
+    const float R = dmax - dmin;
+    double M = fabs((double)dmin) > fabs((double)dmax) ? fabs((double)dmin) : fabs((double)dmax);
+    for (int32_t vi = 0; vi < V; ++vi) {
+        const double c = cos(phi[vi]), sn = sin(phi[vi]), r = rho[vi];
+        double Ld = ceil((2.0 * r) * (double)R);                        /* O5, Eq. 3 */
+        if (!(Ld <= (double)max_scan)) Ld = (double)max_scan;
+        const int32_t L = (int32_t)Ld, h = L / 2;
+        uint8_t *mask = masks + (int64_t)vi * P;
+        int64_t nc = 0, marked = 0;
+        if (h > 0) {
+            const int32_t cap = 2 * h + 1;
+            int32_t *dx = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
+            int32_t *dy = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
+            int32_t *g = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
+            int32_t *xs = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
+            int32_t *ys = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
+            int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
+            int32_t *O = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
+            float *v = (float *)malloc(sizeof(float) * (size_t)cap);
+            double *w = (double *)malloc(sizeof(double) * (size_t)cap);
+            orc_dir_offsets(phi[vi], h, dx, dy);
+            const double eps = 0x1p-16 * (r * M + 1.0);
+            for (int32_t cy = 0; cy < H; ++cy) {
+                for (int32_t cx = 0; cx < W; ++cx) {
+                    const int64_t ci = (int64_t)cy * W + cx;
+                    /* O6: Eq. 2 */
+                    const double dot = c * (double)Ex[ci] + sn * (double)Ey[ci];
+                    if (!(E[ci] > t_edge && dot > 0.0)) continue;
+                    ++nc;
+                    int32_t n = 0;                                      /* O7: Eq. 4 */
+                    for (int32_t gg = -h; gg <= h; ++gg) {
+                        const int32_t x = cx + dx[gg + h], y = cy + dy[gg + h];
+                        if (x < 0 || x >= W || y < 0 || y >= H) continue;
+                        g[n] = gg; xs[n] = x; ys[n] = y; v[n] = D[(int64_t)y * W + x];
+                        ++n;
+                    }
+                    for (int32_t i = 0; i < n; ++i) w[i] = (double)g[i] + r * (double)v[i];   /* O8 */
+                    orc_sort(w, n, idx);                                /* O9 */
+                    for (int32_t i = 0; i < n; ++i) O[i] = 0;           /* O10 */
+                    for (int32_t i = 0; i < n; ++i) {
+                        const int32_t p = idx[i];
+                        for (int32_t j = i + 1; j < n && (N == 0 || j - i <= N / 2); ++j) {
+                            const int32_t q = idx[j];
+                            if (N == 0 && !(w[q] - w[p] < (double)t_dist + eps)) break;
+                            if (pair_rho(v[q], v[p], g[q] - g[p], r, t_dist, t_disp)) O[p]++;
+                        }
+                        for (int32_t j = i - 1; j >= 0 && (N == 0 || i - j <= N / 2); --j) {
+                            const int32_t q = idx[j];
+                            if (N == 0 && !(w[p] - w[q] < (double)t_dist + eps)) break;
+                            if (pair_rho(v[q], v[p], g[q] - g[p], r, t_dist, t_disp)) O[p]++;
+                        }
+                    }
+                    for (int32_t i = 0; i < n; ++i)                      /* O11: Eq. 6, OR */
+                        if (O[i] > 0) mask[(int64_t)ys[i] * W + xs[i]] = 1;
+                }
+            }
+            free(dx); free(dy); free(g); free(xs); free(ys); free(idx); free(O); free(v); free(w);
+        }
+        for (int64_t i = 0; i < P; ++i) marked += mask[i];
+        if (info) {
+            info[4 * vi + 0] = (int32_t)nc;
+            info[4 * vi + 1] = L;
+            info[4 * vi + 2] = h;
+            info[4 * vi + 3] = (int32_t)marked;
+        }
+    }
+    free(Ex); free(Ey); free(E);
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * NEXT #3: pixel-wise median fusion.
  * Per pixel: copy the K values, insertion-sort them (plain, O(K^2)), take the
  * middle one (odd K) or the fp32 mean of the two middle ones (even K).

@@ -114,6 +114,15 @@ int orc_detect_range(const float *D, int32_t H, int32_t W, const int32_t *baseli
                      float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t N,
                      float dmin, float dmax, uint8_t *masks, int32_t *info);
 
+/* NEXT #2: real-valued baseline directions (reading Q23): view i has baseline
+ * angle phi[i] (radians, finite) and length rho[i] in (0, 8]; N as for
+ * orc_detect_n (0 = infinity).  masks [V][H][W], info as orc_detect. */
+int orc_detect_dirs(const float *D, int32_t H, int32_t W, const double *phi, const double *rho, int32_t V,
+                    float t_edge, float t_dist, float t_disp, int32_t max_scan, int32_t N,
+                    uint8_t *masks, int32_t *info);
+/* Sample offsets of the direction phi: dx, dy [2h + 1] for g = -h..h. */
+int orc_dir_offsets(double phi, int32_t h, int32_t *dx, int32_t *dy);
+
 /* Pixel-wise median fusion of K disparity estimates.
  * PAPER.md:238 (§4.2, "fused to a single disparity map by pixel-wise median
  * filtering"); SPEC.md:51-58 (fuse_median: for even counts the arithmetic
