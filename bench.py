@@ -298,6 +298,45 @@ def gather_leg(d, nf, views, dev, world, rank, steps):
             "note": "torch.distributed.gather (NCCL) of the packed masks of all frames; not in value"}
 
 
+def calibrated_dirs(n=8, jitter=0.05):
+    """A perturbed ring of 8 peripheral cameras (the 3x3 array's directions
+    with +-0.05 rad / +-5 % calibration error; seeded, fixed)."""
+    import math
+    from paper_2408_14050_b200 import scenes
+    rng = scenes.SplitMix64(777)
+    out = []
+    for k in range(n):
+        u = rng.uniform(2)
+        out.append((2 * math.pi * k / n + jitter * (2 * u[0] - 1),
+                    (math.sqrt(2) if k % 2 else 1.0) * (1 + jitter * (2 * u[1] - 1))))
+    return out
+
+
+def dirs_leg(d, masks, nf, args):
+    """Real-valued directions (NEXT #2, occ_create_dirs): the same resident
+    frames with 8 calibrated directions, N = infinity, device-timed."""
+    import torch
+    from paper_2408_14050_b200.occ import Detector
+    dirs = calibrated_dirs()
+    det = Detector(H, W, directions=dirs, max_batch=nf)
+    stream = torch.cuda.current_stream(d.device)
+    for _ in range(3):
+        det.detect(d, out=masks)
+    reps = max(3, min(args.steps, 5))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        det.detect(d, out=masks)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    det.close()
+    pv = nf * H * W * len(dirs)
+    return {"directions": [[round(a, 6), round(r, 6)] for a, r in dirs], "N": "inf", "frames": nf,
+            "ms_per_step": ms, "value": pv / (ms / 1e3) / 1e6, "unit": "MPV/s", "kernel": "k_nwin (directions)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -312,6 +351,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fuse", action="store_true", help="skip the median-fusion leg")
     ap.add_argument("--nwin", type=int, default=8, help="finite-N leg's N (0: skip the leg)")
+    ap.add_argument("--no-dirs", action="store_true", help="skip the real-valued directions leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -443,6 +483,7 @@ def main():
 
     # ---------------- finite-N leg (NEXT #1): N = 8 per-window sort ----------------
     nwin = nwin_leg(d, masks, nf, views, args, peak) if args.nwin > 0 else None
+    dirs = None if args.no_dirs else dirs_leg(d, masks, nf, args)
 
     if rank != 0:
         return
@@ -457,7 +498,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world, nf),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_u8": e2e_u8, "clocks": clk.summary(),
         "gpu_launches": launches, "path": args.path,
-        "fuse_median": fuse, "finite_n": nwin, "mask_gather": gather,
+        "fuse_median": fuse, "finite_n": nwin, "directions": dirs, "mask_gather": gather,
     }
     print(json.dumps(line), flush=True)
 

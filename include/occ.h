@@ -68,6 +68,11 @@ enum {
  * per-pixel kernel (debug / cross-check). */
 enum { OCC_PATH_AUTO = 0, OCC_PATH_TILED = 1, OCC_PATH_DIRECT = 2 };
 
+/* A real-valued peripheral direction (calibrated
+ * non-grid arrays): baseline angle in radians (image coordinates, x right, y
+ * down; the angle of b) and baseline length in grid units, (0, 8]. */
+typedef struct { double baseline_angle, baseline_length; } occ_direction;
+
 /* Fills the paper's defaults. */
 void occ_default_params(occ_params *p);
 
@@ -81,6 +86,19 @@ void occ_default_params(occ_params *p);
  * OCC_ERR_OOM. */
 int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_views,
                const occ_params *params, int32_t max_batch, occ_ctx **out);
+
+/* Context for real-valued directions (reading Q23 of DESIGN.md; PAPER.md:
+ * 103-128 with SPEC.md:179, 241-242): candidates E > t_e and
+ * fl64(cos(phi) E_x) + fl64(sin(phi) E_y) > 0; sample g of candidate C at
+ * C + g u, u = -(cos phi, sin phi), each coordinate rounded half away from
+ * zero (offset tables computed on the host); h = floor(min(cap,
+ * ceil(fl64(2 rho) R)) / 2); W = g + rho V; pair |dg + fl64(rho delta)| <
+ * t_dist and delta > t_disp.  Detection runs the per-window kernel (N =
+ * infinity by default, occ_set_neighbors for finite N); occ_set_path has no
+ * effect.  Same buffers, formats and errors as occ_create (an angle must be
+ * finite, a length in (0, 8]). */
+int occ_create_dirs(int32_t H, int32_t W, const occ_direction *dirs, int32_t n_views,
+                    const occ_params *params, int32_t max_batch, occ_ctx **out);
 
 /* Enqueues detection for `batch` frames.  disparity: device [batch][H][W]
  * fp32; masks: device [batch][n_views][H][W] uint8.  cuda_stream is a

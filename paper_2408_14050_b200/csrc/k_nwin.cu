@@ -60,8 +60,17 @@ struct NwinArgs {
     int64_t ngran, gpf;        // granules total / per frame
     int32_t cap;               // window capacity of the storage this launch uses
     unsigned char *gbuf;       // global scratch (big launch): [warp][cap * kNwinEntryBytes]
-    int32_t smax;              // largest ||b||_inf of the views (longest windows)
+    int32_t smax;              // largest ||b||_inf (ceil of the length) of the views
+    int32_t angles;            // real-valued directions: candidates computed here (Eq. 1-2)
+    const int2 *offs;          // their Eq. 4 offset tables
 };
+
+// Eq. 3 with the W scale rho (rho = s for grid baselines: equal to view_h)
+__device__ __forceinline__ int32_t view_h_rho(float R, double rho, int32_t cap) {
+    double L = ceil(__dmul_rn(__dmul_rn(2.0, rho), (double)R));
+    if (!(L <= (double)cap)) L = (double)cap;
+    return ((int32_t)L) >> 1;
+}
 
 // Per-warp window storage, kNwinEntryBytes per entry: w (binary64), v,
 // sorted index, run starts.  cap is even, so every warp's slice stays
@@ -90,45 +99,70 @@ __device__ __forceinline__ int32_t fdiv(int32_t a, int32_t den) {   // floor(a /
     return den == 1 ? a : (den == 2 ? (a >> 1) : floordiv(a, den));
 }
 
+// Sample g of a candidate's scan window (Eq. 4): grid baselines walk the
+// digital line (S6: major coordinate pc - sg g, orc_scanline's x = cx - sg g,
+// minor line + floor(major num / den)); real-valued directions add the
+// host-computed rounded offset of g u (reading Q23).  false: outside the image.
+struct Geo {
+    int32_t angle, X, sg, num, den, pc, line, nmaj, nmin, cx, cy, W, H;
+    const int2 *off;      // angle: offsets, indexed by g (centred)
+    __device__ __forceinline__ void init(const NwinArgs &a, const ViewDesc &vd, int32_t x, int32_t y) {
+        angle = vd.angle; cx = x; cy = y; W = a.W; H = a.H;
+        X = vd.xmajor; sg = vd.sg; num = vd.num; den = vd.den;
+        pc = X ? x : y;
+        line = angle ? 0 : (X ? y - fdiv(x * num, den) : x - fdiv(y * num, den));
+        nmaj = X ? W : H; nmin = X ? H : W;
+        off = angle ? a.offs + vd.off_base + a.p.max_scan / 2 : nullptr;
+    }
+    __device__ __forceinline__ bool at(int32_t g, int32_t &x, int32_t &y) const {
+        if (angle) {
+            const int2 o = __ldg(off + g);
+            x = cx + o.x; y = cy + o.y;
+            return x >= 0 && x < W && y >= 0 && y < H;
+        }
+        const int32_t mj = pc - sg * g;
+        const int32_t mn = line + fdiv(mj * num, den);
+        x = X ? mj : mn; y = X ? mn : mj;
+        return mj >= 0 && mj < nmaj && mn >= 0 && mn < nmin;
+    }
+};
+
 // One candidate window (warp-cooperative).
 __device__ __forceinline__ void window(const NwinArgs &a, const float *__restrict__ Df, uint8_t *Mv,
                                        const ViewDesc &vd, int32_t h, int32_t cx, int32_t cy,
                                        const WinBuf &B) {
     const int lane = threadIdx.x & 31;
-    // digital line through the candidate (S6): sample g has major coordinate
-    // pc - sg g (orc_scanline: x = cx - sg g) and minor line + floor(major num / den)
-    const int32_t X = vd.xmajor, sg = vd.sg, num = vd.num, den = vd.den, s = vd.s;
-    const int32_t pc = X ? cx : cy;
-    const int32_t line = X ? cy - fdiv(cx * num, den) : cx - fdiv(cy * num, den);
-    const int32_t nmaj = X ? a.W : a.H, nmin = X ? a.H : a.W;
-    // 1. valid extent (the clipped line is one interval of g)
+    Geo geo;
+    geo.init(a, vd, cx, cy);
+    const double rho = vd.rho;          // W = G + rho V (rho = s for grid baselines)
+    // 1. valid extent (the clipped line is one interval of g: the in-image
+    // test of a rounded point moving along a straight line is monotone)
     int32_t glo = INT_MAX, ghi = INT_MIN;
     for (int32_t g0 = -h; g0 <= h; g0 += 32) {
         const int32_t g = g0 + lane;
-        const int32_t mj = pc - sg * g;
-        const int32_t mn = line + fdiv(mj * num, den);
-        if (g <= h && mj >= 0 && mj < nmaj && mn >= 0 && mn < nmin) { glo = min(glo, g); ghi = max(ghi, g); }
+        int32_t xx, yy;
+        if (g <= h && geo.at(g, xx, yy)) { glo = min(glo, g); ghi = max(ghi, g); }
     }
     glo = __reduce_min_sync(0xffffffffu, glo);
     ghi = __reduce_max_sync(0xffffffffu, ghi);
     const int32_t n = ghi - glo + 1;        // >= 1: the candidate itself
-    // 2. V = D on the window, W = fl64(G + s V)
+    // 2. V = D on the window, W = fl64(G + fl64(rho V))
     float vmin = INFINITY, vmax = -INFINITY;
     for (int32_t i0 = 0; i0 < n; i0 += 128) {      // 4 gathers in flight per lane
         float vv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int32_t i = i0 + 32 * u + lane;
-            const int32_t mj = pc - sg * (glo + i);
-            const int32_t mn = line + fdiv(mj * num, den);
-            vv[u] = i < n ? __ldg(Df + (X ? (int64_t)mn * a.W + mj : (int64_t)mj * a.W + mn)) : 0.0f;
+            int32_t xx = 0, yy = 0;
+            if (i < n) geo.at(glo + i, xx, yy);
+            vv[u] = i < n ? __ldg(Df + (int64_t)yy * a.W + xx) : 0.0f;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int32_t i = i0 + 32 * u + lane;
             if (i < n) {
                 B.v[i] = vv[u];
-                B.w[i] = __dadd_rn((double)(glo + i), __dmul_rn((double)s, (double)vv[u]));
+                B.w[i] = __dadd_rn((double)(glo + i), __dmul_rn(rho, (double)vv[u]));
                 vmin = fminf(vmin, vv[u]);
                 vmax = fmaxf(vmax, vv[u]);
             }
@@ -147,9 +181,10 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
     // the rest one binary search.  Inside smooth regions w grows by about 1
     // per sample, so a window has a few runs (one more per depth edge whose
     // near side comes first).  Windows with more than kMaxRuns runs (noise
-    // at s >= 2, random maps) count directly: q with g_q - g_i > s (v_i -
-    // vmin) >= s (v_i - v_q) has exact w_q > w_i, so (rounding is monotone,
-    // ties go by index) key_q > key_i without a comparison; symmetrically below.
+    // at s >= 2, random maps) count directly: q with g_q - g_i >= rho (v_i -
+    // vmin) + 1 >= rho (v_i - v_q) + 1 has w_q > w_i (the exact difference is
+    // >= 1, far above the roundings of w), so key_q > key_i without a
+    // comparison; symmetrically below.
     int32_t m = 0;
     for (int32_t b0 = 0; b0 < n; b0 += 32) {
         const int32_t i = b0 + lane;
@@ -187,8 +222,8 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
         for (int32_t i = lane; i < n; i += 32) {
             const double wi = B.w[i];
             const float vi = B.v[i];
-            const double kd = ceil(__dmul_ru((double)s, __dsub_ru((double)vmax, (double)vi)));
-            const double ku = ceil(__dmul_ru((double)s, __dsub_ru((double)vi, (double)vmin)));
+            const double kd = ceil(__dmul_ru(rho, __dsub_ru((double)vmax, (double)vi))) + 1.0;
+            const double ku = ceil(__dmul_ru(rho, __dsub_ru((double)vi, (double)vmin))) + 1.0;
             const int32_t lo = kd >= (double)i ? 0 : i - (int32_t)kd;
             const int32_t hi = ku >= (double)(n - 1 - i) ? n - 1 : i + (int32_t)ku;
             int32_t rank = lo;
@@ -210,7 +245,7 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
     const int32_t half = a.half;
     const float t_dist = a.p.t_dist, t_disp = a.p.t_disp;
     const double M = fmax(fabs((double)vmin), fabs((double)vmax));
-    const double lim = __dadd_rn((double)t_dist, __dmul_rn(0x1p-16, __dadd_rn(__dmul_rn((double)s, M), 1.0)));
+    const double lim = __dadd_rn((double)t_dist, __dmul_rn(0x1p-16, __dadd_rn(__dmul_rn(rho, M), 1.0)));
     int32_t *hit = B.run;
     for (int32_t r = lane; r < n; r += 32) hit[r] = 0;
     __syncwarp();
@@ -229,7 +264,7 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
                 if (near) {
                     const float delta = __fsub_rn(B.v[iq], vp);
                     const int32_t dk = iq - ip;                        // g_q - g_p
-                    const double x = __dmul_rn((double)s, (double)delta);
+                    const double x = __dmul_rn(rho, (double)delta);
                     if (x > __dsub_rn(-(double)t_dist, (double)dk) && x < __dsub_rn((double)t_dist, (double)dk)) {
                         if (delta > t_disp) hp = true;                 // p behind q
                         else if (-delta > t_disp) hit[rq] = 1;         // q behind p
@@ -244,9 +279,9 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
     __syncwarp();
     for (int32_t r = lane; r < n; r += 32) {
         if (!hit[r]) continue;                                           // Eq. 6
-        const int32_t mj = pc - sg * (glo + B.s[r]);
-        const int32_t mn = line + fdiv(mj * num, den);
-        mask_put(Mv, a.mf, a.W, X ? mj : mn, X ? mn : mj, true);
+        int32_t xx, yy;
+        geo.at(glo + B.s[r], xx, yy);
+        mask_put(Mv, a.mf, a.W, xx, yy, true);
     }
     __syncwarp();
 }
@@ -283,14 +318,33 @@ __global__ void __launch_bounds__(32 * kNwinWarps) k_nwin(NwinArgs a) {
         const float *Df = a.D + (int64_t)f * HW;
         for (int32_t sub = 0; sub < kGran; sub += 32) {
             const int64_t pix = p0 + sub + lane;
-            const uint32_t code = pix < HW ? load_code(a.codes, a.code_bytes, (int64_t)f * HW + pix) : 0u;
+            uint32_t code = 0u;
+            float ex = 0.0f, ey = 0.0f;
+            if (a.angles) {
+                // real-valued directions: Eq. 1 and E > t_e here (the squared
+                // exact threshold, as K0), the direction test per view below
+                if (pix < HW) {
+                    const int32_t y = (int32_t)(pix / a.W), x = (int32_t)(pix - (int64_t)y * a.W);
+                    const float c = __ldg(Df + pix);
+                    ex = x + 1 < a.W ? __fsub_rn(__ldg(Df + pix + 1), c) : 0.0f;
+                    ey = y + 1 < a.H ? __fsub_rn(__ldg(Df + pix + a.W), c) : 0.0f;
+                    code = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)) > a.p.e2_thresh ? 1u : 0u;
+                }
+            } else {
+                code = pix < HW ? load_code(a.codes, a.code_bytes, (int64_t)f * HW + pix) : 0u;
+            }
             if (__ballot_sync(0xffffffffu, code != 0u) == 0u) continue;
             for (int32_t vi = 0; vi < a.nviews; ++vi) {
                 const ViewDesc &vd = a.views[vi];
-                const int32_t h = view_h(R, vd.s, a.p.max_scan);
+                const int32_t h = view_h_rho(R, vd.rho, a.p.max_scan);
                 if (h <= 0) continue;                   // Q17: no window, no marks
                 if ((2 * h + 1 > kNwinCap) != kBig) continue;   // the other launch's window
-                uint32_t cand = __ballot_sync(0xffffffffu, (code >> vd.candbit) & 1u);
+                // Eq. 2: grid baselines from the K0 codes; directions as
+                // fl64(cos phi E_x) + fl64(sin phi E_y) > 0 (reading Q23)
+                const bool isc = a.angles ? (code != 0u && __dadd_rn(__dmul_rn(vd.ca, (double)ex),
+                                                                     __dmul_rn(vd.sa, (double)ey)) > 0.0)
+                                          : ((code >> vd.candbit) & 1u) != 0u;
+                uint32_t cand = __ballot_sync(0xffffffffu, isc);
                 uint8_t *Mv = a.masks + ((int64_t)f * a.nviews + vi) * a.mf.vbytes;
                 while (cand) {
                     const int b = __ffs(cand) - 1;
@@ -311,12 +365,16 @@ size_t nwin_smem_bytes() { return (size_t)kNwinWarps * kNwinCap * kNwinEntryByte
 cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, const ViewDesc *views,
                         int32_t nviews, const FrameStats *st, const Params &p, int32_t N, uint8_t *masks,
                         const MaskFmt &mf, const void *codes, int32_t code_bytes, uint32_t *work,
-                        NwinScratch &big, int32_t smax, int32_t nsm, cudaStream_t s) {
+                        NwinScratch &big, int32_t smax, int32_t angles, const int2 *offs, int32_t nsm,
+                        cudaStream_t s) {
     NwinArgs a{};
     a.smax = smax;
+    a.angles = angles;
+    a.offs = offs;
     a.D = D; a.H = H; a.W = W; a.frames = frames;
     a.codes = codes; a.code_bytes = code_bytes;
-    a.views = views; a.nviews = nviews; a.st = st; a.p = p; a.half = N / 2;
+    a.views = views; a.nviews = nviews; a.st = st; a.p = p;
+    a.half = N > 0 ? N / 2 : (1 << 30);     // N = 0: infinity (every pair within t_dist + eps)
     a.masks = masks; a.mf = mf;
     a.gpf = ((int64_t)H * W + kGran - 1) / kGran;
     a.ngran = a.gpf * frames;

@@ -20,6 +20,8 @@ struct occ_ctx {
     int32_t H = 0, W = 0, V = 0, nfam = 0, max_batch = 0, device = 0;
     int32_t path = OCC_PATH_AUTO;
     int32_t neighbors = 0;               // occ_set_neighbors: N (0 = infinity)
+    int32_t angles = 0;                  // occ_create_dirs context: real-valued directions
+    int2 *d_offs = nullptr;              // their Eq. 4 offset tables [V][2 (max_scan/2) + 1]
     uint32_t *d_nwin_work = nullptr;     // k_nwin granule counters (lazy)
     NwinScratch nwin_big;                // k_nwin scratch for windows > kNwinCap (lazy)
     FrameStats *d_override = nullptr;    // occ_set_frame_stats (lazy), n_override frames
@@ -318,6 +320,81 @@ const char *occ_strerror(int code) {
     }
 }
 
+// Device side of a context whose views (and families) are set up: work
+// lists, chunking, device copies, offset tables.  Frees c on failure.
+int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_batch, occ_ctx **out) {
+    c->nfam = (int32_t)c->fams.size();
+    build_tiles(c);
+    c->code_bytes = c->nfam <= 4 ? 1 : (c->nfam <= 8 ? 2 : 4);
+    {   // frames per K0/K1 chunk (measured: 48 MiB 54.6 ms/step, 96 MiB 51.7,
+        // 160-640 MiB 50.3-50.6 at C5)
+        const double per = (double)H * W * (4.0 + c->code_bytes);
+        const char *ev = getenv("OCC_CHUNK_MIB");          // tuning knob (default 256 MiB)
+        const double budget = (ev ? std::max(1, atoi(ev)) : 256) * 1048576.0;
+        c->chunk = (int32_t)std::max(1.0, std::min(64.0, std::floor(budget / per)));
+        c->chunk = std::min(c->chunk, max_batch);
+    }
+
+    if (cudaGetDevice(&c->device) != cudaSuccess) { cudaGetLastError(); delete c; return OCC_ERR_CUDA; }
+    if (cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess) c->nsm = 148;
+    if (cudaMalloc(&c->d_views, sizeof(ViewDesc) * c->views.size()) != cudaSuccess ||
+        cudaMalloc(&c->d_fams, sizeof(FamilyDesc) * c->fams.size()) != cudaSuccess ||
+        cudaMalloc(&c->d_groups, sizeof(GroupDesc) * c->groups.size()) != cudaSuccess ||
+        cudaMalloc(&c->d_tiles, sizeof(TileDesc) * std::max<size_t>(1, c->tiles.size())) != cudaSuccess ||
+        cudaMalloc(&c->d_all_tiles, sizeof(TileDesc) * std::max<size_t>(1, c->all_tiles.size())) != cudaSuccess ||
+        cudaMalloc(&c->d_units, sizeof(LineUnit) * std::max<size_t>(1, c->units.size())) != cudaSuccess ||
+        cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess ||
+        cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
+        (!c->units.empty() &&
+         (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = (int32_t)std::min<double>(
+              16.0 * 1048576.0, std::max(65536.0, (double)c->chunk * H * W * n_views / 64.0)))) != cudaSuccess ||
+          cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess))) {
+        cudaGetLastError();
+        occ_destroy(c);
+        return OCC_ERR_OOM;
+    }
+    if (cudaMemcpy(c->d_views, c->views.data(), sizeof(ViewDesc) * c->views.size(),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_fams, c->fams.data(), sizeof(FamilyDesc) * c->fams.size(),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_groups, c->groups.data(), sizeof(GroupDesc) * c->groups.size(),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        (c->tiles.size() && cudaMemcpy(c->d_tiles, c->tiles.data(), sizeof(TileDesc) * c->tiles.size(),
+                                       cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (c->all_tiles.size() && cudaMemcpy(c->d_all_tiles, c->all_tiles.data(),
+                                           sizeof(TileDesc) * c->all_tiles.size(),
+                                           cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (c->units.size() && cudaMemcpy(c->d_units, c->units.data(), sizeof(LineUnit) * c->units.size(),
+                                       cudaMemcpyHostToDevice) != cudaSuccess)) {
+        occ_destroy(c);
+        return OCC_ERR_CUDA;
+    }
+    if (c->angles && cudaMalloc(&c->d_nwin_work, 2 * sizeof(uint32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        occ_destroy(c);
+        return OCC_ERR_OOM;
+    }
+    if (c->angles) {   // Eq. 4 sample offsets of every direction, |g| <= max_scan / 2
+        const int32_t hc = c->params.max_scan / 2, n = 2 * hc + 1;
+        std::vector<int2> off((size_t)n * c->V);
+        for (int32_t v = 0; v < c->V; ++v) {
+            const ViewDesc &vd = c->views[(size_t)v];
+            for (int32_t g = -hc; g <= hc; ++g) {
+                // round half away from zero of g u, u = (-cos phi, -sin phi) (reading Q23)
+                off[(size_t)v * n + (g + hc)] = make_int2((int32_t)std::round((double)g * vd.ux),
+                                                          (int32_t)std::round((double)g * vd.uy));
+            }
+        }
+        if (cudaMalloc(&c->d_offs, sizeof(int2) * off.size()) != cudaSuccess) { cudaGetLastError(); occ_destroy(c); return OCC_ERR_OOM; }
+        if (cudaMemcpy(c->d_offs, off.data(), sizeof(int2) * off.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            occ_destroy(c);
+            return OCC_ERR_CUDA;
+        }
+    }
+    *out = c;
+    return OCC_OK;
+}
+
 int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_views,
                const occ_params *params, int32_t max_batch, occ_ctx **out) {
     if (!out) return OCC_ERR_INVALID_ARG;
@@ -374,56 +451,52 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
         vd.fam = fam;
         vd.candbit = 2 * fam + (vd.sg < 0 ? 1 : 0);
         near_far(vd, p);
+        vd.rho = (double)vd.s;
         c->views.push_back(vd);
     }
-    c->nfam = (int32_t)c->fams.size();
-    build_tiles(c);
-    c->code_bytes = c->nfam <= 4 ? 1 : (c->nfam <= 8 ? 2 : 4);
-    {   // frames per K0/K1 chunk (measured: 48 MiB 54.6 ms/step, 96 MiB 51.7,
-        // 160-640 MiB 50.3-50.6 at C5)
-        const double per = (double)H * W * (4.0 + c->code_bytes);
-        const char *ev = getenv("OCC_CHUNK_MIB");          // tuning knob (default 256 MiB)
-        const double budget = (ev ? std::max(1, atoi(ev)) : 256) * 1048576.0;
-        c->chunk = (int32_t)std::max(1.0, std::min(64.0, std::floor(budget / per)));
-        c->chunk = std::min(c->chunk, max_batch);
-    }
+    return create_tail(c, H, W, n_views, max_batch, out);
+}
 
-    if (cudaGetDevice(&c->device) != cudaSuccess) { cudaGetLastError(); delete c; return OCC_ERR_CUDA; }
-    if (cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess) c->nsm = 148;
-    if (cudaMalloc(&c->d_views, sizeof(ViewDesc) * c->views.size()) != cudaSuccess ||
-        cudaMalloc(&c->d_fams, sizeof(FamilyDesc) * c->fams.size()) != cudaSuccess ||
-        cudaMalloc(&c->d_groups, sizeof(GroupDesc) * c->groups.size()) != cudaSuccess ||
-        cudaMalloc(&c->d_tiles, sizeof(TileDesc) * std::max<size_t>(1, c->tiles.size())) != cudaSuccess ||
-        cudaMalloc(&c->d_all_tiles, sizeof(TileDesc) * std::max<size_t>(1, c->all_tiles.size())) != cudaSuccess ||
-        cudaMalloc(&c->d_units, sizeof(LineUnit) * std::max<size_t>(1, c->units.size())) != cudaSuccess ||
-        cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess ||
-        cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
-        (!c->units.empty() &&
-         (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = (int32_t)std::min<double>(
-              16.0 * 1048576.0, std::max(65536.0, (double)c->chunk * H * W * n_views / 64.0)))) != cudaSuccess ||
-          cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess))) {
-        cudaGetLastError();
-        occ_destroy(c);
-        return OCC_ERR_OOM;
+int occ_create_dirs(int32_t H, int32_t W, const occ_direction *dirs, int32_t n_views,
+                    const occ_params *params, int32_t max_batch, occ_ctx **out) {
+    if (!out) return OCC_ERR_INVALID_ARG;
+    *out = nullptr;
+    occ_params p;
+    occ_default_params(&p);
+    if (params) p = *params;
+    if (H < 2 || W < 2 || H > 32768 || W > 32768 || n_views < 1 || !dirs || max_batch < 1) return OCC_ERR_INVALID_ARG;
+    if (n_views > kMaxViews) return OCC_ERR_UNSUPPORTED;
+    if (!(std::isfinite(p.t_edge) && p.t_edge > 0.0f) || !(p.t_dist >= 0x1p-12f && p.t_dist <= 0x1p16f) ||
+        !(p.t_disp >= 0.0f && p.t_disp <= 0x1p16f) || p.max_scan < 1 || p.max_scan > 65536)
+        return OCC_ERR_INVALID_ARG;
+    for (int32_t i = 0; i < n_views; ++i)
+        if (!std::isfinite(dirs[i].baseline_angle) || !(dirs[i].baseline_length > 0.0 && dirs[i].baseline_length <= 8.0))
+            return OCC_ERR_INVALID_ARG;
+    occ_ctx *c = new (std::nothrow) occ_ctx();
+    if (!c) return OCC_ERR_OOM;
+    c->H = H; c->W = W; c->V = n_views; c->max_batch = max_batch;
+    c->mf.packed = 0; c->mf.Wb = (W + 31) / 32; c->mf.vbytes = (int64_t)H * W;
+    c->params.t_edge = p.t_edge;
+    c->params.t_dist = p.t_dist;
+    c->params.t_disp = p.t_disp;
+    c->params.max_scan = p.max_scan;
+    c->params.e2_thresh = sqrt_thresh(p.t_edge);
+    c->angles = 1;
+    for (int32_t i = 0; i < n_views; ++i) {
+        ViewDesc vd{};
+        vd.angle = 1;
+        vd.ca = std::cos(dirs[i].baseline_angle);       // Eq. 2 direction (reading Q23)
+        vd.sa = std::sin(dirs[i].baseline_angle);
+        vd.ux = -vd.ca;                                 // displacement = baseline + pi
+        vd.uy = -vd.sa;
+        vd.rho = dirs[i].baseline_length;
+        vd.s = (int32_t)std::ceil(vd.rho);
+        vd.off_base = i * (2 * (p.max_scan / 2) + 1);
+        vd.fam = -1;
+        vd.candbit = 31;
+        c->views.push_back(vd);
     }
-    if (cudaMemcpy(c->d_views, c->views.data(), sizeof(ViewDesc) * c->views.size(),
-                   cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(c->d_fams, c->fams.data(), sizeof(FamilyDesc) * c->fams.size(),
-                   cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(c->d_groups, c->groups.data(), sizeof(GroupDesc) * c->groups.size(),
-                   cudaMemcpyHostToDevice) != cudaSuccess ||
-        (c->tiles.size() && cudaMemcpy(c->d_tiles, c->tiles.data(), sizeof(TileDesc) * c->tiles.size(),
-                                       cudaMemcpyHostToDevice) != cudaSuccess) ||
-        (c->all_tiles.size() && cudaMemcpy(c->d_all_tiles, c->all_tiles.data(),
-                                           sizeof(TileDesc) * c->all_tiles.size(),
-                                           cudaMemcpyHostToDevice) != cudaSuccess) ||
-        (c->units.size() && cudaMemcpy(c->d_units, c->units.data(), sizeof(LineUnit) * c->units.size(),
-                                       cudaMemcpyHostToDevice) != cudaSuccess)) {
-        occ_destroy(c);
-        return OCC_ERR_CUDA;
-    }
-    *out = c;
-    return OCC_OK;
+    return create_tail(c, H, W, n_views, max_batch, out);
 }
 
 int occ_set_mask_format(occ_ctx *c, int32_t format) {
@@ -515,7 +588,7 @@ int occ_set_frame_stats(occ_ctx *c, const float *dmin, const float *dmax, const 
 namespace {
 int32_t smax_of(const occ_ctx *c) {
     int32_t m = 1;
-    for (const ViewDesc &v : c->views) m = std::max(m, v.s);
+    for (const ViewDesc &v : c->views) m = std::max(m, (int32_t)std::ceil(v.rho));
     return m;
 }
 
@@ -534,10 +607,11 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
                                cudaMemcpyDeviceToDevice, s));
         ps.end();
     }
-    if (c->neighbors > 0) {         // finite N: per-window kernel (masks pre-zeroed)
+    if (c->neighbors > 0 || c->angles) {   // finite N / real directions: per-window kernel (masks pre-zeroed)
         ProfScope pn(c, OCC_KERNEL_NWIN, s);
         CK(launch_nwin(Dc, c->H, c->W, n, c->d_views, c->V, c->d_stats + c0, c->params, c->neighbors, Mc,
-                       c->mf, c->d_codes, c->code_bytes, c->d_nwin_work, c->nwin_big, smax_of(c), c->nsm, s));
+                       c->mf, c->d_codes, c->code_bytes, c->d_nwin_work, c->nwin_big, smax_of(c), c->angles,
+                       c->d_offs, c->nsm, s));
         launches += 2 * c->params.max_scan / 2 + 1 > kNwinCap ? 2 : 1;
         pn.end();
         return OCC_OK;
@@ -579,14 +653,14 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
     CK(cudaSetDevice(c->device));
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
-    if (c->mf.packed || c->neighbors > 0)   // packed planes / finite N: kernels set marks only
+    if (c->mf.packed || c->neighbors > 0 || c->angles)   // packed / finite N / directions: kernels set marks only
         CK(cudaMemsetAsync(M, 0, (size_t)batch * c->V * c->mf.vbytes, s));
     {
         ProfScope ps(c, OCC_KERNEL_INIT, s);
         CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
         ps.end();
     }
-    if (c->path == OCC_PATH_DIRECT && c->neighbors == 0) {
+    if (c->path == OCC_PATH_DIRECT && c->neighbors == 0 && !c->angles) {
         {
             ProfScope ps(c, OCC_KERNEL_STATS, s);
             CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;
@@ -636,7 +710,7 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
     // pipeline granularity: ~64 MiB of D per copy (finer than the device-side
     // chunk, so the first H2D and the last D2H expose little of the step)
     const int32_t pipe = (int32_t)std::max<int64_t>(1, ((int64_t)64 << 20) / (int64_t)(HW * sizeof(float)));
-    const bool direct = c->path == OCC_PATH_DIRECT && c->neighbors == 0;
+    const bool direct = c->path == OCC_PATH_DIRECT && c->neighbors == 0 && !c->angles;
     const int32_t chunk = direct ? batch : std::min(c->chunk, pipe);
     const int32_t nchunks = (batch + chunk - 1) / chunk;
     while ((int32_t)c->ev_pipe.size() < 2 * nchunks + 1) {
@@ -654,7 +728,7 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
         CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
         ps.end();
     }
-    if ((c->mf.packed || c->neighbors > 0) && !direct)
+    if ((c->mf.packed || c->neighbors > 0 || c->angles) && !direct)
         CK(cudaMemsetAsync(c->d_stage_M, 0, (size_t)batch * c->V * c->mf.vbytes, s));
     for (int32_t i = 0; i < nchunks; ++i) {
         const int32_t c0 = i * chunk, n = std::min(chunk, batch - c0);
@@ -707,7 +781,7 @@ int occ_frame_info(occ_ctx *c, int32_t frame, float *dmin, float *dmax, int32_t 
     if (h_per_view) {
         const float R = hi - lo;
         for (int32_t v = 0; v < c->V; ++v) {
-            double L = std::ceil(2.0 * (double)c->views[v].s * (double)R);
+            double L = std::ceil((2.0 * c->views[v].rho) * (double)R);
             if (!(L <= (double)c->params.max_scan)) L = c->params.max_scan;
             h_per_view[v] = fs.nonfinite ? 0 : ((int32_t)L) / 2;
         }
@@ -794,6 +868,7 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_gq_count);
     cudaFree(c->d_nwin_work);
     cudaFree(c->d_override);
+    cudaFree(c->d_offs);
     cudaFree(c->nwin_big.buf);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);

@@ -31,6 +31,13 @@ struct ViewDesc {
     // exact fp32 thresholds: delta in (lo, hi) <=> Eq. 5 test holds
     float back_lo[kMaxNear], back_hi[kMaxNear];   // dk = -j, j = 1..nback
     float fwd_lo[kMaxNear], fwd_hi[kMaxNear];     // dk = +f, f = 1..nfwd
+    // W scaling (Eq. 4 / W): rho = s for grid baselines, the Euclidean length
+    // for real-valued directions (occ_create_dirs, reading Q23)
+    double rho;
+    int32_t angle;      // 1: real-valued direction (k_nwin only)
+    int32_t off_base;   // its offset table: entries [off_base, off_base + 2 (max_scan / 2) + 1)
+    double ca, sa;      // cos / sin of the baseline angle (Eq. 2)
+    double ux, uy;      // displacement unit vector (-ca, -sa)
 };
 
 struct FamilyDesc {
@@ -164,7 +171,8 @@ size_t nwin_smem_bytes();
 cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, const ViewDesc *views,
                         int32_t nviews, const FrameStats *st, const Params &p, int32_t N, uint8_t *masks,
                         const MaskFmt &mf, const void *codes, int32_t code_bytes, uint32_t *work,
-                        NwinScratch &big, int32_t smax, int32_t nsm, cudaStream_t s);
+                        NwinScratch &big, int32_t smax, int32_t angles, const int2 *offs, int32_t nsm,
+                        cudaStream_t s);
 cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
                             const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
                             FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s);

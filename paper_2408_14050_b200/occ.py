@@ -29,13 +29,17 @@ EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", 
            "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
            "occ_version", "occ_profile", "occ_profile_read", "occ_fuse_median", "occ_set_mask_format",
            "occ_mask_bytes", "occ_set_neighbors", "occ_get_neighbors", "occ_frame_stats",
-           "occ_set_frame_stats"]
+           "occ_set_frame_stats", "occ_create_dirs"]
 MASK_FORMATS = {"u8": 0, "bits": 1}
 KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5, "nwin": 6}
 
 
 class occ_baseline(ctypes.Structure):
     _fields_ = [("bx", ctypes.c_int32), ("by", ctypes.c_int32)]
+
+
+class occ_direction(ctypes.Structure):
+    _fields_ = [("baseline_angle", ctypes.c_double), ("baseline_length", ctypes.c_double)]
 
 
 class occ_params(ctypes.Structure):
@@ -99,6 +103,8 @@ def lib() -> ctypes.CDLL:
         L.occ_set_neighbors.restype = ctypes.c_int
         L.occ_get_neighbors.argtypes = [vp]
         L.occ_get_neighbors.restype = i32
+        L.occ_create_dirs.argtypes = [i32, i32, vp, i32, vp, i32, vp]
+        L.occ_create_dirs.restype = ctypes.c_int
         L.occ_frame_stats.argtypes = [vp, vp, i32, vp, vp, vp, vp]
         L.occ_frame_stats.restype = ctypes.c_int
         L.occ_set_frame_stats.argtypes = [vp, vp, vp, vp, i32]
@@ -131,6 +137,16 @@ def create_raw(H: int, W: int, baselines: Sequence[Tuple[int, int]], params: Opt
     return rc, (h.value if rc == OCC_OK else None)
 
 
+def create_dirs_raw(H: int, W: int, dirs, params: Optional[occ_params], max_batch: int = 1):
+    """Call occ_create_dirs with [(baseline_angle, baseline_length), ...]."""
+    arr = (occ_direction * max(1, len(dirs)))(*[occ_direction(float(a), float(r)) for a, r in dirs])
+    h = ctypes.c_void_p()
+    rc = lib().occ_create_dirs(int(H), int(W), ctypes.addressof(arr) if len(dirs) else None, len(dirs),
+                               ctypes.addressof(params) if params is not None else None, int(max_batch),
+                               ctypes.addressof(h))
+    return rc, (h.value if rc == OCC_OK else None)
+
+
 class Detector:
     """``Detector(H, W, baselines).detect(D)`` -> uint8 masks [B, V, H, W].
 
@@ -138,17 +154,31 @@ class Detector:
     is enqueued on the current torch CUDA stream and does not synchronise.
     """
 
-    def __init__(self, H: int, W: int, baselines: Sequence[Tuple[int, int]], t_edge: float = 1.0,
+    def __init__(self, H: int, W: int, baselines: Optional[Sequence[Tuple[int, int]]] = None, t_edge: float = 1.0,
                  t_dist: float = 2.0, t_disp: float = 0.5, max_scan: int = 4096, max_batch: int = 1,
-                 path: str = "auto", mask_format: str = "u8", neighbors: int = 0):
+                 path: str = "auto", mask_format: str = "u8", neighbors: int = 0,
+                 directions: Optional[Sequence[Tuple[float, float]]] = None):
+        """baselines: integer grid offsets (occ_create); or directions:
+        [(baseline_angle_rad, baseline_length), ...] (occ_create_dirs, NEXT #2)."""
         self.H, self.W = int(H), int(W)
-        self.baselines: List[Tuple[int, int]] = [(int(a), int(b)) for a, b in baselines]
-        self.V = len(self.baselines)
         self.max_batch = int(max_batch)
         p = occ_params(t_edge, t_dist, t_disp, max_scan)
-        rc, h = create_raw(self.H, self.W, self.baselines, p, self.max_batch)
+        if (baselines is None) == (directions is None):
+            raise ValueError("give exactly one of baselines / directions")
+        if directions is not None:
+            self.directions = [(float(a), float(r)) for a, r in directions]
+            self.baselines = []
+            self.V = len(self.directions)
+            rc, h = create_dirs_raw(self.H, self.W, self.directions, p, self.max_batch)
+            what = "occ_create_dirs"
+        else:
+            self.directions = None
+            self.baselines: List[Tuple[int, int]] = [(int(a), int(b)) for a, b in baselines]
+            self.V = len(self.baselines)
+            rc, h = create_raw(self.H, self.W, self.baselines, p, self.max_batch)
+            what = "occ_create"
         if rc != OCC_OK:
-            raise OccError(rc, "occ_create")
+            raise OccError(rc, what)
         self._h = h
         self._last_batch = 0
         self.set_path(path)
