@@ -326,12 +326,14 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
     c->nfam = (int32_t)c->fams.size();
     build_tiles(c);
     c->code_bytes = c->nfam <= 4 ? 1 : (c->nfam <= 8 ? 2 : 4);
-    {   // frames per K0/K1 chunk (measured: 48 MiB 54.6 ms/step, 96 MiB 51.7,
-        // 160-640 MiB 50.3-50.6 at C5)
+    {   // frames per K0/K1 chunk.  With frame-major k_line the chunk only
+        // sets the launch count (L2 locality is per frame); measured at C5:
+        // 256 MiB (25 frames) 53.1 ms/step, 1 GiB 51.5, 2 GiB (207 frames)
+        // 51.3, 4 GiB (one launch) 52.4
         const double per = (double)H * W * (4.0 + c->code_bytes);
-        const char *ev = getenv("OCC_CHUNK_MIB");          // tuning knob (default 256 MiB)
-        const double budget = (ev ? std::max(1, atoi(ev)) : 256) * 1048576.0;
-        c->chunk = (int32_t)std::max(1.0, std::min(64.0, std::floor(budget / per)));
+        const char *ev = getenv("OCC_CHUNK_MIB");          // tuning knob (default 2 GiB)
+        const double budget = (ev ? std::max(1, atoi(ev)) : 2048) * 1048576.0;
+        c->chunk = (int32_t)std::max(1.0, std::min(1024.0, std::floor(budget / per)));
         c->chunk = std::min(c->chunk, max_batch);
     }
 

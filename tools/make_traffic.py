@@ -22,13 +22,13 @@ def dram(rep):
     return tot, v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
 
 
-frames = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+frames = int(sys.argv[3]) if len(sys.argv) > 3 else 207   # first chunk at the default 2 GiB
 parts = [dram(r) for r in sys.argv[1:3]]
 H, W, V = 1080, 1920, 8
 res = {"kernel": "line", "bytes_per_launch": sum(p[0] for p in parts),
        "alg_bytes_per_launch": frames * H * W * (4 + V),
        "parts": {p[1][:60]: p[0] for p in parts},
-       "source": "ncu --set full --clock-control none, one 25-frame C5 chunk (bench --steps 2 --warmup 3)"}
+       "source": f"ncu --set full --clock-control none, one {frames}-frame C5 chunk (bench --steps 2 --warmup 3)"}
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 with open(os.path.join(root, "profiles", "ncu_traffic.json"), "w") as f:
     json.dump(res, f, indent=1)
