@@ -1168,7 +1168,7 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
     static int nw = 0;
     if (!nw) {
         const char *ev = getenv("OCC_LINE_WARPS");
-        nw = ev ? max(1, min(4, atoi(ev))) : 2;
+        nw = ev ? max(1, min(4, atoi(ev))) : 4;
     }
     dim3 grid((unsigned)((a.nwork + nw - 1) / nw));
     const size_t smem = WSMEM * (size_t)nw;
@@ -1178,7 +1178,7 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
     static int carve = -2;
     if (carve == -2) {
         const char *ev = getenv("OCC_LINE_CARVEOUT");
-        carve = ev ? atoi(ev) : 60;
+        carve = ev ? atoi(ev) : 50;
     }
     if (code_bytes == 1) {
         e = cudaFuncSetAttribute(k_line<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
