@@ -337,6 +337,64 @@ def dirs_leg(d, masks, nf, args):
             "ms_per_step": ms, "value": pv / (ms / 1e3) / 1e6, "unit": "MPV/s", "kernel": "k_nwin (directions)"}
 
 
+def small_leg():
+    """Launch-bound small configs (C1, C2 "launch-bound; use CUDA
+    graphs and report both"): per-frame device latency of occ_detect issued
+    directly vs replayed from a captured CUDA graph, and the masks of a replay
+    checked against the direct call."""
+    import torch
+    from paper_2408_14050_b200 import scenes
+    from paper_2408_14050_b200.occ import Detector
+    res = {}
+    for cfg in (1, 2, 3):
+        D = scenes.make_scene(cfg)
+        views = scenes.config_views(cfg)
+        h, w = D.shape
+        d = torch.from_numpy(D).cuda()[None]
+        det = Detector(h, w, views)
+        out = det.detect(d)
+        ref = out.clone()
+        reps = 200 if cfg < 3 else 50
+        st = torch.cuda.Stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(st):
+            for _ in range(10):
+                det.detect(d, out=out)
+            e0.record(st)
+            for _ in range(reps):
+                det.detect(d, out=out)
+            e1.record(st)
+        torch.cuda.synchronize()
+        direct_us = e0.elapsed_time(e1) / reps * 1e3
+        entry = {"H": h, "W": w, "views": len(views), "direct_us": direct_us,
+                 "direct_mpvs": h * w * len(views) / direct_us}
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                det.detect(d, out=out)
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            entry["graph_matches_direct"] = bool(torch.equal(out, ref))
+            with torch.cuda.stream(st):
+                for _ in range(10):
+                    g.replay()
+                e0.record(st)
+                for _ in range(reps):
+                    g.replay()
+                e1.record(st)
+            torch.cuda.synchronize()
+            entry["graph_us"] = e0.elapsed_time(e1) / reps * 1e3
+            entry["graph_mpvs"] = h * w * len(views) / entry["graph_us"]
+            del g
+        except Exception as ex:   # reported, never fatal
+            entry["graph_error"] = f"{type(ex).__name__}: {ex}"[:200]
+        det.close()
+        res[f"C{cfg}"] = entry
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -352,6 +410,7 @@ def main():
     ap.add_argument("--no-fuse", action="store_true", help="skip the median-fusion leg")
     ap.add_argument("--nwin", type=int, default=8, help="finite-N leg's N (0: skip the leg)")
     ap.add_argument("--no-dirs", action="store_true", help="skip the real-valued directions leg")
+    ap.add_argument("--no-small", action="store_true", help="skip the C1-C3 latency / CUDA-graph leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -484,6 +543,7 @@ def main():
     # ---------------- finite-N leg (NEXT #1): N = 8 per-window sort ----------------
     nwin = nwin_leg(d, masks, nf, views, args, peak) if args.nwin > 0 else None
     dirs = None if args.no_dirs else dirs_leg(d, masks, nf, args)
+    small = None if (args.no_small or rank != 0) else small_leg()
 
     if rank != 0:
         return
@@ -498,7 +558,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world, nf),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_u8": e2e_u8, "clocks": clk.summary(),
         "gpu_launches": launches, "path": args.path,
-        "fuse_median": fuse, "finite_n": nwin, "directions": dirs, "mask_gather": gather,
+        "fuse_median": fuse, "finite_n": nwin, "directions": dirs, "small_configs": small, "mask_gather": gather,
     }
     print(json.dumps(line), flush=True)
 

@@ -20,6 +20,7 @@ struct occ_ctx {
     int32_t H = 0, W = 0, V = 0, nfam = 0, max_batch = 0, device = 0;
     int32_t path = OCC_PATH_AUTO;
     int32_t neighbors = 0;               // occ_set_neighbors: N (0 = infinity)
+    int32_t line_seg = kLineSeg;         // positions per k_line unit (<= kLineSeg, multiple of 32)
     int32_t angles = 0;                  // occ_create_dirs context: real-valued directions
     int2 *d_offs = nullptr;              // their Eq. 4 offset tables [V][2 (max_scan/2) + 1]
     uint32_t *d_nwin_work = nullptr;     // k_nwin granule counters (lazy)
@@ -226,9 +227,9 @@ void add_line_units(occ_ctx *c, int32_t gi) {
         }
         if (tlo >= thi) continue;
         const int32_t a = tlo & ~31, b = (thi + 31) & ~31;
-        for (int32_t t0 = a; t0 < b; t0 += kLineSeg) {
+        for (int32_t t0 = a; t0 < b; t0 += c->line_seg) {
             LineUnit u{};
-            u.group = gi; u.l0 = l0; u.t0 = t0; u.t1 = std::min(t0 + kLineSeg, b);
+            u.group = gi; u.l0 = l0; u.t0 = t0; u.t1 = std::min(t0 + c->line_seg, b);
             c->units.push_back(u);
         }
     }
@@ -259,6 +260,15 @@ void build_tiles(occ_ctx *c) {
     for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi) {
         eligible[gi] = line_eligible(c, c->groups[gi]);
         if (eligible[gi]) add_line_units(c, gi);
+    }
+    // segment length: 256 positions, shorter when a call of max_batch frames
+    // would not fill the GPU (a unit is one warp's serial work, ~0.1 ms at
+    // 256 positions): single small frames trade margin work for parallelism
+    while (c->line_seg > 32 && (double)c->units.size() * c->max_batch < 8.0 * 148 * 4) {
+        c->line_seg /= 2;
+        c->units.clear();
+        for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi)
+            if (eligible[gi]) add_line_units(c, gi);
     }
     // longest units first (diagonal families sweep ~1.7x the work per
     // position): the last wave of warps is made of short units
@@ -662,7 +672,10 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
         CK(launch_stats_init(c->d_stats, batch, s)); ++launches;
         ps.end();
     }
-    if (c->path == OCC_PATH_DIRECT && c->neighbors == 0 && !c->angles) {
+    // tiny calls (C1-sized: a few thousand pixel-views) are latency bound:
+    // one thread per pixel-view beats a handful of line-sweep warps
+    const bool tiny = c->path == OCC_PATH_AUTO && (int64_t)batch * HW * c->V <= kTinyPixelViews;
+    if ((c->path == OCC_PATH_DIRECT || tiny) && c->neighbors == 0 && !c->angles) {
         {
             ProfScope ps(c, OCC_KERNEL_STATS, s);
             CK(launch_stats(D, HW, batch, c->d_stats, s)); ++launches;

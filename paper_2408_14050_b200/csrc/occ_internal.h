@@ -123,8 +123,9 @@ cudaError_t launch_direct(const float *D, int32_t H, int32_t W, int32_t batch,
                           const FrameStats *st, const Params &p, uint8_t *masks, const MaskFmt &mf,
                           cudaStream_t s);
 size_t tile_smem_bytes();
-constexpr int kTilePositions = 224;    // TP (7 blocks of 32: smem for 3 CTAs per SM)
-constexpr int kTileHaloMax = 96;       // staged halo per side (multiple of 32)
+constexpr int64_t kTinyPixelViews = 1 << 16;   // AUTO: per-pixel kernel for calls this small
+constexpr int kTilePositions = 160;    // TP (5 blocks of 32: with the 128 halo, smem for 3 CTAs per SM)
+constexpr int kTileHaloMax = 128;      // staged halo per side (multiple of 32): C4 knights need 97
 cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
                         const TileDesc *tiles, int32_t ntiles, const GroupDesc *groups,
                         const ViewDesc *views, int32_t nviews, const FamilyDesc *fams,
