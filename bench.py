@@ -395,6 +395,36 @@ def small_leg():
     return res
 
 
+def c4_leg(peak, frames=2):
+    """BASELINE config 4 (4096x3072, 5x5 array, 24 views incl. s = 2 and the
+    knight families): device time of one occ_detect over `frames` frames."""
+    import torch
+    from paper_2408_14050_b200 import scenes
+    from paper_2408_14050_b200.occ import Detector
+    D = np.stack([scenes.make_scene(4, 0, f) for f in range(frames)])
+    views = scenes.config_views(4)
+    B, h, w = D.shape
+    d = torch.from_numpy(D).cuda()
+    det = Detector(h, w, views, max_batch=B)
+    out = det.detect(d)
+    det.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        det.detect(d, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    kt = det.profile_read()
+    det.close()
+    pv = B * h * w * len(views)
+    return {"frames": B, "views": len(views), "ms_per_call": ms, "value": pv / (ms / 1e3) / 1e6, "unit": "MPV/s",
+            "hbm_frac": B * h * w * (4 + len(views)) / (ms / 1e3) / 1e9 / peak,
+            "kernels_ms": {k: v[0] / reps for k, v in kt.items() if v[1]}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -544,6 +574,7 @@ def main():
     nwin = nwin_leg(d, masks, nf, views, args, peak) if args.nwin > 0 else None
     dirs = None if args.no_dirs else dirs_leg(d, masks, nf, args)
     small = None if (args.no_small or rank != 0) else small_leg()
+    c4 = None if (args.no_small or rank != 0) else c4_leg(peak)
 
     if rank != 0:
         return
@@ -558,7 +589,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(world, nf),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_u8": e2e_u8, "clocks": clk.summary(),
         "gpu_launches": launches, "path": args.path,
-        "fuse_median": fuse, "finite_n": nwin, "directions": dirs, "small_configs": small, "mask_gather": gather,
+        "fuse_median": fuse, "finite_n": nwin, "directions": dirs, "small_configs": small, "c4": c4, "mask_gather": gather,
     }
     print(json.dumps(line), flush=True)
 
