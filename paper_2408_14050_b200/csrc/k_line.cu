@@ -1156,30 +1156,22 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
     if (nunits <= 0) return cudaSuccess;
     LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch, gq, gq_count, gq_cap,
                nunits * batch, mf, 0};
-    static int order = -1;
-    if (order < 0) {
-        const char *ev = getenv("OCC_LINE_ORDER");
-        // frame-major by default: the warps in flight cover about one frame,
-        // whose D and codes stay in L2 for all four families (measured: k_line
-        // DRAM reads per 25-frame chunk 1.34 GB -> 0.26 GB, same time)
-        order = ev ? atoi(ev) : 1;
-    }
+    // tuning knobs, read once (thread-safe static initialisation)
+    // frame-major by default: the warps in flight cover about one frame,
+    // whose D and codes stay in L2 for all four families (measured: k_line
+    // DRAM reads per 25-frame chunk 1.34 GB -> 0.26 GB, same time)
+    static const int order = [] { const char *ev = getenv("OCC_LINE_ORDER"); return ev ? atoi(ev) : 1; }();
     a.frame_major = order;
-    static int nw = 0;
-    if (!nw) {
+    static const int nw = [] {
         const char *ev = getenv("OCC_LINE_WARPS");
-        nw = ev ? max(1, min(4, atoi(ev))) : 4;
-    }
+        return ev ? max(1, min(4, atoi(ev))) : 4;
+    }();
     dim3 grid((unsigned)((a.nwork + nw - 1) / nw));
     const size_t smem = WSMEM * (size_t)nw;
     cudaError_t e;
     // shared memory holds only per-warp bit words / queues; the rest of the
     // SM's 256 KB serves as L1 for the line reads and partner probes
-    static int carve = -2;
-    if (carve == -2) {
-        const char *ev = getenv("OCC_LINE_CARVEOUT");
-        carve = ev ? atoi(ev) : 50;
-    }
+    static const int carve = [] { const char *ev = getenv("OCC_LINE_CARVEOUT"); return ev ? atoi(ev) : 50; }();
     if (code_bytes == 1) {
         e = cudaFuncSetAttribute(k_line<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -378,16 +378,16 @@ cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, co
     a.masks = masks; a.mf = mf;
     a.gpf = ((int64_t)H * W + kGran - 1) / kGran;
     a.ngran = a.gpf * frames;
-    static int occ_blocks = 0;
     const size_t smem = nwin_smem_bytes();
-    if (!occ_blocks) {
-        cudaError_t e = cudaFuncSetAttribute(k_nwin<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, k_nwin<false>, 32 * kNwinWarps, smem);
-        if (e != cudaSuccess) return e;
-        if (occ_blocks < 1) occ_blocks = 1;
-    }
-    cudaError_t e = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), s);
+    // per-device attribute and occupancy (current device; computed per call:
+    // cheap host queries, no static state shared between devices or threads)
+    cudaError_t e = cudaFuncSetAttribute(k_nwin<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ_blocks = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, k_nwin<false>, 32 * kNwinWarps, smem);
+    if (e != cudaSuccess) return e;
+    if (occ_blocks < 1) occ_blocks = 1;
+    e = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
     a.work = work;
     a.cap = kNwinCap;

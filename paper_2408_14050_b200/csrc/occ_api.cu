@@ -727,11 +727,10 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
     // measured at C5 (e2e ms/step for 32/64/128/256 MiB): packed masks
     // 56.3/51.5/50.0/51.4 (H2D bound: larger copies, less exposed
     // start-up); uint8 masks 82.8/83.8/86.4/91.6 (D2H bound: finer copies)
-    static int pipe_env = -2;
-    if (pipe_env == -2) {
-        const char *ev = getenv("OCC_PIPE_MIB");             // tuning knob
-        pipe_env = ev ? std::max(1, atoi(ev)) : -1;
-    }
+    static const int pipe_env = [] {                       // tuning knob, read once
+        const char *ev = getenv("OCC_PIPE_MIB");
+        return ev ? std::max(1, atoi(ev)) : -1;
+    }();
     const int pipe_mib = pipe_env > 0 ? pipe_env : (c->mf.packed ? 128 : 32);
     const int32_t pipe = (int32_t)std::max<int64_t>(1, ((int64_t)pipe_mib << 20) / (int64_t)(HW * sizeof(float)));
     const bool direct = c->path == OCC_PATH_DIRECT && c->neighbors == 0 && !c->angles;
