@@ -1115,7 +1115,8 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
                                               MaskFmt mf, int32_t W, int64_t HW, int32_t nviews,
                                               const ViewDesc *__restrict__ views,
                                               Params p, const HardEntry *__restrict__ gq,
-                                              const uint32_t *__restrict__ gq_count, int32_t gq_cap) {
+                                              const uint32_t *__restrict__ gq_count, int32_t gq_cap,
+                                              const FrameStats *__restrict__ st) {
     const uint32_t n = min(*gq_count, (uint32_t)gq_cap);
     const float NaN = __int_as_float(0x7fc00000);
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
@@ -1128,11 +1129,17 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
         vk.thi = __fadd_rn(p.t_dist, 0x1p-10f);
         const float *Ds = D + (int64_t)f * HW + he.pix;
         const float vp = __ldg(Ds);
+        // a partner at offset j needs j < s delta + t_dist with delta =
+        // fl(v_q - v_p) <= fl(vmax - v_p) (rounding is monotone): offsets past
+        // floor(s fl(vmax - v_p) + t_dist) cannot pair
+        const float vmax = key_float(st[f].maxkey);
+        const double jv = floor(__dadd_rn(__dmul_rn((double)s, (double)__fsub_rn(vmax, vp)), (double)p.t_dist));
+        const int32_t jm = (int32_t)fmin((double)he.jm, jv);
         bool hit = false;
-        for (int32_t j0 = 3; j0 <= he.jm && !hit; j0 += 16) {
+        for (int32_t j0 = 3; j0 <= jm && !hit; j0 += 16) {
             float vq[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= he.jm) ? __ldg(Ds + (int64_t)(j0 + u) * he.step) : NaN;
+            for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * he.step) : NaN;
 #pragma unroll 4
             for (int u = 0; u < 16; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
         }
@@ -1143,8 +1150,8 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
 cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW,
                         int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
-                        int32_t nsm, cudaStream_t s) {
-    k_hard<<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, nviews, views, p, gq, gq_count, gq_cap);
+                        const FrameStats *st, int32_t nsm, cudaStream_t s) {
+    k_hard<<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, nviews, views, p, gq, gq_count, gq_cap, st);
     return cudaGetLastError();
 }
 

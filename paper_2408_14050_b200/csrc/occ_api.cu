@@ -636,7 +636,7 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
                        c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_codes,
                        c->code_bytes, c->d_dbg, c->d_gq, c->d_gq_count, c->gq_cap, s));
         CK(launch_hard(Dc, Mc, c->mf, c->W, HW, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
-                       c->gq_cap, c->nsm, s));
+                       c->gq_cap, c->d_stats + c0, c->nsm, s));
         launches += 2;
         pl.end();
     }

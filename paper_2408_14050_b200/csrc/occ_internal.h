@@ -155,7 +155,7 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
 cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW,
                         int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
-                        int32_t nsm, cudaStream_t s);
+                        const FrameStats *st, int32_t nsm, cudaStream_t s);
 // Pixel-wise median fusion (k_fuse.cu): stack [K][n] -> out [n].
 constexpr int kFuseMaxK = 64;
 cudaError_t launch_fuse_median(const float *stack, int32_t K, int64_t n, float *out, int nsm, cudaStream_t s);
