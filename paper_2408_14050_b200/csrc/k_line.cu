@@ -540,94 +540,20 @@ __device__ __forceinline__ uint32_t queue_bits(const int DIR, const Ctx &c, cons
     return bits & ~take;
 }
 
-// Exact resolution of far survivors S (bit r <-> tau0 + r) of one view.
-// DIR = +1: partners at tau + j (view +b), -1: at tau - j (view -b).
-// These are the survivors the sweep's witness probe did not confirm: first
-// the line's last far offset -1..+2, then a warp-cooperative exhaustive search.
+// Far survivors S (bit r <-> tau0 + r) of one view that the sweep's witness
+// probe did not confirm: all of them go to the deferred queue, searched after
+// the kernel by k_hard (one thread per survivor, the whole GPU, IPC ~3)
+// instead of in this latency-bound warp.  Measured at C5: resolving them here
+// first (the line's last offset, then the parked guess +-1 and a secant step)
+// cost 46.0 ms per step against 36.9 ms for queueing them all.
 __device__ __noinline__ uint32_t resolve(const int DIR, const Ctx &c, uint32_t S, const Blk &b, const ViewK &vk,
-                                         const Params &p, int32_t &jl, int32_t *qbuf, int32_t &qn,
+                                         const Params &p, int32_t *qbuf, int32_t &qn,
                                          uint8_t *Mv, uint32_t &left, int32_t vid) {
     const int lane = c.lane;
     const int32_t h = vk.h;
     OCC_PH_T0(tph);
-    uint32_t hits = 0u, hard = 0u;
     dbg_add(c.dbg, DIR > 0 ? 0 : 1, __popc(S));
-    // 1. the line's last far offset jl for every survivor of the block (bands:
-    //    the partner offset moves with the pixel), 4 independent probes per
-    //    round; vp from the staged chunk
-    uint32_t miss = 0u;
-    {
-        const int32_t j = jl;
-        uint32_t T = S;
-        while (__any_sync(FULL, T != 0u)) {
-            int32_t rr[4];
-            float vq[4], vpv[4];
-            int32_t jmv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                rr[u] = -1;
-                if (T) { rr[u] = DIR > 0 ? 31 - __clz(T) : __ffs(T) - 1; T &= ~(1u << rr[u]); }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                vq[u] = __int_as_float(0x7fc00000);
-                vpv[u] = 0.0f;
-                jmv[u] = 0;
-                if (rr[u] >= 0) {
-                    const int32_t tau = b.tau0 + rr[u];
-                    vpv[u] = b.cb[rr[u] * SP];
-                    jmv[u] = min(dcov_of(DIR, b.Wc, b.cfall, b.tau0, rr[u], h),
-                                 DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
-                    if (j >= 3 && j <= jmv[u]) vq[u] = __ldg(c.Dl + (int64_t)(tau + DIR * j) * c.S);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (rr[u] < 0) continue;
-                if (j >= 3 && j <= jmv[u] && pair_far(vq[u], vpv[u], j, vk, p)) hits |= 1u << rr[u];
-                else miss |= 1u << rr[u];
-            }
-        }
-    }
-    // 2. the rest: the filter witness SA parked by the sweep (past it A falls
-    //    ~1 per step on a flat occluder, so the partner sits near
-    //    jw = max(|SA - tau|, s (v_SA - v_p))); probes jw, jw + 1, jw - 1 in
-    //    parallel, then one secant step from jw
-    while (__any_sync(FULL, miss != 0u)) {
-        dbg_add(c.dbg, 9, 1u);
-        if (miss) {
-            const int32_t r = DIR > 0 ? 31 - __clz(miss) : __ffs(miss) - 1;
-            miss &= ~(1u << r);
-            const int32_t tau = b.tau0 + r;
-            const float vp = b.cb[r * SP];
-            int32_t jm = dcov_of(DIR, b.Wc, b.cfall, b.tau0, r, h);
-            jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
-            const int32_t jw = (int32_t)b.sab[r * 32 + lane];    // the sweep's partner guess
-            float vq[3];
-#pragma unroll
-            for (int u = 0; u < 3; ++u) {
-                const int32_t jj = jw + (u == 0 ? 0 : (u == 1 ? 1 : -1));
-                vq[u] = (jj >= 3 && jj <= jm) ? __ldg(c.Dl + (int64_t)(tau + DIR * jj) * c.S)
-                                              : __int_as_float(0x7fc00000);
-            }
-            bool hit = false;
-#pragma unroll
-            for (int u = 0; u < 3; ++u) {
-                const int32_t jj = jw + (u == 0 ? 0 : (u == 1 ? 1 : -1));
-                if (!hit && pair_far(vq[u], vp, jj, vk, p)) { hit = true; jl = jj; }
-            }
-            if (!hit) {
-                const float yy = __fmaf_rn(vk.fs, __fsub_rn(vq[0], vp), -(float)jw);
-                const int32_t js = jw + (yy == yy ? (int32_t)rintf(fminf(fmaxf(yy, -64.0f), 64.0f)) : 0);
-                if ((js < jw - 1 || js > jw + 1) && js >= 3 && js <= jm &&
-                    pair_far(__ldg(c.Dl + (int64_t)(tau + DIR * js) * c.S), vp, js, vk, p)) {
-                    hit = true; jl = js;
-                }
-            }
-            if (hit) hits |= 1u << r; else hard |= 1u << r;
-        }
-    }
-    dbg_add(c.dbg, 2, __popc(hits));
+    const uint32_t hits = 0u, hard = S;
     dbg_add(c.dbg, 3, __popc(hard));
     // queue the rest for the deferred lane-parallel search.  Flushing here is
     // safe: the queue holds only earlier blocks, whose masks are stored.
@@ -865,7 +791,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     {
         const int32_t kS = max(min(kT + nbr, kEmax), kT);
         float v1 = NaN, v2 = NaN, v3 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY, VW = NaN;
-        int32_t SA = 0, jl = 0;
+        int32_t SA = 0;
         int slot = 0;
         stage_chunk(c, stg, kS);
         cp_commit();
@@ -970,7 +896,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                     b.tau0 = tau0; b.cb = cb;
                     b.Wc = cand_bits32(cwP, tau0 + h, WB, lane); b.cfall = cp.pcl;
                     b.sab = sab; b.T0 = T0;
-                    mP |= resolve(1, c, surv, b, vk, a.p, jl, qbuf, qn, MP, left, vP);
+                    mP |= resolve(1, c, surv, b, vk, a.p, qbuf, qn, MP, left, vP);
                 }
                 store_block(c, MP, mP, k);
                 while (__any_sync(FULL, left != 0u)) {        // queue overflow (rare)
@@ -997,7 +923,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     {
         const int32_t kS = min(max(kB - nbr, kEmin), kB);
         float v1 = NaN, v2 = NaN, v3 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY, VW = NaN;
-        int32_t SA = 0, jl = 0;
+        int32_t SA = 0;
         int slot = 0;
         stage_chunk(c, stg, kS);
         cp_commit();
@@ -1064,7 +990,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 b.tau0 = tau0; b.cb = cb;
                 b.Wc = cand_bits32(cwN, tau0 - h, WB, lane); b.cfall = cn.ncl;
                 b.sab = sab; b.T0 = T0;
-                mN |= resolve(-1, c, surv, b, vk, a.p, jl, qbuf, qn, MN, left, vN);
+                mN |= resolve(-1, c, surv, b, vk, a.p, qbuf, qn, MN, left, vN);
             }
             dbg_add(c.dbg, 7, 32u);
             store_block(c, MN, mN, k);

@@ -359,7 +359,7 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
         (!c->units.empty() &&
          (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = (int32_t)std::min<double>(
-              16.0 * 1048576.0, std::max(65536.0, (double)c->chunk * H * W * n_views / 64.0)))) != cudaSuccess ||
+              64.0 * 1048576.0, std::max(65536.0, (double)c->chunk * H * W * n_views / 64.0)))) != cudaSuccess ||
           cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess))) {
         cudaGetLastError();
         occ_destroy(c);
