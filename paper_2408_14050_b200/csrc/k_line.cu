@@ -467,11 +467,11 @@ __device__ __noinline__ void flush_queue(const int DIR, const Ctx &c, const int3
         if (base + (uint32_t)qn <= (uint32_t)c.gq_cap) {
             for (int32_t e = c.lane; e < qn; e += 32) {
                 const int32_t tau = qbuf[2 * e], w = qbuf[2 * e + 1];
-                const int32_t src = w & 31, jm = w >> 5;
+                const int32_t src = w & 31, jm = (w >> 5) & 0x1FFFF, jw = (int32_t)((uint32_t)w >> 22);
                 HardEntry he;
                 he.pix = (int32_t)(line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S);
                 he.step = DIR * c.S;
-                he.jm = jm;
+                he.jm = jm | (jw << 20);
                 he.fv = (c.f << 8) | vid;
                 c.gq[base + (uint32_t)e] = he;
             }
@@ -484,7 +484,7 @@ __device__ __noinline__ void flush_queue(const int DIR, const Ctx &c, const int3
         const int32_t e = e0 + c.lane;
         if (e < qn) {
             const int32_t tau = qbuf[2 * e], w = qbuf[2 * e + 1];
-            const int32_t src = w & 31, jm = w >> 5;
+            const int32_t src = w & 31, jm = (w >> 5) & 0x1FFFF;
             const float *Ds = c.Df + line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S;
             const int32_t st = DIR * c.S;
             const float vp = __ldg(Ds);
@@ -531,8 +531,10 @@ __device__ __forceinline__ uint32_t queue_bits(const int DIR, const Ctx &c, cons
         const int32_t tau = b.tau0 + r;
         int32_t jm = dcov_of(DIR, b.Wc, b.cfall, b.tau0, r, h);
         jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
+        // the sweep's partner guess rides along (10 bits; k_hard probes it first)
+        const int32_t jw = min(max((int32_t)b.sab[r * 32 + lane], 0), 1023);
         qbuf[2 * pos] = tau;
-        qbuf[2 * pos + 1] = (max(jm, 0) << 5) | lane;
+        qbuf[2 * pos + 1] = (jw << 22) | (max(jm, 0) << 5) | lane;
         ++pos;
     }
     qn += tot;
@@ -1060,8 +1062,19 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
         // floor(s fl(vmax - v_p) + t_dist) cannot pair
         const float vmax = key_float(st[f].maxkey);
         const double jv = floor(__dadd_rn(__dmul_rn((double)s, (double)__fsub_rn(vmax, vp)), (double)p.t_dist));
-        const int32_t jm = (int32_t)fmin((double)he.jm, jv);
+        const int32_t jm = (int32_t)fmin((double)(he.jm & 0xFFFFF), jv);
+        const int32_t jw = he.jm >> 20;          // the sweep's partner guess
         bool hit = false;
+        {   // the sweep's guess +-1 first (its exact guess already failed the probe)
+            float vg[3];
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int32_t jj = jw + (u == 0 ? 0 : (u == 1 ? 1 : -1));
+                vg[u] = (jj >= 3 && jj <= jm) ? __ldg(Ds + (int64_t)jj * he.step) : NaN;
+            }
+#pragma unroll
+            for (int u = 0; u < 3; ++u) hit = hit || pair_far(vg[u], vp, jw + (u == 0 ? 0 : (u == 1 ? 1 : -1)), vk, p);
+        }
         for (int32_t j0 = 3; j0 <= jm && !hit; j0 += 16) {
             float vq[16];
 #pragma unroll

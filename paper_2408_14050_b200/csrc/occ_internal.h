@@ -142,7 +142,8 @@ struct LineUnit {
 };
 // An exhaustive far-partner search deferred to k_hard: survivor at pixel
 // index pix of frame f, view v (fv = f << 8 | v); partners at pix + j * step,
-// j = 3 .. jm (jm = dcov clipped to the image).
+// j = 3 .. jm, jm = (field jm) & 0xFFFFF (dcov clipped to the image); bits 20+
+// carry the sweep's partner guess (0..1023), probed +-1 first.
 struct HardEntry {
     int32_t pix, step, jm, fv;
 };
