@@ -38,9 +38,14 @@
 
 #include "occ_device.cuh"
 
+#ifndef SWEEP_UNROLL
+#define SWEEP_UNROLL 4
+#endif
+
 namespace occ {
 
 namespace {
+constexpr int kSweepUnroll = SWEEP_UNROLL;      // sweep / probe loops
 constexpr int SEGB = kLineSeg / 32;            // blocks per segment
 constexpr int CMW = kLineCandMarginWords;       // candidate margin words per side
 constexpr int NCW = SEGB + 2 * CMW;             // candidate words per view
@@ -824,7 +829,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             const int32_t tau0 = 32 * k;
             const CovP cp = cov_p(cwP, tau0, h, WB, lane);
             uint32_t Xs1 = 0, Xg1 = 0, Xl1 = 0, Xlf = 0, Xs2 = 0, Xg2 = 0, Xl2 = 0, XFR = 0;
-#pragma unroll 8
+#pragma unroll kSweepUnroll
             for (int r = 31; r >= 0; --r) {
                 const float v0 = cb[r * SP];
                 const float d1 = __fsub_rn(v1, v0), d2 = __fsub_rn(v2, v0);
@@ -883,7 +888,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                     const int32_t pc0 = (cand_bits32(cwP, tau0 + h, WB, lane) & 1u) ? tau0 + h : cp.pcl;
                     const int32_t jcb = min(pc0 + h - tau0, c.ehi - 1 - tau0);
                     uint32_t XH = 0u;
-#pragma unroll 8
+#pragma unroll kSweepUnroll
                     for (int r = 31; r >= 0; --r) {
                         const int32_t jv = min((int32_t)sab[r * 32 + lane], jcb - r);
                         const bool ok = jv >= 3 && tau0 + r >= c.elo && ((surv >> r) & 1u);
@@ -954,7 +959,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             const int32_t tau0 = 32 * k;
             const CovN cn = cov_n(cwN, tau0, h, WB, lane);
             uint32_t XFR = 0;
-#pragma unroll 8
+#pragma unroll kSweepUnroll
             for (int r = 0; r < 32; ++r) {
                 const float v0 = cb[r * SP];
                 const float A0 = __fmaf_rn(fs_, v0, ip);
@@ -977,7 +982,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 const int32_t nc0 = (cand_bits32(cwN, tau0 + 31 - h, WB, lane) & 1u) ? tau0 + 31 - h : cn.ncl;
                 const int32_t jcb = min(tau0 + h - nc0, tau0 - c.elo);
                 uint32_t XH = 0u;
-#pragma unroll 8
+#pragma unroll kSweepUnroll
                 for (int r = 31; r >= 0; --r) {
                     const int32_t jv = min((int32_t)sab[r * 32 + lane], jcb + r);
                     const bool ok = jv >= 3 && tau0 + r < c.ehi && ((surv >> r) & 1u);
