@@ -56,7 +56,10 @@ constexpr size_t OFF_Q = OFF_NN + sizeof(uint32_t) * SEGB * 32;
 constexpr size_t OFF_SAB = OFF_Q + sizeof(int32_t) * 2 * QCAP;
 constexpr int SP = 33;                          // staging pitch (floats per position)
 constexpr size_t OFF_STG = OFF_SAB + sizeof(int16_t) * 32 * 32;
-constexpr size_t WSMEM = OFF_STG + sizeof(float) * 2 * 32 * SP;
+#ifndef LINE_ONE_SLOT
+#define LINE_ONE_SLOT 1      // one staging slot: smem 12.4 KB per warp, 16 warps per SM (C5 33.2 -> 28.8 ms per step)
+#endif
+constexpr size_t WSMEM = OFF_STG + sizeof(float) * (LINE_ONE_SLOT ? 1 : 2) * 32 * SP;
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr int32_t NONE_LO = -(1 << 28), NONE_HI = (1 << 28);
 }  // namespace
@@ -803,6 +806,14 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
         stage_chunk(c, stg, kS);
         cp_commit();
         for (int32_t k = kS; k >= kB; --k) {
+#if LINE_ONE_SLOT
+            // one staging slot: chunk k was staged at the end of the previous
+            // iteration; chunk k - 1 is staged after this one is done
+            const float *cb = stg + lane;
+            (void)slot;
+            cp_wait<0>();
+            __syncwarp();
+#else
             // chunk k is (being) staged in `slot`; stage k - 1 into the other slot
             const float *cb = stg + slot * 32 * SP + lane;
             float *nxt = stg + (slot ^ 1) * 32 * SP;
@@ -812,6 +823,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             cp_wait<1>();
             __syncwarp();
             slot ^= 1;
+#endif
             float ip = (float)(32 * k + 31 - T0);
             SA += 32;                                  // witness offset relative to tau0 = 32 k
             if (k > kT) {
@@ -824,6 +836,11 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                     A3 = A2; A2 = A1; A1 = A0; v3 = v2; v2 = v1; v1 = v0;
                     ip = __fsub_rn(ip, 1.0f);
                 }
+#if LINE_ONE_SLOT
+                __syncwarp();
+                stage_chunk(c, stg, k - 1);
+                cp_commit();
+#endif
                 continue;
             }
             const int32_t tau0 = 32 * k;
@@ -854,9 +871,13 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 ip = __fsub_rn(ip, 1.0f);
             }
             // tails: delta1 at 32k - 1, delta2 at 32k - 1 and 32k - 2 (chunk k - 1)
+#if LINE_ONE_SLOT
+            const float vm1 = gv(c, 32 * k - 1), vm2 = gv(c, 32 * k - 2);
+#else
             cp_wait<0>();
             __syncwarp();
             const float vm1 = nxt[31 * SP + lane], vm2 = nxt[30 * SP + lane];
+#endif
             const float d1m = __fsub_rn(v1, vm1), d2m1 = __fsub_rn(v2, vm1), d2m2 = __fsub_rn(v1, vm2);
             const uint32_t s1m = sgnbit(d1m), g1m = sgnbit(__fsub_rn(fabsf(d1m), a1n));
             const uint32_t t1m = (g1m ^ 1u) & sgnbit(__fsub_rn(fabsf(d1m), bhi0));
@@ -916,6 +937,13 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                     qn = 0;
                 }
             }
+#if LINE_ONE_SLOT
+            __syncwarp();
+            if (k - 1 >= kB) {
+                stage_chunk(c, stg, k - 1);
+                cp_commit();
+            }
+#endif
         }
         cp_wait<0>();
         if (vP >= 0 && qn > 0) flush_queue(1, c, qbuf, qn, vk, a.p, MP, vP);
@@ -935,6 +963,12 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
         stage_chunk(c, stg, kS);
         cp_commit();
         for (int32_t k = kS; k <= kT; ++k) {
+#if LINE_ONE_SLOT
+            const float *cb = stg + lane;
+            (void)slot;
+            cp_wait<0>();
+            __syncwarp();
+#else
             const float *cb = stg + slot * 32 * SP + lane;
             float *nxt = stg + (slot ^ 1) * 32 * SP;
             __syncwarp();
@@ -943,6 +977,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
             cp_wait<1>();
             __syncwarp();
             slot ^= 1;
+#endif
             float ip = (float)(32 * k - T0);
             SA -= 32;                                  // witness offset relative to tau0 = 32 k
             if (k < kB) {
@@ -954,6 +989,11 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                     A3 = A2; A2 = A1; A1 = A0; v3 = v2; v2 = v1; v1 = v0;
                     ip = __fadd_rn(ip, 1.0f);
                 }
+#if LINE_ONE_SLOT
+                __syncwarp();
+                stage_chunk(c, stg, k + 1);
+                cp_commit();
+#endif
                 continue;
             }
             const int32_t tau0 = 32 * k;
@@ -1010,6 +1050,13 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 flush_queue(-1, c, qbuf, qn, vk, a.p, MN, vN);
                 qn = 0;
             }
+#if LINE_ONE_SLOT
+            __syncwarp();
+            if (k + 1 <= kT) {
+                stage_chunk(c, stg, k + 1);
+                cp_commit();
+            }
+#endif
         }
         cp_wait<0>();
         if (qn > 0) flush_queue(-1, c, qbuf, qn, vk, a.p, MN, vN);
