@@ -51,11 +51,24 @@ constexpr int CMW = kLineCandMarginWords;       // candidate margin words per si
 constexpr int NCW = SEGB + 2 * CMW;             // candidate words per view
 constexpr size_t OFF_CW = 0;
 constexpr size_t OFF_NN = OFF_CW + sizeof(uint32_t) * 2 * NCW * 32;
-constexpr int QCAP = 128;                       // deferred hard survivors per warp
+#ifndef LINE_QCAP
+#define LINE_QCAP 128
+#endif
+#ifndef LINE_SAB8
+#define LINE_SAB8 0
+#endif
+#if LINE_SAB8
+typedef uint8_t SabT;                           // partner guesses saturated at 255
+#define SAB_MAX 255
+#else
+typedef int16_t SabT;
+#define SAB_MAX 30000
+#endif
+constexpr int QCAP = LINE_QCAP;                 // deferred hard survivors per warp
 constexpr size_t OFF_Q = OFF_NN + sizeof(uint32_t) * SEGB * 32;
 constexpr size_t OFF_SAB = OFF_Q + sizeof(int32_t) * 2 * QCAP;
 constexpr int SP = 33;                          // staging pitch (floats per position)
-constexpr size_t OFF_STG = OFF_SAB + sizeof(int16_t) * 32 * 32;
+constexpr size_t OFF_STG = (OFF_SAB + sizeof(SabT) * 32 * 32 + 15) & ~(size_t)15;
 #ifndef LINE_ONE_SLOT
 #define LINE_ONE_SLOT 1      // one staging slot: smem 12.4 KB per warp, 16 warps per SM (C5 33.2 -> 28.8 ms per step)
 #endif
@@ -421,7 +434,7 @@ struct Blk {
     uint32_t Wc;           // candidate bits of [tau0 + h, +31] (+b) / [tau0 - h, +31] (-b)
     int32_t cfall;         // last candidate < tau0 + h (+b) / first candidate >= tau0 + 32 - h (-b)
     const float *cb;       // the block's staged values, lane column ([r * SP])
-    const int16_t *sab;    // filter witness of each survivor, relative to tau0 ([r][lane])
+    const SabT *sab;       // partner guess of each survivor ([r][lane])
     int32_t T0;
 };
 
@@ -727,7 +740,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
     uint32_t *cw = reinterpret_cast<uint32_t *>(smem + OFF_CW);
     uint32_t *nn = reinterpret_cast<uint32_t *>(smem + OFF_NN);
     int32_t *qbuf = reinterpret_cast<int32_t *>(smem + OFF_Q);
-    int16_t *sab = reinterpret_cast<int16_t *>(smem + OFF_SAB);
+    SabT *sab = reinterpret_cast<SabT *>(smem + OFF_SAB);
     float *stg = reinterpret_cast<float *>(smem + OFF_STG);
     int32_t qn = 0;
     const int32_t T0 = u.t0, T1 = u.t1;            // multiples of 32
@@ -866,7 +879,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 // ~1 per step along a flat occluder, so the partner sits near
                 // jw = max(SA - i, s (v_SA - v_i))
                 if (fr < 0.0f)
-                    sab[r * 32 + lane] = (int16_t)max(SA - r, __float2int_rn(fminf(__fmul_rn(fs_, __fsub_rn(VW, v0)), 30000.0f)));
+                    sab[r * 32 + lane] = (SabT)min(max(SA - r, __float2int_rn(fminf(__fmul_rn(fs_, __fsub_rn(VW, v0)), 30000.0f))), SAB_MAX);
                 A3 = A2; A2 = A1; A1 = A0; v3 = v2; v2 = v1; v1 = v0;
                 ip = __fsub_rn(ip, 1.0f);
             }
@@ -1007,7 +1020,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
                 const float fr = __fsub_rn(__fsub_rn(A0, vk.T), SX);
                 XFR = push(XFR, fr);
                 if (fr < 0.0f)
-                    sab[r * 32 + lane] = (int16_t)max(r - SA, __float2int_rn(fminf(__fmul_rn(fs_, __fsub_rn(VW, v0)), 30000.0f)));
+                    sab[r * 32 + lane] = (SabT)min(max(r - SA, __float2int_rn(fminf(__fmul_rn(fs_, __fsub_rn(VW, v0)), 30000.0f))), SAB_MAX);
                 A3 = A2; A2 = A1; A1 = A0; v3 = v2; v2 = v1; v1 = v0;
                 ip = __fadd_rn(ip, 1.0f);
             }
@@ -1065,7 +1078,10 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
 
 // grid: (units, frames); one warp per block
 template <int CB>
-__global__ void __launch_bounds__(128) k_line(LineArgs a) {
+#ifndef LINE_MINB
+#define LINE_MINB 1
+#endif
+__global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     // one work unit per warp, frame-major (units fastest, longest first)
     const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
