@@ -488,12 +488,10 @@ __device__ __noinline__ void flush_queue(const int DIR, const Ctx &c, const int3
         if (base + (uint32_t)qn <= (uint32_t)c.gq_cap) {
             for (int32_t e = c.lane; e < qn; e += 32) {
                 const int32_t tau = qbuf[2 * e], w = qbuf[2 * e + 1];
-                const int32_t src = w & 31, jm = (w >> 5) & 0x1FFFF, jw = (int32_t)((uint32_t)w >> 22);
+                const int32_t src = w & 31, jm = (w >> 5) & 0x1FFFF;
                 HardEntry he;
                 he.pix = (int32_t)(line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S);
-                he.step = DIR * c.S;
-                he.jm = jm | (jw << 20);
-                he.fv = (c.f << 8) | vid;
+                he.meta = (uint32_t)jm | ((uint32_t)c.f << 17) | ((uint32_t)vid << 25);
                 c.gq[base + (uint32_t)e] = he;
             }
             __syncwarp();
@@ -552,10 +550,8 @@ __device__ __forceinline__ uint32_t queue_bits(const int DIR, const Ctx &c, cons
         const int32_t tau = b.tau0 + r;
         int32_t jm = dcov_of(DIR, b.Wc, b.cfall, b.tau0, r, h);
         jm = min(jm, DIR > 0 ? c.ehi - 1 - tau : tau - c.elo);
-        // the sweep's partner guess rides along (10 bits; k_hard probes it first)
-        const int32_t jw = min(max((int32_t)b.sab[r * 32 + lane], 0), 1023);
         qbuf[2 * pos] = tau;
-        qbuf[2 * pos + 1] = (jw << 22) | (max(jm, 0) << 5) | lane;
+        qbuf[2 * pos + 1] = (max(jm, 0) << 5) | lane;
         ++pos;
     }
     qn += tot;
@@ -1117,8 +1113,10 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
     const float NaN = __int_as_float(0x7fc00000);
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         const HardEntry he = gq[e];
-        const int32_t f = he.fv >> 8, v = he.fv & 255;
-        const int32_t s = views[v].s;
+        const int32_t f = (int32_t)((he.meta >> 17) & 255u), v = (int32_t)(he.meta >> 25);
+        const ViewDesc &vdv = views[v];
+        const int32_t s = vdv.s;
+        const int32_t step = (vdv.sg > 0 ? 1 : -1) * line_stride(vdv.lkind, W);
         ViewK vk;
         vk.s = s; vk.h = 0; vk.fs = (float)s; vk.T = 0.0f;
         vk.tlo = __fsub_rn(p.t_dist, 0x1p-10f);
@@ -1130,23 +1128,12 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
         // floor(s fl(vmax - v_p) + t_dist) cannot pair
         const float vmax = key_float(st[f].maxkey);
         const double jv = floor(__dadd_rn(__dmul_rn((double)s, (double)__fsub_rn(vmax, vp)), (double)p.t_dist));
-        const int32_t jm = (int32_t)fmin((double)(he.jm & 0xFFFFF), jv);
-        const int32_t jw = he.jm >> 20;          // the sweep's partner guess
+        const int32_t jm = (int32_t)fmin((double)(he.meta & 0x1FFFFu), jv);
         bool hit = false;
-        {   // the sweep's guess +-1 first (its exact guess already failed the probe)
-            float vg[3];
-#pragma unroll
-            for (int u = 0; u < 3; ++u) {
-                const int32_t jj = jw + (u == 0 ? 0 : (u == 1 ? 1 : -1));
-                vg[u] = (jj >= 3 && jj <= jm) ? __ldg(Ds + (int64_t)jj * he.step) : NaN;
-            }
-#pragma unroll
-            for (int u = 0; u < 3; ++u) hit = hit || pair_far(vg[u], vp, jw + (u == 0 ? 0 : (u == 1 ? 1 : -1)), vk, p);
-        }
         for (int32_t j0 = 3; j0 <= jm && !hit; j0 += 16) {
             float vq[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * he.step) : NaN;
+            for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * step) : NaN;
 #pragma unroll 4
             for (int u = 0; u < 16; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
         }

@@ -343,7 +343,7 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         const double per = (double)H * W * (4.0 + c->code_bytes);
         const char *ev = getenv("OCC_CHUNK_MIB");          // tuning knob (default 2 GiB)
         const double budget = (ev ? std::max(1, atoi(ev)) : 2048) * 1048576.0;
-        c->chunk = (int32_t)std::max(1.0, std::min(1024.0, std::floor(budget / per)));
+        c->chunk = (int32_t)std::max(1.0, std::min((double)kMaxChunkFrames, std::floor(budget / per)));
         c->chunk = std::min(c->chunk, max_batch);
     }
 
@@ -462,6 +462,7 @@ int occ_create(int32_t H, int32_t W, const occ_baseline *baselines, int32_t n_vi
         fd.view[fd.nviews++] = i;
         vd.fam = fam;
         vd.candbit = 2 * fam + (vd.sg < 0 ? 1 : 0);
+        vd.lkind = fd.kind;
         near_far(vd, p);
         vd.rho = (double)vd.s;
         c->views.push_back(vd);

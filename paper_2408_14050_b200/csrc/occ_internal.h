@@ -25,6 +25,7 @@ struct ViewDesc {
     int32_t num, den;   // reduced slope of the family (den > 0)
     int32_t fam;        // family index (lines shared by +-m b0)
     int32_t candbit;    // bit of the per-pixel candidate code: 2*fam + (sg < 0)
+    int32_t lkind;      // k_line geometry of its family (0 rows .. 3 anti-diagonals; 8 other)
     int32_t jstar;      // first backward offset whose Eq. 5 test implies delta > t_disp
     int32_t nback;      // near backward offsets j = 1..nback (nback = jstar-1)
     int32_t nfwd;       // near forward offsets f = 1..nfwd
@@ -140,13 +141,16 @@ constexpr int kLineCandMarginWords = 4;  // candidate words staged beyond the se
 struct LineUnit {
     int32_t group, l0, t0, t1;
 };
-// An exhaustive far-partner search deferred to k_hard: survivor at pixel
-// index pix of frame f, view v (fv = f << 8 | v); partners at pix + j * step,
-// j = 3 .. jm, jm = (field jm) & 0xFFFFF (dcov clipped to the image); bits 20+
-// carry the sweep's partner guess (0..1023), probed +-1 first.
+// An exhaustive far-partner search deferred to k_hard (8 bytes): survivor at
+// pixel index pix of frame f (of the chunk), view v; partners at
+// pix + j * sg(v) * stride(kind(v)), j = 3 .. jm (dcov clipped to the image).
+// meta = jm | f << 17 | v << 25 (jm <= 2 * (65536 / 2) < 2^17, f < 256,
+// v < 64).
 struct HardEntry {
-    int32_t pix, step, jm, fv;
+    int32_t pix;
+    uint32_t meta;
 };
+constexpr int kMaxChunkFrames = 255;     // f field of HardEntry
 size_t line_smem_bytes();
 cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
