@@ -264,7 +264,9 @@ void build_tiles(occ_ctx *c) {
     // segment length: 256 positions, shorter when a call of max_batch frames
     // would not fill the GPU (a unit is one warp's serial work, ~0.1 ms at
     // 256 positions): single small frames trade margin work for parallelism
-    while (c->line_seg > 32 && (double)c->units.size() * c->max_batch < 8.0 * 148 * 4) {
+    static const int min_seg = [] { const char *ev = getenv("OCC_LINE_MINSEG"); return ev ? std::max(32, atoi(ev)) : 32; }();
+    // one resident wave is 148 SMs x 16 warps (k_line at 4 warps per CTA)
+    while (c->line_seg > min_seg && (double)c->units.size() * c->max_batch < 148.0 * 16) {
         c->line_seg /= 2;
         c->units.clear();
         for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi)
