@@ -138,3 +138,18 @@ def test_dirs_argument_validation(torch_cuda):
             Detector(16, 16, directions=bad)
     with pytest.raises(ValueError):
         Detector(16, 16)
+
+
+def test_dirs_full_c5_frames_bench_launch(torch_cuda):
+    # the launch configuration bench.py's directions leg times: one call over a
+    # batch of C5 frames with the bench's 8 calibrated directions; sampled
+    # whole frames vs the oracle
+    import bench
+    dirs = bench.calibrated_dirs()
+    D = scenes.make_batch(5, 4)
+    g, st = run(torch_cuda, D, dirs, fmt="bits")
+    assert st == [0] * 4
+    for f in (0, 3):
+        o = oracle.detect_dirs(D[f], dirs)
+        for i, d in enumerate(dirs):
+            assert_same(g[f, i], o[i], f"C5 frame {f} dir {d}")
