@@ -1134,8 +1134,22 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
             float vq[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * step) : NaN;
-#pragma unroll 4
-            for (int u = 0; u < 16; ++u) hit = hit || pair_far(vq[u], vp, j0 + u, vk, p);
+            // branch-free fast test of the 16 offsets (fp32 with the 2^-10
+            // band, as pair_far); offsets inside the band take the exact test
+            float mn = INFINITY;
+            bool band = false;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                vq[u] = fabsf(__fmaf_rn(vk.fs, __fsub_rn(vq[u], vp), -(float)(j0 + u)));   // NaN beyond jm
+                mn = fminf(mn, vq[u]);
+                band |= vq[u] >= vk.tlo && vq[u] <= vk.thi;
+            }
+            hit = mn < vk.tlo;
+            if (!hit && band) {
+                for (int u = 0; u < 16 && !hit; ++u)
+                    if (vq[u] >= vk.tlo && vq[u] <= vk.thi)
+                        hit = pair_exact_slow(__ldg(Ds + (int64_t)(j0 + u) * step), vp, j0 + u, s, p.t_dist, p.t_disp);
+            }
         }
         if (hit) mask_put(masks + ((int64_t)f * nviews + v) * mf.vbytes, mf, W, he.pix % W, he.pix / W, true);
     }
