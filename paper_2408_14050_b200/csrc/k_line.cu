@@ -1103,6 +1103,9 @@ __global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
 // Exhaustive far-partner searches queued by k_line: one thread per entry
 // (survivor p of view v in frame f), offsets 3..dcov(p) along its line, 16
 // loads in flight; a confirmed Eq. 5 pair sets the mask byte.
+#ifndef HARD_BATCH
+#define HARD_BATCH 16        // offsets (loads in flight) per k_hard step
+#endif
 __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
                                               MaskFmt mf, int32_t W, int64_t HW, int32_t nviews,
                                               const ViewDesc *__restrict__ views,
@@ -1130,23 +1133,23 @@ __global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8
         const double jv = floor(__dadd_rn(__dmul_rn((double)s, (double)__fsub_rn(vmax, vp)), (double)p.t_dist));
         const int32_t jm = (int32_t)fmin((double)(he.meta & 0x1FFFFu), jv);
         bool hit = false;
-        for (int32_t j0 = 3; j0 <= jm && !hit; j0 += 16) {
-            float vq[16];
+        for (int32_t j0 = 3; j0 <= jm && !hit; j0 += HARD_BATCH) {
+            float vq[HARD_BATCH];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * step) : NaN;
-            // branch-free fast test of the 16 offsets (fp32 with the 2^-10
+            for (int u = 0; u < HARD_BATCH; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * step) : NaN;
+            // branch-free fast test of the HARD_BATCH offsets (fp32 with the 2^-10
             // band, as pair_far); offsets inside the band take the exact test
             float mn = INFINITY;
             bool band = false;
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < HARD_BATCH; ++u) {
                 vq[u] = fabsf(__fmaf_rn(vk.fs, __fsub_rn(vq[u], vp), -(float)(j0 + u)));   // NaN beyond jm
                 mn = fminf(mn, vq[u]);
                 band |= vq[u] >= vk.tlo && vq[u] <= vk.thi;
             }
             hit = mn < vk.tlo;
             if (!hit && band) {
-                for (int u = 0; u < 16 && !hit; ++u)
+                for (int u = 0; u < HARD_BATCH && !hit; ++u)
                     if (vq[u] >= vk.tlo && vq[u] <= vk.thi)
                         hit = pair_exact_slow(__ldg(Ds + (int64_t)(j0 + u) * step), vp, j0 + u, s, p.t_dist, p.t_disp);
             }
