@@ -19,17 +19,17 @@
 //          view -b delta < 0) -- and the far-partner filter of view +b (suffix
 //          max of A = s v - pos over q >= i + 3).  Per 32 positions: window
 //          coverage of both views as two threshold masks (previous / next
-//          candidate), the near marks, far survivors and
-//          their exact resolution, the +b mask store; the -b near marks are
-//          parked in shared memory.
+//          candidate), the near marks, the far survivors and
+//          one probe each, the +b mask store; the -b near marks are parked in
+//          shared memory.
 //  pass B  ascending tau: far filter of view -b (prefix max of s v + pos),
-//          exact resolution of its survivors, the -b mask store.
-// Far survivors (filter passed, no near mark, dcov >= 3) are resolved with
-// the exact Eq. 5 test (pair_exact): first at the offset of the line's last
-// far hit +-2, then at the offset suggested by the nearest edge candidate,
-// then by a warp-cooperative exhaustive search.  D is staged per warp in a
-// ring of kLineRingChunks x 32 positions (cp.async, coalesced); probes
-// outside the ring read global memory (L2).
+//          its survivors' probes, the -b mask store.
+// Far survivors (filter passed, no near mark, dcov >= 3) get one branch-free
+// exact probe (fp32 with a 2^-10 band) at the partner offset guessed from the
+// filter's witness; the rest are queued (8-byte entries) for k_hard, which
+// searches them exhaustively with one thread each after the kernel.  D is
+// staged per warp one chunk of 32 positions x 32 lines at a time (cp.async,
+// coalesced, 33-float pitch); probes read global memory (L1 / L2).
 //
 // Frames the kernel cannot serve with this scheme (h < 17 or h + 32 beyond
 // the candidate margin) are computed by the exact per-pixel
