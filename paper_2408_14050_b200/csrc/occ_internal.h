@@ -136,7 +136,6 @@ cudaError_t launch_tile(const float *D, int32_t H, int32_t W, int32_t batch,
 // arrays: one warp per unit = 32 consecutive lines x [t0, t1) in the lane's
 // time coordinate (t0, t1 multiples of 32, t1 - t0 <= kLineSeg).
 constexpr int kLineSeg = 256;
-constexpr int kLineRingChunks = 5;       // ring of 5 x 32 staged positions per warp
 constexpr int kLineCandMarginWords = 4;  // candidate words staged beyond the segment (h + 32 <= 128)
 struct LineUnit {
     int32_t group, l0, t0, t1;
