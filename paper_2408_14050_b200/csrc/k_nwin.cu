@@ -138,13 +138,24 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
     // 1. valid extent (the clipped line is one interval of g: the in-image
     // test of a rounded point moving along a straight line is monotone)
     int32_t glo = INT_MAX, ghi = INT_MIN;
-    for (int32_t g0 = -h; g0 <= h; g0 += 32) {
-        const int32_t g = g0 + lane;
-        int32_t xx, yy;
-        if (g <= h && geo.at(g, xx, yy)) { glo = min(glo, g); ghi = max(ghi, g); }
+    if (!geo.angle && geo.den == 1 && geo.num >= -1 && geo.num <= 1) {
+        // rows / columns / diagonals: major coordinate mj = pc - sg g in
+        // [0, nmaj) and minor line + num mj in [0, nmin), in closed form
+        int32_t lo = 0, hi = geo.nmaj - 1;
+        if (geo.num == 1) { lo = max(lo, -geo.line); hi = min(hi, geo.nmin - 1 - geo.line); }
+        if (geo.num == -1) { lo = max(lo, geo.line - geo.nmin + 1); hi = min(hi, geo.line); }
+        // mj in [lo, hi]  <=>  g in [pc - hi, pc - lo] (sg = 1) or [lo - pc, hi - pc] (sg = -1)
+        glo = max(-h, geo.sg > 0 ? geo.pc - hi : lo - geo.pc);
+        ghi = min(h, geo.sg > 0 ? geo.pc - lo : hi - geo.pc);
+    } else {
+        for (int32_t g0 = -h; g0 <= h; g0 += 32) {
+            const int32_t g = g0 + lane;
+            int32_t xx, yy;
+            if (g <= h && geo.at(g, xx, yy)) { glo = min(glo, g); ghi = max(ghi, g); }
+        }
+        glo = __reduce_min_sync(0xffffffffu, glo);
+        ghi = __reduce_max_sync(0xffffffffu, ghi);
     }
-    glo = __reduce_min_sync(0xffffffffu, glo);
-    ghi = __reduce_max_sync(0xffffffffu, ghi);
     const int32_t n = ghi - glo + 1;        // >= 1: the candidate itself
     // 2. V = D on the window, W = fl64(G + fl64(rho V))
     float vmin = INFINITY, vmax = -INFINITY;
@@ -263,11 +274,14 @@ __device__ __forceinline__ void window(const NwinArgs &a, const float *__restric
                 near = __dsub_rn(B.w[iq], wp) < lim;
                 if (near) {
                     const float delta = __fsub_rn(B.v[iq], vp);
-                    const int32_t dk = iq - ip;                        // g_q - g_p
-                    const double x = __dmul_rn(rho, (double)delta);
-                    if (x > __dsub_rn(-(double)t_dist, (double)dk) && x < __dsub_rn((double)t_dist, (double)dk)) {
-                        if (delta > t_disp) hp = true;                 // p behind q
-                        else if (-delta > t_disp) hit[rq] = 1;         // q behind p
+                    const bool pq = delta > t_disp, qp = -delta > t_disp;   // only then the distance
+                    if (pq || qp) {
+                        const int32_t dk = iq - ip;                    // g_q - g_p
+                        const double x = __dmul_rn(rho, (double)delta);
+                        if (x > __dsub_rn(-(double)t_dist, (double)dk) && x < __dsub_rn((double)t_dist, (double)dk)) {
+                            if (pq) hp = true;                         // p behind q
+                            else hit[rq] = 1;                          // q behind p
+                        }
                     }
                 }
             }
