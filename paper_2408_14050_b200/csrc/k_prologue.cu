@@ -32,6 +32,16 @@ __device__ __forceinline__ CodeT pixel_code(float c, float right, float below, b
     const float ey = has_b ? __fsub_rn(below, c) : 0.0f;
     const float e2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
     uint32_t code = 0;
+    if (NF == -4) {
+        // the 3x3 array's families (1,0), (0,1), (1,1), (1,-1): the same fp32
+        // dot products as the generic loop below with the +-1 products folded
+        // (1 * x = x, -1 * y = -y exactly); the 0 * E products are kept, so an
+        // infinite E gives NaN and no candidate, as there.  Branch-free.
+        auto sgn2 = [](float x) -> uint32_t { return (x > 0.0f ? 1u : 0u) | (x < 0.0f ? 2u : 0u); };
+        code = sgn2(__fadd_rn(ex, __fmul_rn(0.0f, ey))) | (sgn2(__fadd_rn(__fmul_rn(0.0f, ex), ey)) << 2) |
+               (sgn2(__fadd_rn(ex, ey)) << 4) | (sgn2(__fsub_rn(ex, ey)) << 6);
+        return (CodeT)(e2 > e2_thresh ? code : 0u);
+    }
     if (e2 > e2_thresh) {
         const int nf = NF > 0 ? NF : fd.n;
 #pragma unroll
@@ -170,8 +180,11 @@ cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames
     // at 1920 wide); scalar path: grid-stride over the pixels
     const int bx = std::max(1, std::min(H, 256));
     dim3 grid(bx, frames);
+    const bool grid3 = nfam == 4 && fd.bx[0] == 1 && fd.by[0] == 0 && fd.bx[1] == 0 && fd.by[1] == 1 &&
+                       fd.bx[2] == 1 && fd.by[2] == 1 && fd.bx[3] == 1 && fd.by[3] == -1;
     if (code_bytes == 1) {
-        if (nfam == 4) k_prologue<uint8_t, 4><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
+        if (grid3) k_prologue<uint8_t, -4><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
+        else if (nfam == 4) k_prologue<uint8_t, 4><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
         else if (nfam == 1) k_prologue<uint8_t, 1><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
         else k_prologue<uint8_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
     } else if (code_bytes == 2) {
