@@ -441,6 +441,8 @@ def main():
     ap.add_argument("--nwin", type=int, default=8, help="finite-N leg's N (0: skip the leg)")
     ap.add_argument("--no-dirs", action="store_true", help="skip the real-valued directions leg")
     ap.add_argument("--no-small", action="store_true", help="skip the C1-C3 latency / CUDA-graph leg")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="profiling only: skip the host-buffer legs (the line then lacks e2e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -554,8 +556,10 @@ def main():
                 "d2h_bytes_per_step": nbytes, "ms_per_step": dt * 1e3, "mask_format": fmt,
                 "note": "occ_detect_host: pinned H2D of D, detect, D2H of all masks, stream sync"}
 
-    e2e = host_leg("bits")
-    e2e_u8 = host_leg("u8")
+    e2e = e2e_u8 = None
+    if not args.no_e2e:
+        e2e = host_leg("bits")
+        e2e_u8 = host_leg("u8")
 
     # ---------------- median fusion leg (NEXT #3): K = 8 per-camera estimates ----------------
     fuse = None
