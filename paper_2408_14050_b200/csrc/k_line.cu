@@ -1106,7 +1106,10 @@ __global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
 #ifndef HARD_BATCH
 #define HARD_BATCH 16        // offsets (loads in flight) per k_hard step
 #endif
-__global__ void __launch_bounds__(256) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
+#ifndef HARD_MINB
+#define HARD_MINB 1
+#endif
+__global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
                                               MaskFmt mf, int32_t W, int64_t HW, int32_t nviews,
                                               const ViewDesc *__restrict__ views,
                                               Params p, const HardEntry *__restrict__ gq,
