@@ -738,7 +738,18 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
     const int32_t pipe = (int32_t)std::max<int64_t>(1, ((int64_t)pipe_mib << 20) / (int64_t)(HW * sizeof(float)));
     const bool direct = c->path == OCC_PATH_DIRECT && c->neighbors == 0 && !c->angles;
     const int32_t chunk = direct ? batch : std::min(c->chunk, pipe);
-    const int32_t nchunks = (batch + chunk - 1) / chunk;
+    // chunk boundaries: full chunks, then the last chunk's worth of frames in
+    // quarter pieces, so that less detection and download trails the final
+    // upload (the pipeline is upload bound)
+    std::vector<int32_t> starts;
+    {
+        int32_t c0 = 0;
+        while (batch - c0 > chunk) { starts.push_back(c0); c0 += chunk; }
+        const int32_t piece = direct ? batch : std::max(1, (chunk + 3) / 4);
+        while (c0 < batch) { starts.push_back(c0); c0 += std::min(piece, batch - c0); }
+        starts.push_back(batch);
+    }
+    const int32_t nchunks = (int32_t)starts.size() - 1;
     while ((int32_t)c->ev_pipe.size() < 2 * nchunks + 1) {
         cudaEvent_t e;
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -757,7 +768,7 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
     if ((c->mf.packed || c->neighbors > 0 || c->angles) && !direct)
         CK(cudaMemsetAsync(c->d_stage_M, 0, (size_t)batch * c->V * c->mf.vbytes, s));
     for (int32_t i = 0; i < nchunks; ++i) {
-        const int32_t c0 = i * chunk, n = std::min(chunk, batch - c0);
+        const int32_t c0 = starts[(size_t)i], n = starts[(size_t)i + 1] - c0;
         CK(cudaMemcpyAsync(c->d_stage_D + (size_t)c0 * HW, Dh + (size_t)c0 * HW, (size_t)n * HW * sizeof(float),
                            cudaMemcpyHostToDevice, c->s_h2d));
         CK(cudaEventRecord(c->ev_pipe[2 * i], c->s_h2d));
