@@ -211,3 +211,15 @@ def test_deterministic_hash(torch_cuda):
     a, _ = run_gpu(torch_cuda, D, scenes.VIEWS_3X3)
     b, _ = run_gpu(torch_cuda, D, scenes.VIEWS_3X3)
     assert hashlib.sha256(a.tobytes()).hexdigest() == hashlib.sha256(b.tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("H,W", [(2, 32768), (32768, 3), (3, 20000)])
+def test_extreme_aspect_ratios(torch_cuda, H, W):
+    # the largest extents the ABI accepts (32768) in one dimension: line units
+    # spanning the whole width / height, diagonals of length <= 3
+    rng = scenes.SplitMix64(905, H, W)
+    D = (np.floor(rng.uniform(H * W).reshape(H, W) * 4.0) * 2.0).astype(np.float32)
+    views = scenes.VIEWS_3X3
+    g, st = run_gpu(torch_cuda, D, views)
+    assert st == [0]
+    assert_same(g[0], oracle.detect(D, views), f"{H}x{W}")
