@@ -248,6 +248,8 @@ struct LineArgs {
     int32_t nwork;             // units x frames
     MaskFmt mf;
     int32_t frame_major;       // work order: 0 frames fastest, 1 units fastest (frame-major)
+    const uint32_t *cand;      // k_cand's candidate words for the chunk, or null (pass 0 from codes)
+    const CandFam *candfam;    // per family (indexed by family), slot descriptors
 };
 
 // Per-warp context
@@ -338,47 +340,75 @@ __device__ __forceinline__ uint32_t code_at(const void *codes, int64_t idx) {
     return __ldg(reinterpret_cast<const uint32_t *>(codes) + idx);
 }
 
+// Candidate words of both views (bits cb and cb + 1 of the codes) for the 32
+// positions t0 .. t0 + 31 of the lane's line: bit r <-> tau = t0 + r.
+template <int CB>
+__device__ __forceinline__ void cand_word(const Ctx &c, const void *codesf, int32_t cb, int32_t t0,
+                                          uint32_t &wp, uint32_t &wn) {
+    const int lane = c.lane;
+    wp = 0u;
+    wn = 0u;
+    if (!(t0 + 31 >= c.elo && t0 < c.ehi)) return;
+    if (c.kind == 0 && CB == 1 && (c.W & 15) == 0 && t0 >= 0 && t0 + 32 <= c.W) {
+        // rows: 32 consecutive codes of the lane's row in two 16-byte loads
+        const uint8_t *row = reinterpret_cast<const uint8_t *>(codesf) + (int64_t)(c.l0 + lane) * c.W + t0;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(row + 16 * hh));
+            const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t tp = (u[e] >> cb) & 0x01010101u;
+                const uint32_t tn = (u[e] >> (cb + 1)) & 0x01010101u;
+                wp |= ((tp * 0x10204080u) >> 28) << (16 * hh + 4 * e);
+                wn |= ((tn * 0x10204080u) >> 28) << (16 * hh + 4 * e);
+            }
+        }
+    } else if (t0 >= c.elo && t0 + 32 <= c.ehi) {
+        const int64_t i0 = c.B + (int64_t)t0 * c.S;
+#pragma unroll 8
+        for (int j = 31; j >= 0; --j) {
+            const uint32_t code = code_at<CB>(codesf, i0 + (int64_t)j * c.S) >> cb;
+            wp = (wp << 1) | (code & 1u);
+            wn = (wn << 1) | ((code >> 1) & 1u);
+        }
+    } else {
+        for (int j = 31; j >= 0; --j) {
+            const int32_t tau = t0 + j;
+            uint32_t code = 0u;
+            if (tau >= c.elo && tau < c.ehi) code = code_at<CB>(codesf, c.B + (int64_t)tau * c.S) >> cb;
+            wp = (wp << 1) | (code & 1u);
+            wn = (wn << 1) | ((code >> 1) & 1u);
+        }
+    }
+}
+
 // pass 0: candidate words of both views (bit cb and cb + 1 of the codes)
 template <int CB>
 __device__ __noinline__ void build_cand(const Ctx &c, const void *codesf, int32_t cb, int32_t WB,
                                            uint32_t *cw, int32_t wlo, int32_t whi) {
     const int lane = c.lane;
     for (int w = 0; w < NCW; ++w) {
-        const int32_t t0 = 32 * (WB + w);
         uint32_t wp = 0u, wn = 0u;
-        if (w >= wlo && w <= whi && t0 + 31 >= c.elo && t0 < c.ehi) {
-            if (c.kind == 0 && CB == 1 && (c.W & 15) == 0 && t0 >= 0 && t0 + 32 <= c.W) {
-                // rows: 32 consecutive codes of the lane's row in two 16-byte loads
-                const uint8_t *row = reinterpret_cast<const uint8_t *>(codesf) + (int64_t)(c.l0 + lane) * c.W + t0;
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const uint4 q = __ldg(reinterpret_cast<const uint4 *>(row + 16 * hh));
-                    const uint32_t u[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const uint32_t tp = (u[e] >> cb) & 0x01010101u;
-                        const uint32_t tn = (u[e] >> (cb + 1)) & 0x01010101u;
-                        wp |= ((tp * 0x10204080u) >> 28) << (16 * hh + 4 * e);
-                        wn |= ((tn * 0x10204080u) >> 28) << (16 * hh + 4 * e);
-                    }
-                }
-            } else if (t0 >= c.elo && t0 + 32 <= c.ehi) {
-                const int64_t i0 = c.B + (int64_t)t0 * c.S;
-#pragma unroll 8
-                for (int j = 31; j >= 0; --j) {
-                    const uint32_t code = code_at<CB>(codesf, i0 + (int64_t)j * c.S) >> cb;
-                    wp = (wp << 1) | (code & 1u);
-                    wn = (wn << 1) | ((code >> 1) & 1u);
-                }
-            } else {
-                for (int j = 31; j >= 0; --j) {
-                    const int32_t tau = t0 + j;
-                    uint32_t code = 0u;
-                    if (tau >= c.elo && tau < c.ehi) code = code_at<CB>(codesf, c.B + (int64_t)tau * c.S) >> cb;
-                    wp = (wp << 1) | (code & 1u);
-                    wn = (wn << 1) | ((code >> 1) & 1u);
-                }
-            }
+        if (w >= wlo && w <= whi) cand_word<CB>(c, codesf, cb, 32 * (WB + w), wp, wn);
+        cw[(0 * NCW + w) * 32 + lane] = wp;
+        cw[(1 * NCW + w) * 32 + lane] = wn;
+    }
+}
+
+// pass 0 from the words k_cand precomputed for the whole chunk (no margin
+// recomputation between neighbouring units)
+__device__ __noinline__ void load_cand(const Ctx &c, const uint32_t *cand, const CandFam &cf, int32_t WB,
+                                       uint32_t *cw, int32_t wlo, int32_t whi) {
+    const int lane = c.lane;
+    const int32_t lb = (c.l0 - cf.lmin) >> 5;
+    const uint32_t *base = cand + (((int64_t)c.f * cf.per_frame + cf.base_slot + (int64_t)lb * cf.nk) << 6);
+    for (int w = 0; w < NCW; ++w) {
+        const int32_t k = WB + w - cf.kmin;
+        uint32_t wp = 0u, wn = 0u;
+        if (w >= wlo && w <= whi && k >= 0 && k < cf.nk) {
+            wp = __ldg(base + ((int64_t)k << 6) + lane);
+            wn = __ldg(base + ((int64_t)k << 6) + 32 + lane);
         }
         cw[(0 * NCW + w) * 32 + lane] = wp;
         cw[(1 * NCW + w) * 32 + lane] = wn;
@@ -793,7 +823,8 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
         OCC_PH_T0(tph);
         // coverage reads candidates within h + 32 of the segment (S8, App. A.2)
         const int32_t wlo = ((T0 - h - 32) >> 5) - WB, whi = ((T1 + h + 31) >> 5) - WB;
-        build_cand<CB>(c, codesf, 2 * gd.fam, WB, cw, wlo, whi);
+        if (a.cand) load_cand(c, a.cand, a.candfam[gd.fam], WB, cw, wlo, whi);
+        else build_cand<CB>(c, codesf, 2 * gd.fam, WB, cw, wlo, whi);
         OCC_PH_T1(c, 2, tph);
     }
     const uint32_t *cwP = cw, *cwN = cw + NCW * 32;
@@ -1169,14 +1200,60 @@ cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32
     return cudaGetLastError();
 }
 
+// Candidate words of every (line block, tau block) of the chunk's line
+// families: one warp per (frame, family, 32 lines, 32 positions), the same
+// computation as k_line's pass 0 (cand_word) done once instead of once per
+// unit and margin.  Layout: [frame][per_frame blocks][view 2][lane 32].
+template <int CB>
+__global__ void __launch_bounds__(256) k_cand(const float *D, int32_t H, int32_t W, const void *codes,
+                                              const CandFam *cf, int32_t ncf, int64_t per_frame,
+                                              int64_t nblocks, uint32_t *cand) {
+    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (gw >= nblocks) return;
+    const int32_t f = (int32_t)(gw / per_frame);
+    const int64_t bi = gw - (int64_t)f * per_frame;
+    int q = 0;
+    while (q + 1 < ncf && bi >= cf[q + 1].base_slot) ++q;
+    const CandFam fam = cf[q];
+    const int64_t r = bi - fam.base_slot;
+    const int32_t lb = (int32_t)(r / fam.nk), k = (int32_t)(r - (int64_t)lb * fam.nk) + fam.kmin;
+    Ctx c;
+    c.kind = fam.kind;
+    c.H = H; c.W = W;
+    c.l0 = fam.lmin + 32 * lb;
+    c.lane = threadIdx.x & 31;
+    lg_ext(c.kind, c.l0, c.lane, H, W, c.elo, c.ehi);
+    c.B = line_base(c.kind, c.l0, c.lane, W);
+    c.S = line_stride(c.kind, W);
+    const int64_t HW = (int64_t)H * W;
+    const void *codesf = reinterpret_cast<const unsigned char *>(codes) + (int64_t)f * HW * CB;
+    uint32_t wp, wn;
+    cand_word<CB>(c, codesf, 2 * fam.fam, 32 * k, wp, wn);
+    uint32_t *o = cand + (gw << 6);
+    o[c.lane] = wp;
+    o[32 + c.lane] = wn;
+}
+
+cudaError_t launch_cand(const float *D, int32_t H, int32_t W, int32_t frames, const void *codes, int32_t code_bytes,
+                        const CandFam *cf_slots, int32_t ncf, int64_t per_frame, uint32_t *cand, cudaStream_t s) {
+    if (ncf <= 0 || per_frame <= 0) return cudaSuccess;
+    const int64_t nblocks = per_frame * frames;
+    const unsigned grid = (unsigned)((nblocks + 7) / 8);
+    if (code_bytes == 1) k_cand<1><<<grid, 256, 0, s>>>(D, H, W, codes, cf_slots, ncf, per_frame, nblocks, cand);
+    else if (code_bytes == 2) k_cand<2><<<grid, 256, 0, s>>>(D, H, W, codes, cf_slots, ncf, per_frame, nblocks, cand);
+    else k_cand<4><<<grid, 256, 0, s>>>(D, H, W, codes, cf_slots, ncf, per_frame, nblocks, cand);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
                         const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
                         const MaskFmt &mf, const void *codes, int32_t code_bytes, unsigned long long *dbg,
-                        HardEntry *gq, uint32_t *gq_count, int32_t gq_cap, cudaStream_t s) {
+                        HardEntry *gq, uint32_t *gq_count, int32_t gq_cap, const uint32_t *cand,
+                        const CandFam *candfam, cudaStream_t s) {
     if (nunits <= 0) return cudaSuccess;
     LineArgs a{D, H, W, units, groups, views, nviews, fams, st, p, masks, codes, dbg, batch, gq, gq_count, gq_cap,
-               nunits * batch, mf, 0};
+               nunits * batch, mf, 0, cand, candfam};
     // tuning knobs, read once (thread-safe static initialisation)
     // frame-major by default: the warps in flight cover about one frame,
     // whose D and codes stay in L2 for all four families (measured: k_line

@@ -21,6 +21,10 @@ struct occ_ctx {
     int32_t path = OCC_PATH_AUTO;
     int32_t neighbors = 0;               // occ_set_neighbors: N (0 = infinity)
     int32_t line_seg = kLineSeg;         // positions per k_line unit (<= kLineSeg, multiple of 32)
+    std::vector<CandFam> candfam;        // k_cand word blocks per family (index = family)
+    CandFam *d_candfam = nullptr;
+    int64_t cand_per_frame = 0;
+    uint32_t *d_cand = nullptr;          // k_cand words for one chunk (null: pass 0 from the codes)
     int32_t angles = 0;                  // occ_create_dirs context: real-valued directions
     int2 *d_offs = nullptr;              // their Eq. 4 offset tables [V][2 (max_scan/2) + 1]
     uint32_t *d_nwin_work = nullptr;     // k_nwin granule counters (lazy)
@@ -272,6 +276,45 @@ void build_tiles(occ_ctx *c) {
         for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi)
             if (eligible[gi]) add_line_units(c, gi);
     }
+    // k_cand word blocks: for every family with line units, all 32-line
+    // blocks x all 32-position tau blocks of its lines' extents
+    c->candfam.assign((size_t)c->nfam, CandFam{});
+    {
+        std::vector<char> lfam((size_t)c->nfam, 0);
+        for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi)
+            if (eligible[gi]) lfam[(size_t)c->groups[gi].fam] = 1;
+        int64_t base = 0;
+        for (int32_t fm = 0; fm < c->nfam; ++fm) {
+            CandFam cf{};
+            cf.fam = fm;
+            cf.kind = c->fams[(size_t)fm].kind;
+            cf.base_slot = base;
+            if (lfam[(size_t)fm] && cf.kind <= 3) {
+                int32_t lmin = 0, lmax = 0;
+                if (cf.kind == 0) { lmin = 0; lmax = H - 1; }
+                else if (cf.kind == 1) { lmin = 0; lmax = W - 1; }
+                else if (cf.kind == 2) { lmin = -(W - 1); lmax = H - 1; }
+                else { lmin = 0; lmax = H + W - 2; }
+                int32_t tlo = INT32_MAX, thi = INT32_MIN;
+                for (int32_t l0 = lmin; l0 <= lmax; l0 += 32)
+                    for (int32_t l = 0; l < 32; ++l) {
+                        int32_t lo, hi;
+                        line_extent(cf.kind, l0, l, H, W, lo, hi);
+                        if (lo < hi) { tlo = std::min(tlo, lo); thi = std::max(thi, hi); }
+                    }
+                if (tlo < thi) {
+                    cf.lmin = lmin;
+                    cf.nlb = (lmax - lmin) / 32 + 1;
+                    cf.kmin = floordiv(tlo, 32);
+                    cf.nk = floordiv(thi - 1, 32) - cf.kmin + 1;
+                    base += (int64_t)cf.nlb * cf.nk;
+                }
+            }
+            c->candfam[(size_t)fm] = cf;
+        }
+        c->cand_per_frame = base;
+        for (CandFam &cf : c->candfam) cf.per_frame = base;
+    }
     // longest units first (diagonal families sweep ~1.7x the work per
     // position): the last wave of warps is made of short units
     std::stable_sort(c->units.begin(), c->units.end(), [&](const LineUnit &x, const LineUnit &y) {
@@ -382,6 +425,20 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
                                        cudaMemcpyHostToDevice) != cudaSuccess)) {
         occ_destroy(c);
         return OCC_ERR_CUDA;
+    }
+    {   // k_cand word buffer for one chunk (optional: pass 0 falls back to the codes)
+        const char *ev = getenv("OCC_LINE_CAND");
+        const bool want = !(ev && atoi(ev) == 0);
+        if (want && !c->units.empty() && c->cand_per_frame > 0) {
+            if (cudaMalloc(&c->d_candfam, sizeof(CandFam) * c->candfam.size()) != cudaSuccess ||
+                cudaMemcpy(c->d_candfam, c->candfam.data(), sizeof(CandFam) * c->candfam.size(),
+                           cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaMalloc(&c->d_cand, (size_t)c->chunk * (size_t)c->cand_per_frame * 64 * sizeof(uint32_t)) != cudaSuccess) {
+                cudaGetLastError();
+                cudaFree(c->d_cand);
+                c->d_cand = nullptr;
+            }
+        }
     }
     if (c->angles && cudaMalloc(&c->d_nwin_work, 2 * sizeof(uint32_t)) != cudaSuccess) {
         cudaGetLastError();
@@ -635,9 +692,14 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
     if (!tiled_only && !c->units.empty()) {
         ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
+        if (c->d_cand) {
+            CK(launch_cand(Dc, c->H, c->W, n, c->d_codes, c->code_bytes, c->d_candfam, c->nfam,
+                           c->cand_per_frame, c->d_cand, s));
+            ++launches;
+        }
         CK(launch_line(Dc, c->H, c->W, n, c->d_units, (int32_t)c->units.size(), c->d_groups,
                        c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_codes,
-                       c->code_bytes, c->d_dbg, c->d_gq, c->d_gq_count, c->gq_cap, s));
+                       c->code_bytes, c->d_dbg, c->d_gq, c->d_gq_count, c->gq_cap, c->d_cand, c->d_candfam, s));
         CK(launch_hard(Dc, Mc, c->mf, c->W, HW, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
                        c->gq_cap, c->d_stats + c0, c->nsm, s));
         launches += 2;
@@ -906,6 +968,8 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_nwin_work);
     cudaFree(c->d_override);
     cudaFree(c->d_offs);
+    cudaFree(c->d_cand);
+    cudaFree(c->d_candfam);
     cudaFree(c->nwin_big.buf);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);

@@ -150,12 +150,22 @@ struct HardEntry {
     uint32_t meta;
 };
 constexpr int kMaxChunkFrames = 255;     // f field of HardEntry
+// Candidate words precomputed per chunk by k_cand (one entry per family;
+// families without line units have nlb = nk = 0): blocks of 32 lines x 32
+// positions, [frame][base_slot + lb * nk + (k - kmin)][view 2][lane 32] uint32.
+struct CandFam {
+    int32_t fam, kind, lmin, nlb, kmin, nk;
+    int64_t base_slot, per_frame;
+};
+cudaError_t launch_cand(const float *D, int32_t H, int32_t W, int32_t frames, const void *codes, int32_t code_bytes,
+                        const CandFam *cf, int32_t ncf, int64_t per_frame, uint32_t *cand, cudaStream_t s);
 size_t line_smem_bytes();
 cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, const LineUnit *units,
                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
                         const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
                         const MaskFmt &mf, const void *codes, int32_t code_bytes, unsigned long long *dbg,
-                        HardEntry *gq, uint32_t *gq_count, int32_t gq_cap, cudaStream_t s);
+                        HardEntry *gq, uint32_t *gq_count, int32_t gq_cap, const uint32_t *cand,
+                        const CandFam *candfam, cudaStream_t s);
 cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW,
                         int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
