@@ -1,6 +1,7 @@
 """Write profiles/ncu_traffic.json from `ncu --set full` captures of one
 25-frame chunk: DRAM bytes (read + write) of k_line + k_hard, the kernels of
-bench.py's "line" scope.  Usage: make_traffic.py prof_line.ncu-rep prof_hard.ncu-rep [frames]"""
+bench.py's "line" scope (k_cand + k_line + k_hard).
+Usage: make_traffic.py [--frames N] rep1.ncu-rep rep2.ncu-rep ..."""
 import csv
 import io
 import json
@@ -22,8 +23,12 @@ def dram(rep):
     return tot, v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
 
 
-frames = int(sys.argv[3]) if len(sys.argv) > 3 else 207   # first chunk at the default 2 GiB
-parts = [dram(r) for r in sys.argv[1:3]]
+args = sys.argv[1:]
+frames = 207                                 # first chunk at the default 2 GiB
+if args and args[0] == "--frames":
+    frames = int(args[1])
+    args = args[2:]
+parts = [dram(r) for r in args]
 H, W, V = 1080, 1920, 8
 res = {"kernel": "line", "bytes_per_launch": sum(p[0] for p in parts),
        "alg_bytes_per_launch": frames * H * W * (4 + V),
