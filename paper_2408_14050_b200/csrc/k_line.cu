@@ -511,25 +511,32 @@ __device__ __noinline__ void flush_queue(const int DIR, const Ctx &c, const int3
     const float NaN = __int_as_float(0x7fc00000);
     // normally the searches go to the global queue, resolved after this
     // kernel by k_hard with the whole GPU (no single warp carries a heavy unit)
+    // The entries that fit below the capacity are always written (k_hard
+    // reads slots [0, min(count, cap)), so every one of them must hold an
+    // entry of this chunk); a reservation straddling the capacity resolves
+    // only its remainder here.
+    int32_t done = 0;
     if (c.gq && qn > 0) {
         uint32_t base = 0u;
         if (c.lane == 0) base = atomicAdd(c.gq_count, (uint32_t)qn);
         base = __shfl_sync(FULL, base, 0);
-        if (base + (uint32_t)qn <= (uint32_t)c.gq_cap) {
-            for (int32_t e = c.lane; e < qn; e += 32) {
-                const int32_t tau = qbuf[2 * e], w = qbuf[2 * e + 1];
-                const int32_t src = w & 31, jm = (w >> 5) & 0x1FFFF;
-                HardEntry he;
-                he.pix = (int32_t)(line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S);
-                he.meta = (uint32_t)jm | ((uint32_t)c.f << 17) | ((uint32_t)vid << 25);
-                c.gq[base + (uint32_t)e] = he;
-            }
-            __syncwarp();
+        const int32_t fit = base >= (uint32_t)c.gq_cap ? 0 : (int32_t)min((uint32_t)qn, (uint32_t)c.gq_cap - base);
+        for (int32_t e = c.lane; e < fit; e += 32) {
+            const int32_t tau = qbuf[2 * e], w = qbuf[2 * e + 1];
+            const int32_t src = w & 31, jm = (w >> 5) & 0x1FFFF;
+            HardEntry he;
+            he.pix = (int32_t)(line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S);
+            he.meta = (uint32_t)jm | ((uint32_t)c.f << 17) | ((uint32_t)vid << 25);
+            c.gq[base + (uint32_t)e] = he;
+        }
+        __syncwarp();
+        done = fit;
+        if (fit == qn) {
             OCC_PH_T1(c, 1, tph);
             return;
         }
     }
-    for (int32_t e0 = 0; e0 < qn; e0 += 32) {
+    for (int32_t e0 = done; e0 < qn; e0 += 32) {
         const int32_t e = e0 + c.lane;
         if (e < qn) {
             const int32_t tau = qbuf[2 * e], w = qbuf[2 * e + 1];
@@ -800,8 +807,7 @@ __device__ __forceinline__ void unit_body(const LineArgs &a, const LineUnit &u, 
         const double eps = ldexp(1.0, -19) * ((double)s * (double)M + 4096.0 + (double)a.p.t_dist);
         vk.T = __double2float_ru(__dadd_rn((double)a.p.t_dist, eps));
     }
-    const int32_t reach = min(2 * h, (int32_t)floor(__dadd_rn((double)a.p.t_dist,
-                                                               __dmul_rn((double)s, (double)R))) + 1);
+    const int32_t reach = partner_reach(a.p.t_dist, s, R, h);
     const int32_t nbr = (reach + 3 + 31) >> 5;
     // thresholds (identical for the two views of the group)
     const float a1n = nextup_f(vd0.back_lo[0]), bhi0 = vd0.back_hi[0];

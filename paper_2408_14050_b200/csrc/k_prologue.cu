@@ -50,9 +50,12 @@ __device__ __forceinline__ CodeT pixel_code(float c, float right, float below, b
             // Eq. 2 <=> b0 . (E_x, E_y) > 0, exact sign: with |b0| components
             // in {0, 1, 2} both products are exact in fp32 and the sign of a
             // correctly rounded sum is the sign of the exact sum; otherwise binary64
+            // (the fp32 products can overflow, e.g. 2 * 2e38 = inf where the
+            // exact product is finite: then the binary64 dot decides)
             bool pos, neg;
-            if (fd.small) {
-                const float dot = __fadd_rn(__fmul_rn(fd.fbx[k], ex), __fmul_rn(fd.fby[k], ey));
+            const float px = __fmul_rn(fd.fbx[k], ex), py = __fmul_rn(fd.fby[k], ey);
+            if (fd.small && isfinite(px) && isfinite(py)) {
+                const float dot = __fadd_rn(px, py);
                 pos = dot > 0.0f; neg = dot < 0.0f;
             } else {
                 const double dot = __dadd_rn(__dmul_rn((double)fd.bx[k], (double)ex),

@@ -373,11 +373,9 @@ __device__ __forceinline__ void tile_body(const TileArgs &a, const G &geo, const
         vr[g].nback = vd.nback; vr[g].nfwd = vd.nfwd;
         vr[g].h = view_h(R, vd.s, p.max_scan);
         // reach: a valid partner has |dk| < t_dist + s R (delta <= R) and <= 2h
-        const int32_t jr = (int32_t)floor(__dadd_rn((double)p.t_dist,
-                                                    __dmul_rn((double)vd.s, (double)R))) + 1;
         // staged halo: far partners (min(2h, reach)), candidates within h of a
         // forward neighbour (h + nfwd), near partners (nback)
-        vr[g].jr = min(2 * vr[g].h, jr);
+        vr[g].jr = partner_reach(p.t_dist, vd.s, R, vr[g].h);
         int32_t need = max(vr[g].h + vd.nfwd, vr[g].jr);
         need = max(need, vd.nback);
         // filter margin: bounds the fp32 rounding of B = s v - u (|u| < 2^12)

@@ -349,6 +349,15 @@ void build_tiles(occ_ctx *c) {
     }
 }
 
+// Capacity of the k_line -> k_hard queue: 1/64 of a chunk's pixel-views,
+// clamped to [64 Ki, 64 Mi] entries.  OCC_GQ_CAP (test knob, read at
+// occ_create) overrides it, e.g. to force the capacity-overflow path.
+int32_t gq_capacity(int32_t chunk, int32_t H, int32_t W, int32_t n_views) {
+    const char *ev = getenv("OCC_GQ_CAP");
+    if (ev && atoi(ev) > 0) return atoi(ev);
+    return (int32_t)std::min<double>(64.0 * 1048576.0, std::max(65536.0, (double)chunk * H * W * n_views / 64.0));
+}
+
 }  // namespace
 
 extern "C" {
@@ -403,8 +412,7 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess ||
         cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
         (!c->units.empty() &&
-         (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = (int32_t)std::min<double>(
-              64.0 * 1048576.0, std::max(65536.0, (double)c->chunk * H * W * n_views / 64.0)))) != cudaSuccess ||
+         (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = gq_capacity(c->chunk, H, W, n_views))) != cudaSuccess ||
           cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess))) {
         cudaGetLastError();
         occ_destroy(c);

@@ -16,6 +16,14 @@ __device__ __forceinline__ int32_t view_h(float R, int32_t s, int32_t cap) {
     return ((int32_t)L) >> 1;
 }
 
+// Largest offset a partner can have: |dk| < t_dist + s R
+// (delta <= R) and |dk| <= 2h.  R = inf (the frame's range overflowed fp32)
+// gives 2h; the comparison runs in binary64 before any conversion to int.
+__device__ __forceinline__ int32_t partner_reach(float t_dist, int32_t s, float R, int32_t h) {
+    const double r = floor(__dadd_rn((double)t_dist, __dmul_rn((double)s, (double)R))) + 1.0;
+    return r < (double)(2 * h) ? (int32_t)r : 2 * h;
+}
+
 __device__ __forceinline__ float frame_range(const FrameStats &fs) {
     return __fsub_rn(key_float(fs.maxkey), key_float(fs.minkey));
 }
