@@ -27,17 +27,36 @@ def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
 
+def defines() -> list:
+    """Extra -D flags of an instrumented build (OCC_DEFINES="-DSWEEP_STATS ...";
+    OCC_LINE_STATS=1 adds -DOCC_LINE_STATS).  Each flag set gets its own object
+    directory and library (libocc_<tag>.so), so instrumented objects are never
+    linked into the product library."""
+    d = os.environ.get("OCC_DEFINES", "").split()
+    if os.environ.get("OCC_LINE_STATS"):        # event counters of k_line (tools/line_stats.py)
+        d.append("-DOCC_LINE_STATS")
+    return sorted(set(d))
+
+
+def lib_path() -> str:
+    d = defines()
+    if not d:
+        return SO
+    import hashlib
+    return os.path.join(HERE, "libocc_" + hashlib.sha1(" ".join(d).encode()).hexdigest()[:8] + ".so")
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.h")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "occ.h")]
     newest = max(os.path.getmtime(p) for p in deps)
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= newest:
-        return SO
+    so = lib_path()
+    if not force and os.path.exists(so) and os.path.getmtime(so) >= newest:
+        return so
     # one object per translation unit, compiled in parallel, then linked
-    objdir = os.path.join(HERE, "build_obj")
+    tag = os.path.basename(so)[len("libocc"):-len(".so")]
+    objdir = os.path.join(HERE, "build_obj" + tag)
     os.makedirs(objdir, exist_ok=True)
-    cflags = [f for f in FLAGS if f != "-shared"]
-    if os.environ.get("OCC_LINE_STATS"):        # event counters of k_line (tools/line_stats.py)
-        cflags.append("-DOCC_LINE_STATS")
+    cflags = [f for f in FLAGS if f != "-shared"] + defines()
     jobs = []
     hdr_newest = max(os.path.getmtime(p) for p in deps if not p.endswith(".cu"))
     for src in sources():
@@ -50,8 +69,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed: {' '.join(r.args)}\n{r.stderr}")
     objs = [os.path.join(objdir, os.path.basename(src)[:-3] + ".o") for src in sources()]
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", SO, *objs], check=True)
-    return SO
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", so, *objs], check=True)
+    return so
 
 
 if __name__ == "__main__":

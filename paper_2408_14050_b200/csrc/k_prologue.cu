@@ -94,7 +94,7 @@ __device__ __forceinline__ void stat_acc(float d, int32_t &lo, int32_t &hi, uint
 template <typename CodeT, int NF>
 __global__ void __launch_bounds__(256) k_prologue(const float *__restrict__ D, int32_t H, int32_t W,
                                                   FamDirs fd, float e2_thresh, FrameStats *st,
-                                                  CodeT *__restrict__ codes) {
+                                                  CodeT *__restrict__ codes, int32_t do_stats) {
     const int f = blockIdx.y;
     const int64_t HW = (int64_t)H * W;
     const float *Df = D + (int64_t)f * HW;
@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(256) k_prologue(const float *__restrict__ D, i
                                       has_b, fd, e2_thresh);
         }
     }
+    if (!do_stats) return;          // statistics already computed by k_words
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(256) k_prologue(const float *__restrict__ D, i
 
 cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
                             const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
-                            FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s) {
+                            FrameStats *st, void *codes, int32_t code_bytes, int32_t do_stats, cudaStream_t s) {
     FamDirs fd{};
     fd.n = nfam;
     fd.small = 1;
@@ -186,15 +187,15 @@ cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames
     const bool grid3 = nfam == 4 && fd.bx[0] == 1 && fd.by[0] == 0 && fd.bx[1] == 0 && fd.by[1] == 1 &&
                        fd.bx[2] == 1 && fd.by[2] == 1 && fd.bx[3] == 1 && fd.by[3] == -1;
     if (code_bytes == 1) {
-        if (grid3) k_prologue<uint8_t, -4><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
-        else if (nfam == 4) k_prologue<uint8_t, 4><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
-        else if (nfam == 1) k_prologue<uint8_t, 1><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
-        else k_prologue<uint8_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes);
+        if (grid3) k_prologue<uint8_t, -4><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes, do_stats);
+        else if (nfam == 4) k_prologue<uint8_t, 4><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes, do_stats);
+        else if (nfam == 1) k_prologue<uint8_t, 1><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes, do_stats);
+        else k_prologue<uint8_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint8_t *)codes, do_stats);
     } else if (code_bytes == 2) {
-        if (nfam == 8) k_prologue<uint16_t, 8><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint16_t *)codes);
-        else k_prologue<uint16_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint16_t *)codes);
+        if (nfam == 8) k_prologue<uint16_t, 8><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint16_t *)codes, do_stats);
+        else k_prologue<uint16_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint16_t *)codes, do_stats);
     } else {
-        k_prologue<uint32_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint32_t *)codes);
+        k_prologue<uint32_t, 0><<<grid, 256, 0, s>>>(D, H, W, fd, e2_thresh, st, (uint32_t *)codes, do_stats);
     }
     return cudaGetLastError();
 }

@@ -1,0 +1,1111 @@
+// k_sweep.cu -- the line-sweep hot path for the four line families of a
+// |b| <= 2 grid array whose views share rows, columns, diagonals and
+// anti-diagonals (§3, Eqs. 1-6):
+//
+//   k_words  (K0)  one pass over D: the exact per-frame min / max / non-finite
+//                  count (Eq. 3) and the candidate bits of
+//                  Eqs. 1-2 of all four families, written
+//                  as 32-bit words in the layout the sweep reads (one word =
+//                  one line x 32 positions), so the sweep never recomputes
+//                  an edge test and needs no per-pixel code bytes.
+//   k_sweep  (K1)  one warp = 32 consecutive lines x a segment of positions
+//                  of one family, both views +-b of the family:
+//                    pass 1 (ascending)  the far filter of view -b (running
+//                      max of s v + pos over the partners behind) and the
+//                      last candidates each window needs, parked per block;
+//                    pass 2 (descending) Eq. 5's near tests of both views
+//                      (shared differences), the far filter of view +b,
+//                      window coverage (S8), the far survivors' witness
+//                      probes, and the uint8 / packed stores of both views.
+//                  Unconfirmed far survivors go to k_hard (k_line.cu).
+//
+// Geometry (digital lines; l0 a multiple of 32, lane l is
+// line l0 + l, tau increases along the family's base direction b0):
+//   kind 0 rows      b0 = ( 1, 0): pixel (tau, l0 + l)
+//   kind 1 columns   b0 = ( 0, 1): pixel (l0 + l, tau)
+//   kind 2 diagonals b0 = ( 1, 1): pixel (tau - l, l0 + tau)          line y - x
+//   kind 3 anti-diag b0 = ( 1,-1): pixel (tau - 31 + l, l0 + 31 - tau) line x + y
+// View +b0 ("P") has its occluders at larger tau, view -b0 ("N") at smaller.
+#include <climits>
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+#include <cstring>
+
+#include "occ_device.cuh"
+
+namespace occ {
+
+namespace {
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr int32_t NONE_LO = -(1 << 29), NONE_HI = (1 << 29);
+constexpr int kSlot = 1280;              // floats per staging slot (5 KB: keeps both slots 1 KB aligned)
+constexpr int kWordSlots = 12;            // words per K0 block and lane
+}  // namespace
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint32_t s_ge(int32_t a) { return a <= 0 ? FULL : (a >= 32 ? 0u : (FULL << a)); }
+__device__ __forceinline__ uint32_t s_le(int32_t b) { return b < 0 ? 0u : (b >= 31 ? FULL : ((2u << b) - 1u)); }
+// w << 1 | sign bit of x
+__device__ __forceinline__ uint32_t s_push(uint32_t w, float x) { return __funnelshift_l(__float_as_uint(x), w, 1); }
+__device__ __forceinline__ uint32_t s_sgn(float x) { return __float_as_uint(x) >> 31; }
+__device__ __forceinline__ float s_nextup(float a) {
+    const int32_t b = __float_as_int(a);
+    if (a == 0.0f) return __int_as_float(1);
+    return __int_as_float(a > 0.0f ? b + 1 : b - 1);
+}
+__device__ __forceinline__ uint32_t s_expand4(uint32_t b4) { return (b4 * 0x00204081u) & 0x01010101u; }
+__device__ __forceinline__ uint32_t s_transpose32(uint32_t x, int lane) {
+    const uint32_t M[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int s = 16 >> k;
+        const uint32_t m = M[k];
+        const uint32_t y = __shfl_xor_sync(FULL, x, s);
+        x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+    }
+    return x;
+}
+__device__ __forceinline__ void s_cp16(float *dst, const float *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void s_cp4(float *dst, const float *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void s_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void s_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// ====================================================================== K0
+// One warp per 32 x 32 pixel block (x-block kx, y-block m, frame f): lane c
+// owns column 32 kx + c and walks the 32 rows.  Per pixel (Eq. 1, reading
+// Q1): E_x = D[x+1,y] - D[x,y], E_y = D[x,y+1] - D[x,y] (0 on the last
+// column / row), edge <=> E^2 > e2_thresh (the exact rewrite of
+// sqrt_rn(E^2) > t_e, DESIGN §2 Q4); Eq. 2 for b0 in {(1,0), (0,1), (1,1),
+// (1,-1)} is the sign of b0 . (E_x, E_y), exact in fp32 here: the +-1
+// products are exact and the rounded sum has the sign of the exact sum; the
+// axis families keep the 0 * E term (0 * inf = NaN: no candidate, as the
+// oracle's binary64 dot).  Bit v of a pixel: candidate of view +b0 (v even)
+// or -b0 (v odd).  Row words (ballots over the lanes) are transposed /
+// skewed into the sweep's (line, 32-position) words:
+//   slots 0,1  rows:      line block m,        block kx; lane = row,    bit = column
+//   slots 2,3  columns:   line block kx,       block m;  lane = column, bit = row
+//   slots 4..7 diagonals: lower (c <= r) / upper (c > r) parts, lane = (r - c) mod 32, bit = r
+//   slots 8..11 anti:     lower (c + r <= 31) / upper parts,   lane = (c + r) mod 32, bit = 31 - r
+struct WordsArgs {
+    const float *D;
+    int32_t H, W, nxb, nyb;
+    float e2_thresh;
+    FrameStats *st;
+    uint32_t *words;       // [frame][nyb][nxb][12][32]
+    int32_t do_stats;
+};
+
+__global__ void __launch_bounds__(128) k_words(WordsArgs a) {
+    __shared__ uint32_t rw[4][32][8];
+    __shared__ int32_t r_lo[4], r_hi[4];
+    __shared__ uint32_t r_bad[4];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t kx = blockIdx.x * 4 + warp, m = blockIdx.y, f = blockIdx.z;
+    const int32_t H = a.H, W = a.W;
+    const float *Df = a.D + (int64_t)f * H * W;
+    int32_t lo = 0x7FFFFFFF, hi = (int32_t)0x80000000;
+    uint32_t bad = 0;
+    if (kx < a.nxb) {
+        const int32_t x = 32 * kx + lane, y0 = 32 * m;
+        const bool xin = x < W, xr = x + 1 < W;
+        float v = (xin && y0 < H) ? __ldg(Df + (int64_t)y0 * W + x) : 0.0f;
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+            const int32_t y = y0 + r;
+            const bool in = xin && y < H, yb = y + 1 < H;
+            const float below = (xin && yb) ? __ldg(Df + (int64_t)(y + 1) * W + x) : 0.0f;
+            float right = __shfl_down_sync(FULL, v, 1);
+            if (lane == 31) right = (xr && y < H) ? __ldg(Df + (int64_t)y * W + x + 1) : 0.0f;
+            const float ex = xr ? __fsub_rn(right, v) : 0.0f;
+            const float ey = yb ? __fsub_rn(below, v) : 0.0f;
+            const float e2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+            const bool edge = in && e2 > a.e2_thresh;
+            const float d0 = __fmaf_rn(0.0f, ey, ex), d1 = __fmaf_rn(0.0f, ex, ey);
+            const float d2 = __fadd_rn(ex, ey), d3 = __fsub_rn(ex, ey);
+            const uint32_t b0 = __ballot_sync(FULL, edge && d0 > 0.0f), b1 = __ballot_sync(FULL, edge && d0 < 0.0f);
+            const uint32_t b2 = __ballot_sync(FULL, edge && d1 > 0.0f), b3 = __ballot_sync(FULL, edge && d1 < 0.0f);
+            const uint32_t b4 = __ballot_sync(FULL, edge && d2 > 0.0f), b5 = __ballot_sync(FULL, edge && d2 < 0.0f);
+            const uint32_t b6 = __ballot_sync(FULL, edge && d3 > 0.0f), b7 = __ballot_sync(FULL, edge && d3 < 0.0f);
+            if (lane == 0) {
+                *reinterpret_cast<uint4 *>(&rw[warp][r][0]) = make_uint4(b0, b1, b2, b3);
+                *reinterpret_cast<uint4 *>(&rw[warp][r][4]) = make_uint4(b4, b5, b6, b7);
+            }
+            if (in) {
+                if (isfinite(v)) {
+                    const int32_t k = float_key(v);
+                    lo = min(lo, k);
+                    hi = max(hi, k);
+                } else {
+                    ++bad;
+                }
+            }
+            v = below;
+        }
+        __syncwarp();
+        const uint4 q0 = *reinterpret_cast<const uint4 *>(&rw[warp][lane][0]);
+        const uint4 q1 = *reinterpret_cast<const uint4 *>(&rw[warp][lane][4]);
+        uint32_t o[kWordSlots];
+        o[0] = q0.x;
+        o[1] = q0.y;
+        o[2] = s_transpose32(q0.z, lane);
+        o[3] = s_transpose32(q0.w, lane);
+        const uint32_t ge = FULL << lane, gea = FULL << (31 - lane);
+        {   // diagonals: Q[r] bit j = R[r] bit ((r - j) mod 32)
+            const uint32_t t4 = s_transpose32(__funnelshift_r(__brev(q1.x), __brev(q1.x), 31 - lane), lane);
+            const uint32_t t5 = s_transpose32(__funnelshift_r(__brev(q1.y), __brev(q1.y), 31 - lane), lane);
+            o[4] = t4 & ge;  o[5] = t5 & ge;
+            o[6] = t4 & ~ge; o[7] = t5 & ~ge;
+        }
+        {   // anti-diagonals: Q[r] bit j = R[r] bit ((j - r) mod 32), then bit reversal (bit = 31 - r)
+            const uint32_t t6 = __brev(s_transpose32(__funnelshift_l(q1.z, q1.z, lane), lane));
+            const uint32_t t7 = __brev(s_transpose32(__funnelshift_l(q1.w, q1.w, lane), lane));
+            o[8] = t6 & gea;  o[9] = t7 & gea;
+            o[10] = t6 & ~gea; o[11] = t7 & ~gea;
+        }
+        uint32_t *dst = a.words + ((((int64_t)f * a.nyb + m) * a.nxb + kx) * kWordSlots) * 32 + lane;
+#pragma unroll
+        for (int s = 0; s < kWordSlots; ++s) dst[s * 32] = o[s];
+    }
+    if (!a.do_stats) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+        hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+        bad += __shfl_xor_sync(FULL, bad, o);
+    }
+    if (lane == 0) { r_lo[warp] = lo; r_hi[warp] = hi; r_bad[warp] = bad; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 4; ++w) { lo = min(lo, r_lo[w]); hi = max(hi, r_hi[w]); bad += r_bad[w]; }
+        if (lo != 0x7FFFFFFF) atomicMin(&a.st[f].minkey, lo);
+        if (hi != (int32_t)0x80000000) atomicMax(&a.st[f].maxkey, hi);
+        if (bad) atomicAdd(&a.st[f].nonfinite, bad);
+    }
+}
+
+cudaError_t launch_words(const float *D, int32_t H, int32_t W, int32_t frames, float e2_thresh, FrameStats *st,
+                         uint32_t *words, int32_t do_stats, cudaStream_t s) {
+    WordsArgs a{D, H, W, (W + 31) / 32, (H + 31) / 32, e2_thresh, st, words, do_stats};
+    dim3 grid((unsigned)((a.nxb + 3) / 4), (unsigned)a.nyb, (unsigned)frames);
+    k_words<<<grid, 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ===================================================================== K1
+struct SweepArgs {
+    const float *D;
+    int32_t H, W, nxb, nyb;
+    const SweepUnit *units;    // sorted by kind (kinds 0..3 at [kstart[k], kstart[k + 1]))
+    int32_t nunits, frames;
+    int32_t kstart[5];
+    int32_t fgroup;            // frames per group: work order group, kind, unit, frame
+    const GroupDesc *groups;
+    const ViewDesc *views;
+    int32_t nviews;
+    const FamilyDesc *fams;
+    const FrameStats *st;
+    Params p;
+    uint8_t *masks;
+    MaskFmt mf;
+    const uint32_t *words;
+    HardEntry *gq;
+    uint32_t *gq_count;
+    int32_t gq_cap;
+    int32_t tma;               // 1: TMA staging (W % 4 == 0, 16-byte aligned frames); 0: 4-byte cp.async
+    unsigned long long *dbg;   // event counters (SWEEP_STATS builds), or null
+};
+// TMA descriptors of D viewed as [frames][H][W] fp32 (out-of-image boxes read NaN)
+struct SweepMaps {
+    CUtensorMap rows;          // box 32 x 32, 128-byte swizzle: kind 0 tile [line][position]
+    CUtensorMap cols;          // box 32 x 32: kind 1 tile [position][line]
+    CUtensorMap run;           // box 32 x 1: one image-row run of the diagonal kinds
+};
+
+// warp-aggregated event counter (SWEEP_STATS builds only; warp-uniform call)
+#ifdef SWEEP_STATS
+#define SST(idx, n)                                                                           \
+    do {                                                                                      \
+        const unsigned t_ = __reduce_add_sync(FULL, (unsigned)(n));                           \
+        if (a.dbg && (threadIdx.x & 31) == 0 && t_) atomicAdd(a.dbg + (idx), (unsigned long long)t_); \
+    } while (0)
+#else
+#define SST(idx, n) do { } while (0)
+#endif
+
+// ---------------------------------------------------------------- mbarrier / TMA
+__device__ __forceinline__ uint32_t s_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void s_mbar_init(uint64_t *b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_smem(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void s_mbar_expect(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_smem(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void s_mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(s_smem(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void s_tma3(float *dst, const CUtensorMap *m, int32_t x, int32_t y, int32_t z, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(s_smem(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(s_smem(bar))
+        : "memory");
+}
+
+// Per-warp constants of one unit
+struct SU {
+    int32_t kind, l0, A, lane, H, W, nxb, nyb, f;
+    int32_t elo, ehi;          // lane's in-image tau range
+    int64_t B;                 // pixel index of the lane's line at tau = 0
+    int32_t S;                 // pixel stride per tau
+    const float *Df;
+    const uint32_t *Wf;        // frame's candidate words
+};
+
+__device__ __forceinline__ void s_extent(int kind, int32_t l0, int32_t l, int32_t H, int32_t W, int32_t &lo,
+                                         int32_t &hi) {
+    const int32_t L = l0 + l;
+    if (kind == 0) { lo = 0; hi = (L < H) ? W : 0; }
+    else if (kind == 1) { lo = 0; hi = (L < W) ? H : 0; }
+    else if (kind == 2) { lo = max(l, -l0); hi = min(W + l, H - l0); }
+    else { lo = max(31 - l, l0 + 32 - H); hi = min(W + 31 - l, l0 + 32); }
+    if (hi < lo) hi = lo;
+}
+__device__ __forceinline__ int64_t s_base(int kind, int32_t l0, int32_t l, int32_t W) {
+    if (kind == 0) return (int64_t)(l0 + l) * W;
+    if (kind == 1) return (int64_t)(l0 + l);
+    if (kind == 2) return (int64_t)l0 * W - l;
+    return (int64_t)(l0 + 31) * W - 31 + l;
+}
+__device__ __forceinline__ int32_t s_stride(int kind, int32_t W) {
+    return kind == 0 ? 1 : (kind == 1 ? W : (kind == 2 ? W + 1 : 1 - W));
+}
+
+// candidate word of view v (0: +b0, 1: -b0) for tau block k of the unit's lines
+template <int KIND>
+__device__ __forceinline__ uint32_t s_word(const SU &u, int32_t k, int v) {
+    const uint32_t *Wl = u.Wf + u.lane + 32 * v;
+    constexpr int kind = KIND;
+    if (kind == 0) return (uint32_t)k < (uint32_t)u.nxb ? __ldg(Wl + (u.A * u.nxb + k) * (kWordSlots * 32)) : 0u;
+    if (kind == 1) return (uint32_t)k < (uint32_t)u.nyb ? __ldg(Wl + (k * u.nxb + u.A) * (kWordSlots * 32) + 64) : 0u;
+    const int32_t m = kind == 2 ? u.A + k : u.A - k;
+    if ((uint32_t)m >= (uint32_t)u.nyb) return 0u;
+    const uint32_t *base = Wl + (m * u.nxb + k) * (kWordSlots * 32) + (kind == 2 ? 4 * 32 : 8 * 32);
+    uint32_t w = 0u;
+    if ((uint32_t)k < (uint32_t)u.nxb) w = __ldg(base);
+    if ((uint32_t)(k - 1) < (uint32_t)u.nxb) w |= __ldg(base - kWordSlots * 32 + 64);
+    return w;
+}
+
+// Stages tau block k (32 positions of the 32 lines) into a slot:
+//   kind 0: [line][32 positions] with the 128-byte swizzle (16-byte chunk c of row l at c ^ (l & 7));
+//   kind 1: [position][32 lines];
+//   kinds 2, 3: [position r][36 x from ((32k + r - 31) & ~3)] (the 32 lines' run of image row r,
+//   4-aligned: the lane's element sits at 31 - l (kind 2) or l (kind 3) plus (r + 1) & 3).
+// Kinds 0, 1 by one TMA box (32 x 32, completion on the slot's mbarrier;
+// out-of-image elements read NaN); kinds 2, 3 by 16-byte cp.async (TMA boxes
+// need 16-byte aligned x and 128-byte aligned destinations: a row run would
+// take 256 bytes of shared memory).  Unaligned frames: 4-byte cp.async.
+// Returns whether the block was staged by TMA (then wait on the mbarrier).
+template <int KIND>
+__device__ __noinline__ bool s_stage(const SU &u, const SweepMaps &tm, float *slot, uint64_t *bar, int32_t k, int tma) {
+    const int lane = u.lane;
+    const float NaN = __int_as_float(0x7fc00000);
+    const int32_t H = u.H, W = u.W;
+    if (tma && KIND <= 1) {
+        if (lane == 0) {
+            s_mbar_expect(bar, 4096u);
+            if (KIND == 0) s_tma3(slot, &tm.rows, 32 * k, u.l0, u.f, bar);
+            else s_tma3(slot, &tm.cols, u.l0, 32 * k, u.f, bar);
+        }
+        return true;
+    }
+    if (tma && KIND >= 2) {        // 16-byte copies of the 4-aligned row runs
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            const int c = lane + 32 * i, r = c / 9, q = c - 9 * r;
+            const int32_t y = KIND == 2 ? u.l0 + 32 * k + r : u.l0 + 31 - 32 * k - r;
+            const int32_t x = ((32 * k + r - 31) & ~3) + 4 * q;
+            float *dst = slot + r * 36 + 4 * q;
+            if ((uint32_t)x < (uint32_t)W && (uint32_t)y < (uint32_t)H) s_cp16(dst, u.Df + (int64_t)y * W + x);
+            else *reinterpret_cast<float4 *>(dst) = make_float4(NaN, NaN, NaN, NaN);
+        }
+        s_commit();
+        return false;
+    }
+    for (int r = 0; r < 32; ++r) {
+        const int32_t tau = 32 * k + r;
+        float *dst;
+        if (KIND == 0) dst = slot + lane * 32 + ((((r >> 2) ^ (lane & 7)) << 2) | (r & 3));
+        else if (KIND == 1) dst = slot + r * 32 + lane;
+        else dst = slot + r * 36 + (KIND == 2 ? 31 - lane : lane) + ((r + 1) & 3);
+        if (tau >= u.elo && tau < u.ehi) s_cp4(dst, u.Df + u.B + (int64_t)tau * u.S);
+        else *dst = NaN;
+    }
+    s_commit();
+    return false;
+}
+__device__ __forceinline__ void s_stage_wait(uint64_t *bar, uint32_t &phase, bool by_tma) {
+    if (by_tma) {
+        s_mbar_wait(bar, phase);
+        phase ^= 1u;
+    } else {
+        s_wait<0>();
+    }
+    __syncwarp();
+}
+
+// the lane's staged values at positions 4g .. 4g + 3 (rb: the lane's read base)
+template <int kind>
+__device__ __forceinline__ float4 s_read4(const float *rb, int g, int sw) {
+    if (kind == 0) return *reinterpret_cast<const float4 *>(rb + ((g ^ sw) << 2));
+    if (kind == 1) {
+        const float *p = rb + g * 128;
+        return make_float4(p[0], p[32], p[64], p[96]);
+    }
+    const float *p = rb + g * 144;
+    return make_float4(p[1], p[36 + 2], p[72 + 3], p[108]);
+}
+template <int kind>
+__device__ __forceinline__ float s_read1(const float *rb, int r, int sw) {
+    if (kind == 0) return rb[((((r >> 2) ^ sw) << 2) | (r & 3))];
+    if (kind == 1) return rb[r * 32];
+    return rb[r * 36 + ((r + 1) & 3)];
+}
+// value at tau straight from global memory (NaN outside the line)
+__device__ __forceinline__ float s_gv(const SU &u, int32_t tau) {
+    return (tau >= u.elo && tau < u.ehi) ? __ldg(u.Df + u.B + (int64_t)tau * u.S) : __int_as_float(0x7fc00000);
+}
+
+// mask bits of one view for tau block k (bit r <-> tau = 32k + r), positions
+// outside the lane's line already cleared
+template <int KIND>
+__device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf, uint32_t word, int32_t k) {
+    const int lane = u.lane;
+    const int32_t H = u.H, W = u.W;
+    if (mf.packed) {
+        uint32_t *P = reinterpret_cast<uint32_t *>(Mv);
+        const int32_t Wb = mf.Wb;
+        if (KIND == 0) {
+            const int32_t y = u.l0 + lane;
+            if (y < H && 32 * k >= 0 && 32 * k < W) P[(int64_t)y * Wb + k] = word;
+        } else if (KIND == 1) {
+            const uint32_t t = s_transpose32(word, lane);
+            const int32_t y = 32 * k + lane;
+            if (y >= 0 && y < H && u.l0 < W) P[(int64_t)y * Wb + (u.l0 >> 5)] = t;
+        } else {
+            // tau = 32k + r is one image row; its 32 lanes form a run of 32 x
+            uint32_t mine = 0u;
+            for (int r = 0; r < 32; ++r) {
+                const uint32_t b = __ballot_sync(FULL, (word >> r) & 1u);
+                if (r == lane) mine = b;
+            }
+            const int32_t tau = 32 * k + lane;
+            const int32_t y = KIND == 2 ? u.l0 + tau : u.l0 + 31 - tau;
+            const uint32_t run = KIND == 2 ? __brev(mine) : mine;      // bit j <-> x = tau - 31 + j
+            if (run && y >= 0 && y < H) {
+                const int32_t x0 = tau - 31, w0 = x0 >> 5, sh = x0 & 31;
+                const uint32_t lo = run << sh, hi = sh ? (run >> (32 - sh)) : 0u;
+                if (lo && w0 >= 0 && w0 < Wb) atomicOr(P + (int64_t)y * Wb + w0, lo);
+                if (hi && w0 + 1 >= 0 && w0 + 1 < Wb) atomicOr(P + (int64_t)y * Wb + w0 + 1, hi);
+            }
+        }
+        return;
+    }
+    if (KIND == 0) {
+        const int32_t y = u.l0 + lane, x0 = 32 * k;
+        if (y >= H) return;
+        uint8_t *row = Mv + (int64_t)y * W;
+        if ((W & 15) == 0 && x0 + 32 <= W) {
+            uint4 *d = reinterpret_cast<uint4 *>(row + x0);
+            __stcs(d, make_uint4(s_expand4(word & 15u), s_expand4((word >> 4) & 15u),
+                                 s_expand4((word >> 8) & 15u), s_expand4((word >> 12) & 15u)));
+            __stcs(d + 1, make_uint4(s_expand4((word >> 16) & 15u), s_expand4((word >> 20) & 15u),
+                                     s_expand4((word >> 24) & 15u), s_expand4(word >> 28)));
+        } else {
+            for (int r = 0; r < 32; ++r)
+                if (x0 + r < W) row[x0 + r] = (uint8_t)((word >> r) & 1u);
+        }
+    } else if (KIND == 1) {
+        const uint32_t t = s_transpose32(word, lane);      // lane r: row 32k + r, bit l = column l0 + l
+        const int32_t y = 32 * k + lane;
+        if (y >= H) return;
+        uint8_t *row = Mv + (int64_t)y * W + u.l0;
+        if ((W & 15) == 0 && u.l0 + 32 <= W) {
+            uint4 *d = reinterpret_cast<uint4 *>(row);
+            __stcs(d, make_uint4(s_expand4(t & 15u), s_expand4((t >> 4) & 15u), s_expand4((t >> 8) & 15u),
+                                 s_expand4((t >> 12) & 15u)));
+            __stcs(d + 1, make_uint4(s_expand4((t >> 16) & 15u), s_expand4((t >> 20) & 15u),
+                                     s_expand4((t >> 24) & 15u), s_expand4(t >> 28)));
+        } else {
+            for (int l = 0; l < 32; ++l)
+                if (u.l0 + l < W) row[l] = (uint8_t)((t >> l) & 1u);
+        }
+    } else {
+        // one image row per tau: the 32 lanes write one contiguous run
+        uint8_t *dst = Mv + u.B + (int64_t)(32 * k) * u.S;
+        if (32 * k >= u.elo && 32 * k + 32 <= u.ehi) {
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) __stcs(dst + (int64_t)r * u.S, (uint8_t)((word >> r) & 1u));
+        } else {
+            for (int r = 0; r < 32; ++r) {
+                const int32_t tau = 32 * k + r;
+                if (tau >= u.elo && tau < u.ehi) __stcs(dst + (int64_t)r * u.S, (uint8_t)((word >> r) & 1u));
+            }
+        }
+    }
+}
+
+// Eq. 5 for a far pair (offset j >= jstar: delta > t_disp is implied):
+// |s fl(vq - vp) - j| < t_dist; fp32 with a 2^-10 band, binary64 inside it.
+__device__ __noinline__ bool s_pair_slow(float vq, float vp, int32_t j, int32_t s, float t_dist, float t_disp) {
+    return pair_exact(vq, vp, -j, s, t_dist, t_disp);
+}
+__device__ __forceinline__ bool s_pair_far(float vq, float vp, int32_t j, float fs, int32_t s, float tlo, float thi,
+                                           const Params &p) {
+    const float x = fabsf(__fmaf_rn(fs, __fsub_rn(vq, vp), -(float)j));
+    if (x < tlo) return true;
+    if (!(x <= thi)) return false;
+    return s_pair_slow(vq, vp, j, s, p.t_dist, p.t_disp);
+}
+
+// exhaustive search of one survivor (queue full): offsets 3..J along the line
+__device__ __noinline__ bool s_exhaust(const SU &u, int32_t tau, int dir, int32_t J, float vp, float fs, int32_t s,
+                                       float tlo, float thi, const Params &p) {
+    for (int32_t j = 3; j <= J; ++j) {
+        const float vq = s_gv(u, tau + dir * j);
+        if (s_pair_far(vq, vp, j, fs, s, tlo, thi, p)) return true;
+    }
+    return false;
+}
+
+// exact per-pixel fallback for the unit's positions (frames the sweep does not serve)
+__device__ __noinline__ void s_direct(const SU &u, const SweepArgs &a, const GroupDesc &gd, const FamilyDesc &fd,
+                                      int32_t T0, int32_t T1, bool zero) {
+    const float R = frame_range(a.st[u.f]);
+    for (int g = 0; g < gd.nv; ++g) {
+        const ViewDesc &vd = a.views[gd.view[g]];
+        const int32_t h = view_h(R, vd.s, a.p.max_scan);
+        uint8_t *Mv = a.masks + ((int64_t)u.f * a.nviews + gd.view[g]) * a.mf.vbytes;
+        for (int32_t tau = max(T0, u.elo); tau < min(T1, u.ehi); ++tau) {
+            const int64_t pix = u.B + (int64_t)tau * u.S;
+            const int32_t y = (int32_t)(pix / u.W), x = (int32_t)(pix - (int64_t)y * u.W);
+            const bool mk = !zero && direct_pixel<false>(u.Df, u.H, u.W, vd, fd, a.p, h, x, y);
+            mask_put(Mv, a.mf, u.W, x, y, mk);
+        }
+    }
+}
+
+struct Rec {                   // pass 1 -> pass 2, per block and lane (12 bytes)
+    uint32_t XN;               // view -b far-filter survivors (bit r <-> tau0 + r)
+    int16_t pclP;              // last +b candidate <= tau0 + h - 1, minus tau0 (clamped: see s_rel)
+    int16_t lcN;               // last -b candidate <= tau0 + 31 - h, minus tau0
+    __half2 VW;                // v at the -b filter's witness after positions 0 / 16 (partner guesses)
+};
+// candidate positions relative to the block, clamped below: a last candidate
+// further than 2h + 32 below the block's start covers none of its windows
+__device__ __forceinline__ int16_t s_rel(int32_t c, int32_t tau0, int32_t h) {
+    return (int16_t)max(c - tau0, -min(2 * h + 64, 32000));
+}
+
+constexpr int kMaxSegBlocks = kSweepSeg / 32;
+constexpr int kListCap = 256;                 // dense survivor list (entries per block)
+constexpr size_t kRecOff = sizeof(float) * kSlot * 2;
+constexpr size_t kListOff = kRecOff + sizeof(Rec) * 32 * kMaxSegBlocks;
+constexpr size_t kMarkOff = kListOff + sizeof(uint16_t) * kListCap;
+constexpr size_t kBarOff = kMarkOff + sizeof(uint32_t) * 64;
+constexpr size_t kSweepWarpSmem = ((kBarOff + 16) + 1023) & ~(size_t)1023;   // 1 KB aligned (128-byte swizzle)
+size_t sweep_smem_bytes() { return kSweepWarpSmem; }
+
+__device__ __forceinline__ int32_t s_guess(float vw, float vp, float fs, int32_t J) {
+    return min(max(__float2int_rn(fminf(fmaxf(__fmul_rn(fs, __fsub_rn(vw, vp)), -1e9f), 1e9f)), 3), J);
+}
+__device__ __forceinline__ float s_sel4(int r, float a0, float a1, float a2, float a3) {
+    return r >= 16 ? (r >= 24 ? a3 : a2) : (r >= 8 ? a1 : a0);
+}
+
+struct SurvCtx {
+    int32_t tau0, h;
+    uint32_t WP, WN;           // window candidate bits: +b [tau0 + h, +31], -b [tau0 - h, +31]
+    int32_t pcl, ncl;          // last +b candidate <= tau0 + h - 1, first -b candidate >= tau0 + 32 - h
+    float Q0, Q1, Q2, Q3;      // +b witness values after positions 7, 15, 23, 31
+    __half2 VW;                // -b witness values after positions 0, 16
+    float fs;
+    int32_t s;
+    float tlo, thi;
+    int32_t vP, vN;
+};
+
+// value of lane src's line at block position r of the staged slot
+template <int kind>
+__device__ __forceinline__ float s_slot_at(const float *slot, int src, int r) {
+    if (kind == 0) return slot[src * 32 + ((((r >> 2) ^ (src & 7)) << 2) | (r & 3))];
+    if (kind == 1) return slot[r * 32 + src];
+    return slot[r * 36 + (kind == 2 ? 31 - src : src) + ((r + 1) & 3)];
+}
+
+// Dense resolution of one block's far survivors (Eq. 5 far pairs,
+// PAPER.md:131-142): the survivors of all lanes are listed lane-major in
+// shared memory (entry = r | view << 5 | lane << 6) and processed 32 per
+// round; a round reads the owner lane's window words and witnesses by
+// shuffles.  For survivor i of view +b (-b): the partner offset j must lie in
+// [3, J], J = dcov(i) (S8) clipped to the line; the probe is at the
+// witness guess j = s (v_w - v_i), then at the fixed point s (v(q) - v_i)
+// of the probed value; a miss goes to k_hard's queue.  Hits are OR-ed into
+// the owner's mask word through shared-memory atomics.
+// one listed survivor, decoded with its owner lane's context (warp-collective: shuffles)
+struct SurvDec {
+    int64_t B;                 // owner line's pixel index at tau = 0
+    int32_t i, J, dir;         // position, largest partner offset, partner direction (+1: +b, -1: -b)
+    float vp, vw;              // v(i), witness value (partner guess)
+    int src, r, view;
+    bool ok;                   // a listed survivor with J >= 3
+};
+template <int KIND>
+__device__ __forceinline__ SurvDec s_decode(const SU &u, const float *slot, const SurvCtx &c, const uint16_t *list,
+                                            uint32_t tot, uint32_t e) {
+    SurvDec d;
+    const bool valid = e < tot;
+    const uint32_t ent = valid ? list[e] : 0u;
+    d.src = (int)(ent >> 6); d.r = (int)(ent & 31); d.view = (int)((ent >> 5) & 1);
+    const int src = d.src, r = d.r;
+    const uint32_t wp = __shfl_sync(FULL, c.WP, src), wn = __shfl_sync(FULL, c.WN, src);
+    const int32_t pcl = __shfl_sync(FULL, c.pcl, src), ncl = __shfl_sync(FULL, c.ncl, src);
+    const float q0 = __shfl_sync(FULL, c.Q0, src), q1 = __shfl_sync(FULL, c.Q1, src);
+    const float q2 = __shfl_sync(FULL, c.Q2, src), q3 = __shfl_sync(FULL, c.Q3, src);
+    const uint32_t vwb = __shfl_sync(FULL, *reinterpret_cast<const uint32_t *>(&c.VW), src);
+    int32_t elo, ehi;
+    s_extent(KIND, u.l0, src, u.H, u.W, elo, ehi);
+    d.B = s_base(KIND, u.l0, src, u.W);
+    d.i = c.tau0 + r;
+    d.vp = s_slot_at<KIND>(slot, src, r);
+    if (d.view == 0) {
+        const uint32_t m = wp & s_le(r);
+        const int32_t pc = m ? c.tau0 + c.h + 31 - __clz(m) : pcl;
+        d.J = min(pc + c.h - d.i, ehi - 1 - d.i);
+        d.dir = 1;
+        d.vw = s_sel4(r, q0, q1, q2, q3);
+    } else {
+        const uint32_t m = wn & s_ge(r);
+        const int32_t nc = m ? c.tau0 - c.h + __ffs(m) - 1 : ncl;
+        d.J = min(d.i + c.h - nc, d.i - elo);
+        d.dir = -1;
+        const __half2 h2 = *reinterpret_cast<const __half2 *>(&vwb);
+        d.vw = r >= 16 ? __high2float(h2) : __low2float(h2);
+    }
+    d.ok = valid && d.J >= 3;
+    return d;
+}
+
+template <int KIND>
+__device__ __noinline__ void s_resolve(const SweepArgs &a, const SU &u, const float *slot, const SurvCtx &c,
+                                       uint32_t sP, uint32_t sN, uint32_t &mP, uint32_t &mN, uint16_t *list,
+                                       uint32_t *marks) {
+    const int lane = u.lane;
+    constexpr int kind = KIND;
+    const float NaN = __int_as_float(0x7fc00000);
+    marks[lane] = 0u;
+    marks[32 + lane] = 0u;
+    // (rare) more survivors than the list holds: blocks of 4 positions in
+    // turn (at most 4 x 64 = 256 <= kListCap entries each)
+    const int rw = __reduce_add_sync(FULL, __popc(sP) + __popc(sN)) > (uint32_t)kListCap ? 4 : 32;
+    static_assert(4 * 64 <= kListCap, "list capacity");
+    const uint32_t sP0 = sP, sN0 = sN;
+    for (int rlo = 0; rlo < 32; rlo += rw) {
+    const uint32_t pm = s_ge(rlo) & s_le(rlo + rw - 1);
+    sP = sP0 & pm;
+    sN = sN0 & pm;
+    // lane-major list: counts, exclusive prefix
+    const uint32_t n = __popc(sP) + __popc(sN);
+    uint32_t inc = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    const uint32_t tot = __shfl_sync(FULL, inc, 31);
+    {
+        uint32_t o = inc - n;
+        const uint16_t tag = (uint16_t)(lane << 6);
+        uint32_t t = sP;
+        while (t) { list[o++] = (uint16_t)(tag | (__ffs(t) - 1)); t &= t - 1u; }
+        t = sN;
+        while (t) { list[o++] = (uint16_t)(tag | 32 | (__ffs(t) - 1)); t &= t - 1u; }
+    }
+    __syncwarp();
+    // rounds of 32 entries, 4 rounds at a time: all their probe loads are in
+    // flight together (the probes are L2 latency bound)
+    for (uint32_t b0 = 0; b0 < tot; b0 += 4 * 32) {
+        SurvDec d[4];
+        float vq[4], w2[4];
+        int32_t j1[4], j2[4];
+        bool hit[4], p2[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            d[q] = s_decode<KIND>(u, slot, c, list, tot, b0 + 32 * q + lane);
+            j1[q] = s_guess(d[q].vw, d[q].vp, c.fs, d[q].J);
+            vq[q] = d[q].ok ? __ldg(u.Df + d[q].B + (int64_t)(d[q].i + d[q].dir * j1[q]) * u.S) : NaN;
+        }
+        bool any2 = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            hit[q] = d[q].ok && s_pair_far(vq[q], d[q].vp, j1[q], c.fs, c.s, c.tlo, c.thi, a.p);
+            SST(3 + d[q].view, hit[q]);
+            j2[q] = s_guess(vq[q], d[q].vp, c.fs, d[q].J);
+            p2[q] = d[q].ok && !hit[q] && vq[q] == vq[q] && j2[q] != j1[q];
+            any2 = any2 || p2[q];
+        }
+        SST(9, lane == 0);
+        if (__any_sync(FULL, any2)) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                w2[q] = p2[q] ? __ldg(u.Df + d[q].B + (int64_t)(d[q].i + d[q].dir * j2[q]) * u.S) : NaN;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool h2 = p2[q] && s_pair_far(w2[q], d[q].vp, j2[q], c.fs, c.s, c.tlo, c.thi, a.p);
+                SST(5 + d[q].view, h2);
+                hit[q] = hit[q] || h2;
+            }
+        }
+        uint32_t bq[4], nq = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (hit[q]) atomicOr(marks + 32 * d[q].view + d[q].src, 1u << d[q].r);
+            const bool miss = d[q].ok && !hit[q];
+            SST(7 + d[q].view, miss);
+            bq[q] = __ballot_sync(FULL, miss);
+            nq += __popc(bq[q]);
+        }
+        if (nq) {
+            uint32_t base = 0u;
+            if (lane == 0) base = atomicAdd(a.gq_count, nq);
+            base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if ((bq[q] >> lane) & 1u) {
+                    const uint32_t slotq = base + __popc(bq[q] & ((1u << lane) - 1u));
+                    const int vid = d[q].view ? c.vN : c.vP;
+                    if (slotq < (uint32_t)a.gq_cap) {
+                        HardEntry he;
+                        he.pix = (int32_t)(d[q].B + (int64_t)d[q].i * u.S);
+                        he.meta = (uint32_t)d[q].J | ((uint32_t)u.f << 17) | ((uint32_t)vid << 25);
+                        a.gq[slotq] = he;
+                    } else {
+                        SU o = u;
+                        int32_t elo, ehi;
+                        s_extent(KIND, u.l0, d[q].src, u.H, u.W, elo, ehi);
+                        o.B = d[q].B; o.elo = elo; o.ehi = ehi;
+                        if (s_exhaust(o, d[q].i, d[q].dir, d[q].J, d[q].vp, c.fs, c.s, c.tlo, c.thi, a.p))
+                            atomicOr(marks + 32 * d[q].view + d[q].src, 1u << d[q].r);
+                    }
+                }
+                base += __popc(bq[q]);
+            }
+        }
+    }
+    __syncwarp();
+    }
+    mP |= marks[lane];
+    mN |= marks[32 + lane];
+    __syncwarp();
+}
+
+template <int KIND>
+__device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm, const SweepUnit &un,
+                                        const GroupDesc &gd, int32_t f, unsigned char *smem, uint32_t *phase) {
+    const FamilyDesc &fd = a.fams[gd.fam];
+    SU u;
+    u.kind = KIND;
+    constexpr int kind = KIND;
+    u.l0 = un.l0;
+    u.A = un.l0 >> 5;
+    u.lane = threadIdx.x & 31;
+    u.H = a.H; u.W = a.W; u.nxb = a.nxb; u.nyb = a.nyb; u.f = f;
+    const int lane = u.lane;
+    s_extent(kind, u.l0, lane, u.H, u.W, u.elo, u.ehi);
+    u.B = s_base(kind, u.l0, lane, u.W);
+    u.S = s_stride(kind, u.W);
+    const int64_t HW = (int64_t)a.H * a.W;
+    u.Df = a.D + (int64_t)f * HW;
+    u.Wf = a.words + (int64_t)f * a.nyb * a.nxb * kWordSlots * 32;
+    float *stg = reinterpret_cast<float *>(smem);
+    Rec *rec = reinterpret_cast<Rec *>(smem + kRecOff);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kBarOff);
+    const int32_t T0 = un.t0, T1 = un.t1;         // multiples of 32
+    const int32_t kB = T0 >> 5, kT = (T1 >> 5) - 1;
+    // read base of the lane in a slot (kind 0: its row; 1: its column; 2, 3: its element of the row runs)
+    const int32_t rbo = kind == 0 ? lane * 32 : (kind == 2 ? 31 - lane : lane);
+    const int sw = lane & 7;
+
+    int32_t vP = -1, vN = -1;
+    for (int g = 0; g < gd.nv; ++g) {
+        if (a.views[gd.view[g]].sg > 0) vP = gd.view[g]; else vN = gd.view[g];
+    }
+    const ViewDesc &vd0 = a.views[vP >= 0 ? vP : vN];
+    const FrameStats fs = a.st[f];
+    const float R = frame_range(fs);
+    const int32_t s = vd0.s;
+    const int32_t h = view_h(R, s, a.p.max_scan);
+    if (fs.nonfinite || h <= 0) {                 // SPEC.md:76 reject / Q17: zero masks
+        s_direct(u, a, gd, fd, T0, T1, true);
+        return;
+    }
+    if (h < 17) {                                 // window coverage below needs 2h >= 34
+        s_direct(u, a, gd, fd, T0, T1, false);
+        return;
+    }
+    const int32_t reach = partner_reach(a.p.t_dist, s, R, h);
+    const int32_t nbr = (reach + 3 + 31) >> 5;    // staged warm-up blocks per pass
+    const int32_t nbl = (T1 - T0) / 32 + nbr;     // blocks per pass
+    const float fs_ = (float)s;
+    float T;                                      // far-filter margin
+    {
+        const float M = fmaxf(fabsf(key_float(fs.minkey)), fabsf(key_float(fs.maxkey)));
+        const double P = 32.0 * (nbl + 2);
+        const double eps = ldexp(1.0, -23) * (double)(2 * nbl + 5) * ((double)s * (double)M + P + (double)a.p.t_dist + 1.0);
+        T = __double2float_ru(__dadd_rn((double)a.p.t_dist, eps));
+    }
+    const float tlo = __fsub_rn(a.p.t_dist, 0x1p-10f), thi = __fadd_rn(a.p.t_dist, 0x1p-10f);
+    const float a1n = s_nextup(vd0.back_lo[0]), bhi0 = vd0.back_hi[0];
+    const float a2n = s_nextup(vd0.back_lo[1]), bhi1 = vd0.back_hi[1];
+    const bool NFWD = vd0.nfwd > 0;
+    const float fhi0 = NFWD ? vd0.fwd_hi[0] : 0.0f;
+    const int tma = a.tma;
+    const float NaN = __int_as_float(0x7fc00000);
+    // unit's tau extent over its lanes (staging range)
+    int32_t kEmin = u.elo >> 5, kEmax = (u.ehi - 1) >> 5;
+    if (u.elo >= u.ehi) { kEmin = 1 << 20; kEmax = -(1 << 20); }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kEmin = min(kEmin, __shfl_xor_sync(FULL, kEmin, o));
+        kEmax = max(kEmax, __shfl_xor_sync(FULL, kEmax, o));
+    }
+    const int32_t hq = h >> 5, hr = h & 31;       // window offsets in words / bits
+    const int32_t nsh = (32 - hr) & 31, nq = hr ? -hq - 1 : -hq;
+
+    // ------------------------------------------------ pass 1 (ascending)
+    // Far filter of view -b: SY = max over q <= i - 3 of A'(q) = s v(q) + (q -
+    // base), base = the current half-block's first position (A' shifted by
+    // -16 per half-block).  Also the last candidates the windows need.
+    {
+        const int32_t kS = max(kB - nbr, kEmin);           // first staged block
+        // word tracking: P window [tau0 + h - 32, tau0 + h - 1] (word k + hq - 1,
+        // shift hr), N window [tau0 - h, tau0 + 31 - h] (word k + nq, shift nsh)
+        const int32_t kW = min(kS, kB - ((2 * h + 63) >> 5));
+        int32_t pcl = NONE_LO, lc = NONE_LO;
+        uint32_t pw_lo = s_word<KIND>(u, kW + hq - 1, 0), nw_lo = s_word<KIND>(u, kW + nq, 1);
+        uint32_t pw_nx = s_word<KIND>(u, kW + hq, 0), nw_nx = s_word<KIND>(u, kW + nq + 1, 1);   // prefetched
+        float A1 = NaN, A2 = NaN, A3 = NaN, w1 = NaN, w2 = NaN, w3 = NaN, SY = -INFINITY, VM = NaN;
+        uint32_t XN = 0u;
+        int slot = 0;
+        bool bt[2] = {false, false};
+        if (kS <= kT) bt[0] = s_stage<KIND>(u, tm, stg, bars, kS, tma);
+        for (int32_t k = kW; k <= kT; ++k) {
+            const uint32_t pw_hi = pw_nx, nw_hi = nw_nx;
+            pw_nx = s_word<KIND>(u, k + 1 + hq, 0);
+            nw_nx = s_word<KIND>(u, k + 1 + nq + 1, 1);
+            const uint32_t WP = __funnelshift_r(pw_lo, pw_hi, hr);
+            pw_lo = pw_hi;
+            if (WP) pcl = 32 * k + h - 32 + 31 - __clz(WP);
+            const uint32_t WN = __funnelshift_r(nw_lo, nw_hi, nsh);
+            nw_lo = nw_hi;
+            if (WN) lc = 32 * k - h + 31 - __clz(WN);
+            if (k < kS) continue;
+            s_stage_wait(bars + slot, phase[slot], bt[slot]);
+            if (k + 1 <= kT) bt[slot ^ 1] = s_stage<KIND>(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k + 1, tma);
+            const float *rb = stg + slot * kSlot + rbo;
+            float Q0 = NaN, Q2 = NaN;
+            if (vN >= 0) {
+#pragma unroll 1
+                for (int hb = 0; hb < 2; ++hb) {
+                    SY = __fsub_rn(SY, 16.0f);
+                    A1 = __fsub_rn(A1, 16.0f); A2 = __fsub_rn(A2, 16.0f); A3 = __fsub_rn(A3, 16.0f);
+                    float qa = NaN;
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const float4 q4 = s_read4<KIND>(rb, 4 * hb + g, sw);
+                        const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float v0 = vv[e];
+                            const float A0 = __fmaf_rn(fs_, v0, (float)(4 * g + e));
+                            if (A3 > SY) { SY = A3; VM = w3; }
+                            XN = s_push(XN, __fsub_rn(__fsub_rn(A0, T), SY));
+                            if (g == 0 && e == 0) qa = VM;
+                            A3 = A2; A2 = A1; A1 = A0;
+                            w3 = w2; w2 = w1; w1 = v0;
+                        }
+                    }
+                    if (hb) Q2 = qa; else Q0 = qa;
+                }
+            }
+            __syncwarp();
+            slot ^= 1;
+            if (k >= kB) {
+                Rec rr;
+                rr.XN = __brev(XN);
+                rr.pclP = s_rel(pcl, 32 * k, h);
+                rr.lcN = s_rel(lc, 32 * k, h);
+                rr.VW = __floats2half2_rn(Q0, Q2);
+                rec[(k - kB) * 32 + lane] = rr;
+            }
+        }
+    }
+
+    // ------------------------------------------------ pass 2 (descending)
+    uint8_t *MP = vP >= 0 ? a.masks + ((int64_t)f * a.nviews + vP) * a.mf.vbytes : nullptr;
+    uint8_t *MN = vN >= 0 ? a.masks + ((int64_t)f * a.nviews + vN) * a.mf.vbytes : nullptr;
+    {
+        const int32_t kS = min(kT + nbr, kEmax);            // first staged block (from the top)
+        const int32_t kW = max(kS, kT + 2 + ((2 * h + 31) >> 5));
+        int32_t fc = NONE_HI, ncl = NONE_HI;
+        uint32_t pw_hi = s_word<KIND>(u, kW + hq + 1, 0), nw_hi = s_word<KIND>(u, kW + nq + 1, 1);
+        uint32_t pw_nx = s_word<KIND>(u, kW + hq, 0), nw_nx = s_word<KIND>(u, kW + nq, 1);   // prefetched
+        uint32_t WNprev = 0u;
+        float v1 = NaN, v2 = NaN, v3 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY, VM = NaN;
+        int slot = 0;
+        bool bt[2] = {false, false};
+        bt[0] = s_stage<KIND>(u, tm, stg, bars, kS, tma);
+        for (int32_t k = kW; k >= kB; --k) {
+            const int32_t tau0 = 32 * k;
+            const uint32_t pw_lo = pw_nx, nw_lo = nw_nx;
+            pw_nx = s_word<KIND>(u, k - 1 + hq, 0);
+            nw_nx = s_word<KIND>(u, k - 1 + nq, 1);
+            const uint32_t WP = __funnelshift_r(pw_lo, pw_hi, hr);      // +b candidates [tau0 + h, tau0 + h + 31]
+            pw_hi = pw_lo;
+            if (WP) fc = tau0 + h + __ffs(WP) - 1;
+            const uint32_t WN = __funnelshift_r(nw_lo, nw_hi, nsh);     // -b candidates [tau0 - h, tau0 - h + 31]
+            nw_hi = nw_lo;
+            if (WNprev) ncl = tau0 + 32 - h + __ffs(WNprev) - 1;
+            WNprev = WN;
+            if (k > kS) continue;
+            s_stage_wait(bars + slot, phase[slot], bt[slot]);
+            if (k - 1 >= kB) bt[slot ^ 1] = s_stage<KIND>(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k - 1, tma);
+            const float *rb = stg + slot * kSlot + rbo;
+            if (k > kT) {
+                // warm-up: far filter of +b only
+#pragma unroll 1
+                for (int hb = 1; hb >= 0; --hb) {
+                    SX = __fsub_rn(SX, 16.0f);
+                    A1 = __fsub_rn(A1, 16.0f); A2 = __fsub_rn(A2, 16.0f); A3 = __fsub_rn(A3, 16.0f);
+#pragma unroll
+                    for (int g = 3; g >= 0; --g) {
+                        const float4 q4 = s_read4<KIND>(rb, 4 * hb + g, sw);
+                        const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                        for (int e = 3; e >= 0; --e) {
+                            const float v0 = vv[e];
+                            const float A0 = __fmaf_rn(fs_, v0, -(float)(4 * g + e));
+                            if (A3 > SX) { SX = A3; VM = v3; }
+                            A3 = A2; A2 = A1; A1 = A0;
+                            v3 = v2; v2 = v1; v1 = v0;
+                        }
+                    }
+                }
+                __syncwarp();
+                slot ^= 1;
+                continue;
+            }
+            // tails for the pairs reaching below the block (d1 at tau0 - 1, d2 at tau0 - 1, tau0 - 2)
+            const float vm1 = s_gv(u, tau0 - 1), vm2 = s_gv(u, tau0 - 2);
+            uint32_t Xs1 = 0, Xg1 = 0, Xl1 = 0, Xlf = 0, Xs2 = 0, Xg2 = 0, Xl2 = 0, XFR = 0;
+            float Q0 = NaN, Q1 = NaN, Q2 = NaN, Q3 = NaN;   // +b witness values after positions 7, 15, 23, 31
+#pragma unroll 1
+            for (int hb = 1; hb >= 0; --hb) {
+                SX = __fsub_rn(SX, 16.0f);
+                A1 = __fsub_rn(A1, 16.0f); A2 = __fsub_rn(A2, 16.0f); A3 = __fsub_rn(A3, 16.0f);
+                float qa = NaN, qb = NaN;
+#pragma unroll
+                for (int g = 3; g >= 0; --g) {
+                    const float4 q4 = s_read4<KIND>(rb, 4 * hb + g, sw);
+                    const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                    for (int e = 3; e >= 0; --e) {
+                        const float v0 = vv[e];
+                        const float d1 = __fsub_rn(v1, v0), d2 = __fsub_rn(v2, v0);
+                        const float e1 = fabsf(d1), e2 = fabsf(d2);
+                        Xs1 = s_push(Xs1, d1);
+                        Xg1 = s_push(Xg1, __fsub_rn(e1, a1n));
+                        Xl1 = s_push(Xl1, __fsub_rn(e1, bhi0));
+                        Xlf = s_push(Xlf, __fsub_rn(e1, fhi0));
+                        Xs2 = s_push(Xs2, d2);
+                        Xg2 = s_push(Xg2, __fsub_rn(e2, a2n));
+                        Xl2 = s_push(Xl2, __fsub_rn(e2, bhi1));
+                        const float A0 = __fmaf_rn(fs_, v0, -(float)(4 * g + e));
+                        if (A3 > SX) { SX = A3; VM = v3; }
+                        XFR = s_push(XFR, __fsub_rn(__fsub_rn(A0, T), SX));
+                        if (g == 3 && e == 3) qb = VM;
+                        if (g == 1 && e == 3) qa = VM;
+                        A3 = A2; A2 = A1; A1 = A0;
+                        v3 = v2; v2 = v1; v1 = v0;
+                    }
+                }
+                if (hb) { Q2 = qa; Q3 = qb; } else { Q0 = qa; Q1 = qb; }
+            }
+            // v1 = v(tau0), v2 = v(tau0 + 1)
+            const float d1m = __fsub_rn(v1, vm1), d2m1 = __fsub_rn(v2, vm1), d2m2 = __fsub_rn(v1, vm2);
+            const uint32_t s1m = s_sgn(d1m), g1m = s_sgn(__fsub_rn(fabsf(d1m), a1n));
+            const uint32_t t1m = (g1m ^ 1u) & s_sgn(__fsub_rn(fabsf(d1m), bhi0));
+            const uint32_t tfm = NFWD ? ((g1m ^ 1u) & s_sgn(__fsub_rn(fabsf(d1m), fhi0))) : 0u;
+            const uint32_t t2m1 = (s_sgn(__fsub_rn(fabsf(d2m1), a2n)) ^ 1u) & s_sgn(__fsub_rn(fabsf(d2m1), bhi1));
+            const uint32_t t2m2 = (s_sgn(__fsub_rn(fabsf(d2m2), a2n)) ^ 1u) & s_sgn(__fsub_rn(fabsf(d2m2), bhi1));
+            const uint32_t s2m1 = s_sgn(d2m1), s2m2 = s_sgn(d2m2);
+            const uint32_t T1 = ~Xg1 & Xl1, T2 = ~Xg2 & Xl2, TF = NFWD ? (~Xg1 & Xlf) : 0u;
+            const uint32_t ext = s_ge(u.elo - tau0) & s_le(u.ehi - 1 - tau0);
+            const Rec rr = rec[(k - kB) * 32 + lane];
+            // view +b: pairs (i, i + j) covered <=> a +b candidate in [i + j - h, i + h]
+            const int32_t pcl = tau0 + rr.pclP;
+            const uint32_t cPa = s_ge(fc - h - tau0);
+            const uint32_t cP1 = cPa | s_le(pcl + h - 1 - tau0);
+            const uint32_t cP2 = cPa | s_le(pcl + h - 2 - tau0);
+            const uint32_t cP3 = cPa | s_le(pcl + h - 3 - tau0);
+            const uint32_t cPf = s_ge(fc - h + 1 - tau0) | s_le(pcl + h - tau0);
+            uint32_t mP = ((T1 & ~Xs1) & cP1) | ((T2 & ~Xs2) & cP2);
+            if (NFWD) mP |= (((TF & Xs1) << 1) | (tfm & s1m)) & cPf;
+            mP &= ext;
+            // view -b: pairs (i - j, i) covered <=> a -b candidate in [i - h, i - j + h]
+            const int32_t lc = tau0 + rr.lcN;
+            const uint32_t cNa = s_le(lc + h - tau0);
+            const uint32_t cN1 = cNa | s_ge(ncl + 1 - h - tau0);
+            const uint32_t cN2 = cNa | s_ge(ncl + 2 - h - tau0);
+            const uint32_t cN3 = cNa | s_ge(ncl + 3 - h - tau0);
+            const uint32_t cNf = s_le(lc + h - 1 - tau0) | s_ge(ncl - h - tau0);
+            const uint32_t n1 = ((T1 & Xs1) << 1) | (t1m & s1m);
+            const uint32_t n2 = ((T2 & Xs2) << 2) | ((t2m1 & s2m1) << 1) | (t2m2 & s2m2);
+            uint32_t mN = (n1 & cN1) | (n2 & cN2);
+            if (NFWD) mN |= (TF & ~Xs1) & cNf;
+            mN &= ext;
+            uint32_t sP = vP >= 0 ? (XFR & cP3 & ~mP & ext) : 0u;
+            uint32_t sN = vN >= 0 ? (rr.XN & cN3 & ~mN & ext) : 0u;
+            SST(0, __popc(ext));
+            SST(1, __popc(sP));
+            SST(2, __popc(sN));
+            SST(10, __popc(mP));
+            SST(11, __popc(mN));
+            // far survivors: a witness-guided exact probe, then one fixed-point
+            // step j <- s (v(q) - v(i)) from the probed value; the rest to k_hard.
+            // Densely: the warp's survivors are listed (lane-major) and resolved
+            // 32 per round, whatever lanes they belong to.
+            if (__any_sync(FULL, (sP | sN) != 0u)) {
+                SurvCtx sc;
+                sc.tau0 = tau0; sc.h = h; sc.WP = WP; sc.WN = WN; sc.pcl = pcl; sc.ncl = ncl;
+                sc.Q0 = Q0; sc.Q1 = Q1; sc.Q2 = Q2; sc.Q3 = Q3; sc.VW = rr.VW;
+                sc.fs = fs_; sc.s = s; sc.tlo = tlo; sc.thi = thi; sc.vP = vP; sc.vN = vN;
+                s_resolve<KIND>(a, u, stg + slot * kSlot, sc, sP, sN, mP, mN,
+                          reinterpret_cast<uint16_t *>(smem + kListOff), reinterpret_cast<uint32_t *>(smem + kMarkOff));
+            }
+            __syncwarp();
+            slot ^= 1;
+            if (vP >= 0) s_store<KIND>(u, MP, a.mf, mP, k);
+            if (vN >= 0) s_store<KIND>(u, MN, a.mf, mN, k);
+        }
+    }
+}
+
+// grid: CTAs of 4 warps, one unit per warp.  Work order: frame groups of
+// fgroup frames; inside a group all units of kind 0, then 1, 2, 3 (longest
+// first), each over the group's frames.  The warps in flight then run one or
+// two kinds on a few frames (D and the words stay in L2).
+constexpr int kSweepWarps = 4;
+__global__ void __launch_bounds__(32 * kSweepWarps, 4) k_sweep(const __grid_constant__ SweepArgs a,
+                                                                 const __grid_constant__ SweepMaps tm) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const uint32_t wid = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
+    if (wid >= (uint32_t)a.nunits * (uint32_t)a.frames) return;
+    const uint32_t per_group = (uint32_t)a.nunits * (uint32_t)a.fgroup;
+    const int32_t g = (int32_t)(wid / per_group);
+    const int32_t f0 = g * a.fgroup, gf = min(a.fgroup, a.frames - f0);
+    const int32_t rem = (int32_t)(wid - (uint32_t)g * per_group);
+    int kk = 0;
+    while (kk < 3 && rem >= a.kstart[kk + 1] * gf) ++kk;
+    const int32_t ri = rem - a.kstart[kk] * gf;
+    const SweepUnit un = a.units[a.kstart[kk] + ri / gf];
+    const int32_t f = f0 + ri % gf;
+    const GroupDesc gd = a.groups[un.group];
+    unsigned char *sm = smem + (size_t)(threadIdx.x >> 5) * kSweepWarpSmem;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + kBarOff);
+    if ((threadIdx.x & 31) == 0) {
+        s_mbar_init(bars, 1);
+        s_mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t phase[2] = {0u, 0u};
+    switch (a.fams[gd.fam].kind) {
+        case 0: sweep_unit<0>(a, tm, un, gd, f, sm, phase); break;
+        case 1: sweep_unit<1>(a, tm, un, gd, f, sm, phase); break;
+        case 2: sweep_unit<2>(a, tm, un, gd, f, sm, phase); break;
+        default: sweep_unit<3>(a, tm, un, gd, f, sm, phase); break;
+    }
+}
+
+// host: TMA descriptors of the chunk's D ([frames][H][W] fp32)
+static bool make_maps(const float *D, int32_t H, int32_t W, int32_t frames, SweepMaps &m) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)frames};
+    const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const cuuint32_t box32[3] = {32, 32, 1}, box1[3] = {32, 1, 1};
+    void *g = const_cast<float *>(D);
+    auto mk = [&](CUtensorMap *t, const cuuint32_t *box, CUtensorMapSwizzle swz) {
+        return enc(t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, g, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA) ==
+               CUDA_SUCCESS;
+    };
+    return mk(&m.rows, box32, CU_TENSOR_MAP_SWIZZLE_128B) && mk(&m.cols, box32, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+           mk(&m.run, box1, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+cudaError_t launch_sweep(const float *D, int32_t H, int32_t W, int32_t frames, const SweepUnit *units,
+                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
+                         const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
+                         const MaskFmt &mf, const uint32_t *words, HardEntry *gq, uint32_t *gq_count,
+                         int32_t gq_cap, const int32_t *kstart, int32_t fgroup, unsigned long long *dbg,
+                         cudaStream_t s) {
+    if (nunits <= 0 || frames <= 0) return cudaSuccess;
+    SweepArgs a{};
+    for (int k = 0; k < 5; ++k) a.kstart[k] = kstart[k];
+    a.fgroup = fgroup;
+    a.D = D; a.H = H; a.W = W; a.nxb = (W + 31) / 32; a.nyb = (H + 31) / 32;
+    a.units = units; a.nunits = nunits; a.frames = frames;
+    a.groups = groups; a.views = views; a.nviews = nviews; a.fams = fams; a.st = st; a.p = p;
+    a.masks = masks; a.mf = mf; a.words = words; a.gq = gq; a.gq_count = gq_count; a.gq_cap = gq_cap;
+    a.dbg = dbg;
+    SweepMaps tm;
+    memset(&tm, 0, sizeof(tm));
+    static const bool no_tma = [] { const char *ev = getenv("OCC_NO_TMA"); return ev && atoi(ev) != 0; }();
+    a.tma = (!no_tma && (W & 3) == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0 && make_maps(D, H, W, frames, tm))
+                ? 1 : 0;
+    const size_t smem = kSweepWarpSmem * kSweepWarps;
+    cudaError_t e = cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(k_sweep, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    const int64_t nw = (int64_t)nunits * frames;
+    k_sweep<<<(unsigned)((nw + kSweepWarps - 1) / kSweepWarps), 32 * kSweepWarps, smem, s>>>(a, tm);
+    return cudaGetLastError();
+}
+
+}  // namespace occ

@@ -42,7 +42,12 @@ struct occ_ctx {
     std::vector<TileDesc> tiles;
     GroupDesc *d_groups = nullptr;
     TileDesc *d_tiles = nullptr;
-    std::vector<LineUnit> units;          // k_line work (eligible groups)
+    std::vector<SweepUnit> sunits;        // k_sweep work (eligible groups; the default line path)
+    SweepUnit *d_sunits = nullptr;
+    uint32_t *d_words = nullptr;          // k_words -> k_sweep candidate words, one chunk of frames
+    int32_t skstart[5] = {0, 0, 0, 0, 0}; // sunits of kind k at [skstart[k], skstart[k + 1])
+    int32_t sfgroup = 1;                  // k_sweep work order: frames per group
+    std::vector<LineUnit> units;          // k_line work (eligible groups, OCC_SWEEP=0)
     std::vector<TileDesc> all_tiles;      // k_tile work for every group (OCC_PATH_TILED)
     LineUnit *d_units = nullptr;
     TileDesc *d_all_tiles = nullptr;
@@ -151,7 +156,20 @@ void near_far(ViewDesc &vd, const occ_params &p) {
     }
 }
 
-#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return OCC_ERR_CUDA; } while (0)
+// CUDA errors map to OCC_ERR_CUDA; OCC_VERBOSE=1 prints the failing call
+bool occ_verbose() {
+    static const bool v = [] { const char *ev = getenv("OCC_VERBOSE"); return ev && atoi(ev) != 0; }();
+    return v;
+}
+#define CK(x)                                                                                       \
+    do {                                                                                            \
+        cudaError_t e_ = (x);                                                                       \
+        if (e_ != cudaSuccess) {                                                                    \
+            if (occ_verbose()) fprintf(stderr, "libocc: %s:%d %s -> %s\n", __FILE__, __LINE__, #x,   \
+                                       cudaGetErrorString(e_));                                     \
+            return OCC_ERR_CUDA;                                                                    \
+        }                                                                                           \
+    } while (0)
 
 // Brackets one launch with events when profiling; returns a CUDA error.
 struct ProfScope {
@@ -239,6 +257,42 @@ void add_line_units(occ_ctx *c, int32_t gi) {
     }
 }
 
+// Host copy of k_sweep's lane extent (s_extent): in-image positions of line
+// l0 + l (l0 a multiple of 32) in the sweep's coordinate tau.
+void sweep_extent(int32_t kind, int32_t l0, int32_t l, int32_t H, int32_t W, int32_t &lo, int32_t &hi) {
+    const int32_t L = l0 + l;
+    if (kind == 0) { lo = 0; hi = (L >= 0 && L < H) ? W : 0; }
+    else if (kind == 1) { lo = 0; hi = (L >= 0 && L < W) ? H : 0; }
+    else if (kind == 2) { lo = std::max(l, -l0); hi = std::min(W + l, H - l0); }
+    else { lo = std::max(31 - l, l0 + 32 - H); hi = std::min(W + 31 - l, l0 + 32); }
+    if (hi < lo) hi = lo;
+}
+
+void add_sweep_units(occ_ctx *c, int32_t gi, int32_t seg) {
+    const int32_t kind = c->fams[c->groups[gi].fam].kind;
+    const int32_t H = c->H, W = c->W;
+    int32_t lmin = 0, lmax = 0;
+    if (kind == 0) { lmin = 0; lmax = H - 1; }
+    else if (kind == 1) { lmin = 0; lmax = W - 1; }
+    else if (kind == 2) { lmin = -(W - 1); lmax = H - 1; }
+    else { lmin = 0; lmax = H + W - 2; }
+    for (int32_t l0 = lmin & ~31; l0 <= lmax; l0 += 32) {
+        int32_t tlo = INT32_MAX, thi = INT32_MIN;
+        for (int32_t l = 0; l < 32; ++l) {
+            int32_t lo, hi;
+            sweep_extent(kind, l0, l, H, W, lo, hi);
+            if (lo < hi) { tlo = std::min(tlo, lo); thi = std::max(thi, hi); }
+        }
+        if (tlo >= thi) continue;
+        const int32_t a = tlo & ~31, b = (thi + 31) & ~31;
+        for (int32_t t0 = a; t0 < b; t0 += seg) {
+            SweepUnit u{};
+            u.group = gi; u.l0 = l0; u.t0 = t0; u.t1 = std::min(t0 + seg, b);
+            c->sunits.push_back(u);
+        }
+    }
+}
+
 // View groups (<= 2 views of one family, +-b pairs of equal s first) and the
 // static tile list: for every group, blocks of 32 consecutive lines and
 // segments of kTilePositions positions covering the lines' in-image extent.
@@ -261,9 +315,43 @@ void build_tiles(occ_ctx *c) {
     }
     const int32_t H = c->H, W = c->W;
     std::vector<char> eligible(c->groups.size(), 0);
+    // k_sweep (default) or the round-1 k_line + k_cand path (OCC_SWEEP=0, kept for A/B runs)
+    static const bool sweep = [] { const char *ev = getenv("OCC_SWEEP"); return ev && atoi(ev) != 0; }();
     for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi) {
         eligible[gi] = line_eligible(c, c->groups[gi]);
-        if (eligible[gi]) add_line_units(c, gi);
+        if (eligible[gi] && !sweep) add_line_units(c, gi);
+    }
+    if (sweep) {
+        // segment length: 256 positions, halved while one call of max_batch
+        // frames would not fill the GPU (148 SMs x 16 warps)
+        int32_t seg = kSweepSeg;
+        for (;;) {
+            c->sunits.clear();
+            for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi)
+                if (eligible[gi]) add_sweep_units(c, gi, seg);
+            if (seg <= 32 || (double)c->sunits.size() * c->max_batch >= 148.0 * 16) break;
+            seg /= 2;
+        }
+        // by kind, longest first inside a kind (k_sweep's work order, k_sweep.cu)
+        auto kind_of = [&](const SweepUnit &x) { return c->fams[c->groups[x.group].fam].kind; };
+        std::stable_sort(c->sunits.begin(), c->sunits.end(), [&](const SweepUnit &x, const SweepUnit &y) {
+            if (kind_of(x) != kind_of(y)) return kind_of(x) < kind_of(y);
+            return x.t1 - x.t0 > y.t1 - y.t0;
+        });
+        for (int k = 0; k <= 4; ++k) {
+            int32_t n = 0;
+            for (const SweepUnit &x : c->sunits) n += kind_of(x) < k ? 1 : 0;
+            c->skstart[k] = n;
+        }
+        // frames per group: every kind's share of a group about one resident
+        // wave (148 SMs x 16 warps), and a group's D + words within ~80 MB of L2
+        int32_t kmin = INT32_MAX;
+        for (int k = 0; k < 4; ++k)
+            if (c->skstart[k + 1] > c->skstart[k]) kmin = std::min(kmin, c->skstart[k + 1] - c->skstart[k]);
+        const double fbytes = (double)H * W * 4.0 + 4.0 * (double)sweep_words_per_frame(H, W);
+        const int32_t by_wave = (int32_t)std::ceil(148.0 * 16 / std::max(1, kmin));
+        const int32_t by_l2 = std::max(1, (int32_t)(80.0e6 / fbytes));
+        c->sfgroup = std::max(1, std::min(by_wave, by_l2));
     }
     // segment length: 256 positions, shorter when a call of max_batch frames
     // would not fill the GPU (a unit is one warp's serial work, ~0.1 ms at
@@ -349,13 +437,13 @@ void build_tiles(occ_ctx *c) {
     }
 }
 
-// Capacity of the k_line -> k_hard queue: 1/64 of a chunk's pixel-views,
-// clamped to [64 Ki, 64 Mi] entries.  OCC_GQ_CAP (test knob, read at
+// Capacity of the k_line / k_sweep -> k_hard queue: 1/16 of a chunk's
+// pixel-views, clamped to [64 Ki, 256 Mi] entries.  OCC_GQ_CAP (test knob, read at
 // occ_create) overrides it, e.g. to force the capacity-overflow path.
 int32_t gq_capacity(int32_t chunk, int32_t H, int32_t W, int32_t n_views) {
     const char *ev = getenv("OCC_GQ_CAP");
     if (ev && atoi(ev) > 0) return atoi(ev);
-    return (int32_t)std::min<double>(64.0 * 1048576.0, std::max(65536.0, (double)chunk * H * W * n_views / 64.0));
+    return (int32_t)std::min<double>(256.0 * 1048576.0, std::max(65536.0, (double)chunk * H * W * n_views / 16.0));
 }
 
 }  // namespace
@@ -394,7 +482,8 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         // sets the launch count (L2 locality is per frame); measured at C5:
         // 256 MiB (25 frames) 53.1 ms/step, 1 GiB 51.5, 2 GiB (207 frames)
         // 51.3, 4 GiB (one launch) 52.4
-        const double per = (double)H * W * (4.0 + c->code_bytes);
+        const double per = (double)H * W * (4.0 + c->code_bytes) +
+                           (c->sunits.empty() ? 0.0 : 4.0 * (double)sweep_words_per_frame(H, W));
         const char *ev = getenv("OCC_CHUNK_MIB");          // tuning knob (default 2 GiB)
         const double budget = (ev ? std::max(1, atoi(ev)) : 2048) * 1048576.0;
         c->chunk = (int32_t)std::max(1.0, std::min((double)kMaxChunkFrames, std::floor(budget / per)));
@@ -411,9 +500,12 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         cudaMalloc(&c->d_units, sizeof(LineUnit) * std::max<size_t>(1, c->units.size())) != cudaSuccess ||
         cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess ||
         cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
-        (!c->units.empty() &&
+        ((!c->units.empty() || !c->sunits.empty()) &&
          (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = gq_capacity(c->chunk, H, W, n_views))) != cudaSuccess ||
-          cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess))) {
+          cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess)) ||
+        (!c->sunits.empty() &&
+         (cudaMalloc(&c->d_sunits, sizeof(SweepUnit) * c->sunits.size()) != cudaSuccess ||
+          cudaMalloc(&c->d_words, sizeof(uint32_t) * (size_t)c->chunk * (size_t)sweep_words_per_frame(H, W)) != cudaSuccess))) {
         cudaGetLastError();
         occ_destroy(c);
         return OCC_ERR_OOM;
@@ -430,7 +522,9 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
                                            sizeof(TileDesc) * c->all_tiles.size(),
                                            cudaMemcpyHostToDevice) != cudaSuccess) ||
         (c->units.size() && cudaMemcpy(c->d_units, c->units.data(), sizeof(LineUnit) * c->units.size(),
-                                       cudaMemcpyHostToDevice) != cudaSuccess)) {
+                                       cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (c->sunits.size() && cudaMemcpy(c->d_sunits, c->sunits.data(), sizeof(SweepUnit) * c->sunits.size(),
+                                        cudaMemcpyHostToDevice) != cudaSuccess)) {
         occ_destroy(c);
         return OCC_ERR_CUDA;
     }
@@ -677,17 +771,30 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
     const int64_t HW = (int64_t)c->H * c->W;
     const float *Dc = D + (int64_t)c0 * HW;
     uint8_t *Mc = M + (int64_t)c0 * c->V * c->mf.vbytes;
+    const bool tiled_only = c->path == OCC_PATH_TILED;
+    const bool nwin = c->neighbors > 0 || c->angles;
+    const bool sweep = !tiled_only && !nwin && !c->sunits.empty();
+    const TileDesc *tl = tiled_only ? c->d_all_tiles : c->d_tiles;
+    const int32_t nt = (int32_t)(tiled_only ? c->all_tiles.size() : c->tiles.size());
     {
         ProfScope ps(c, OCC_KERNEL_STATS, s);
-        CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
-                           c->d_stats + c0, c->d_codes, c->code_bytes, s)); ++launches;
+        if (sweep) {
+            CK(launch_words(Dc, c->H, c->W, n, c->params.e2_thresh, c->d_stats + c0, c->d_words, 1, s)); ++launches;
+            if (nt > 0) {    // k_tile's groups read the per-pixel codes
+                CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
+                                   c->d_stats + c0, c->d_codes, c->code_bytes, 0, s)); ++launches;
+            }
+        } else {
+            CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
+                               c->d_stats + c0, c->d_codes, c->code_bytes, 1, s)); ++launches;
+        }
         if (c->n_override > c0)    // imposed whole-frame statistics (spatial sharding)
             CK(cudaMemcpyAsync(c->d_stats + c0, c->d_override + c0,
                                sizeof(FrameStats) * (size_t)std::min(n, c->n_override - c0),
                                cudaMemcpyDeviceToDevice, s));
         ps.end();
     }
-    if (c->neighbors > 0 || c->angles) {   // finite N / real directions: per-window kernel (masks pre-zeroed)
+    if (nwin) {   // finite N / real directions: per-window kernel (masks pre-zeroed)
         ProfScope pn(c, OCC_KERNEL_NWIN, s);
         CK(launch_nwin(Dc, c->H, c->W, n, c->d_views, c->V, c->d_stats + c0, c->params, c->neighbors, Mc,
                        c->mf, c->d_codes, c->code_bytes, c->d_nwin_work, c->nwin_big, smax_of(c), c->angles,
@@ -696,8 +803,17 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         pn.end();
         return OCC_OK;
     }
-    const bool tiled_only = c->path == OCC_PATH_TILED;
-    if (!tiled_only && !c->units.empty()) {
+    if (sweep) {
+        ProfScope pl(c, OCC_KERNEL_LINE, s);
+        CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
+        CK(launch_sweep(Dc, c->H, c->W, n, c->d_sunits, (int32_t)c->sunits.size(), c->d_groups, c->d_views, c->V,
+                        c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_words, c->d_gq, c->d_gq_count,
+                        c->gq_cap, c->skstart, c->sfgroup, c->d_dbg, s));
+        CK(launch_hard(Dc, Mc, c->mf, c->W, HW, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
+                       c->gq_cap, c->d_stats + c0, c->nsm, s));
+        launches += 2;
+        pl.end();
+    } else if (!tiled_only && !c->units.empty()) {
         ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
         if (c->d_cand) {
@@ -713,8 +829,6 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         launches += 2;
         pl.end();
     }
-    const TileDesc *tl = tiled_only ? c->d_all_tiles : c->d_tiles;
-    const int32_t nt = (int32_t)(tiled_only ? c->all_tiles.size() : c->tiles.size());
     if (nt > 0) {
         ProfScope pt(c, OCC_KERNEL_TILE, s);
         CK(launch_tile(Dc, c->H, c->W, n, tl, nt, c->d_groups, c->d_views, c->V, c->d_fams,
@@ -970,6 +1084,8 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_tiles);
     cudaFree(c->d_all_tiles);
     cudaFree(c->d_units);
+    cudaFree(c->d_sunits);
+    cudaFree(c->d_words);
     cudaFree(c->d_dbg);
     cudaFree(c->d_gq);
     cudaFree(c->d_gq_count);

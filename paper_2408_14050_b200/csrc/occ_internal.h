@@ -190,6 +190,27 @@ cudaError_t launch_nwin(const float *D, int32_t H, int32_t W, int32_t frames, co
                         cudaStream_t s);
 cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames,
                             const FamilyDesc *fams_host, int32_t nfam, float e2_thresh,
-                            FrameStats *st, void *codes, int32_t code_bytes, cudaStream_t s);
+                            FrameStats *st, void *codes, int32_t code_bytes, int32_t do_stats, cudaStream_t s);
+// Line-sweep hot path (k_sweep.cu) for the rows / columns / diagonals /
+// anti-diagonals families: K0 words (stats + candidate words of the four
+// families, [frame][ceil(H/32)][ceil(W/32)][12][32] uint32) and one warp per
+// unit = 32 consecutive lines (l0 a multiple of 32) x [t0, t1) positions
+// (multiples of 32, t1 - t0 <= 256).
+struct SweepUnit {
+    int32_t group, l0, t0, t1;
+};
+constexpr int kSweepSeg = 256;
+inline int64_t sweep_words_per_frame(int32_t H, int32_t W) {
+    return (int64_t)((H + 31) / 32) * ((W + 31) / 32) * 12 * 32;
+}
+cudaError_t launch_words(const float *D, int32_t H, int32_t W, int32_t frames, float e2_thresh, FrameStats *st,
+                         uint32_t *words, int32_t do_stats, cudaStream_t s);
+size_t sweep_smem_bytes();
+cudaError_t launch_sweep(const float *D, int32_t H, int32_t W, int32_t frames, const SweepUnit *units,
+                         int32_t nunits, const GroupDesc *groups, const ViewDesc *views, int32_t nviews,
+                         const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
+                         const MaskFmt &mf, const uint32_t *words, HardEntry *gq, uint32_t *gq_count,
+                         int32_t gq_cap, const int32_t *kstart, int32_t fgroup, unsigned long long *dbg,
+                         cudaStream_t s);
 
 }  // namespace occ
