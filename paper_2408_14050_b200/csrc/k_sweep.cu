@@ -296,19 +296,26 @@ __device__ __forceinline__ int32_t s_stride(int kind, int32_t W) {
     return kind == 0 ? 1 : (kind == 1 ? W : (kind == 2 ? W + 1 : 1 - W));
 }
 
-// candidate word of view v (0: +b0, 1: -b0) for tau block k of the unit's lines
-template <int KIND>
-__device__ __forceinline__ uint32_t s_word(const SU &u, int32_t k, int v) {
-    const uint32_t *Wl = u.Wf + u.lane + 32 * v;
-    constexpr int kind = KIND;
-    if (kind == 0) return (uint32_t)k < (uint32_t)u.nxb ? __ldg(Wl + (u.A * u.nxb + k) * (kWordSlots * 32)) : 0u;
-    if (kind == 1) return (uint32_t)k < (uint32_t)u.nyb ? __ldg(Wl + (k * u.nxb + u.A) * (kWordSlots * 32) + 64) : 0u;
-    const int32_t m = kind == 2 ? u.A + k : u.A - k;
-    if ((uint32_t)m >= (uint32_t)u.nyb) return 0u;
-    const uint32_t *base = Wl + (m * u.nxb + k) * (kWordSlots * 32) + (kind == 2 ? 4 * 32 : 8 * 32);
-    uint32_t w = 0u;
-    if ((uint32_t)k < (uint32_t)u.nxb) w = __ldg(base);
-    if ((uint32_t)(k - 1) < (uint32_t)u.nxb) w |= __ldg(base - kWordSlots * 32 + 64);
+// candidate words of both views (x: +b0, y: -b0) for tau block k of the unit's lines
+__device__ __forceinline__ uint2 s_word2(const SU &u, int32_t k) {
+    const uint32_t *Wl = u.Wf + u.lane;
+    constexpr int St = kWordSlots * 32;
+    if (u.kind == 0) {
+        if ((uint32_t)k >= (uint32_t)u.nxb) return make_uint2(0u, 0u);
+        const uint32_t *p = Wl + (u.A * u.nxb + k) * St;
+        return make_uint2(__ldg(p), __ldg(p + 32));
+    }
+    if (u.kind == 1) {
+        if ((uint32_t)k >= (uint32_t)u.nyb) return make_uint2(0u, 0u);
+        const uint32_t *p = Wl + (k * u.nxb + u.A) * St + 64;
+        return make_uint2(__ldg(p), __ldg(p + 32));
+    }
+    const int32_t m = u.kind == 2 ? u.A + k : u.A - k;
+    uint2 w = make_uint2(0u, 0u);
+    if ((uint32_t)m >= (uint32_t)u.nyb) return w;
+    const uint32_t *p = Wl + (m * u.nxb + k) * St + (u.kind == 2 ? 4 * 32 : 8 * 32);
+    if ((uint32_t)k < (uint32_t)u.nxb) { w.x = __ldg(p); w.y = __ldg(p + 32); }
+    if ((uint32_t)(k - 1) < (uint32_t)u.nxb) { w.x |= __ldg(p - St + 64); w.y |= __ldg(p - St + 96); }
     return w;
 }
 
@@ -322,25 +329,25 @@ __device__ __forceinline__ uint32_t s_word(const SU &u, int32_t k, int v) {
 // need 16-byte aligned x and 128-byte aligned destinations: a row run would
 // take 256 bytes of shared memory).  Unaligned frames: 4-byte cp.async.
 // Returns whether the block was staged by TMA (then wait on the mbarrier).
-template <int KIND>
 __device__ __noinline__ bool s_stage(const SU &u, const SweepMaps &tm, float *slot, uint64_t *bar, int32_t k, int tma) {
     const int lane = u.lane;
     const float NaN = __int_as_float(0x7fc00000);
     const int32_t H = u.H, W = u.W;
-    if (tma && KIND <= 1) {
+    if (tma && u.kind <= 1) {
         if (lane == 0) {
             s_mbar_expect(bar, 4096u);
-            if (KIND == 0) s_tma3(slot, &tm.rows, 32 * k, u.l0, u.f, bar);
+            if (u.kind == 0) s_tma3(slot, &tm.rows, 32 * k, u.l0, u.f, bar);
             else s_tma3(slot, &tm.cols, u.l0, 32 * k, u.f, bar);
         }
         return true;
     }
-    if (tma && KIND >= 2) {        // 16-byte copies of the 4-aligned row runs
-#pragma unroll
+    if (tma) {                       // kinds 2, 3: 16-byte copies of the 4-aligned row runs
+        const int32_t dy = u.kind == 2 ? 32 * k : -32 * k;
+#pragma unroll 3
         for (int i = 0; i < 9; ++i) {
             const int c = lane + 32 * i, r = c / 9, q = c - 9 * r;
-            const int32_t y = KIND == 2 ? u.l0 + 32 * k + r : u.l0 + 31 - 32 * k - r;
-            const int32_t x = ((32 * k + r - 31) & ~3) + 4 * q;
+            const int32_t y = (u.kind == 2 ? u.l0 + r : u.l0 + 31 - r) + dy;
+            const int32_t x = 32 * k + ((r - 31) & ~3) + 4 * q;
             float *dst = slot + r * 36 + 4 * q;
             if ((uint32_t)x < (uint32_t)W && (uint32_t)y < (uint32_t)H) s_cp16(dst, u.Df + (int64_t)y * W + x);
             else *reinterpret_cast<float4 *>(dst) = make_float4(NaN, NaN, NaN, NaN);
@@ -351,9 +358,9 @@ __device__ __noinline__ bool s_stage(const SU &u, const SweepMaps &tm, float *sl
     for (int r = 0; r < 32; ++r) {
         const int32_t tau = 32 * k + r;
         float *dst;
-        if (KIND == 0) dst = slot + lane * 32 + ((((r >> 2) ^ (lane & 7)) << 2) | (r & 3));
-        else if (KIND == 1) dst = slot + r * 32 + lane;
-        else dst = slot + r * 36 + (KIND == 2 ? 31 - lane : lane) + ((r + 1) & 3);
+        if (u.kind == 0) dst = slot + lane * 32 + ((((r >> 2) ^ (lane & 7)) << 2) | (r & 3));
+        else if (u.kind == 1) dst = slot + r * 32 + lane;
+        else dst = slot + r * 36 + (u.kind == 2 ? 31 - lane : lane) + ((r + 1) & 3);
         if (tau >= u.elo && tau < u.ehi) s_cp4(dst, u.Df + u.B + (int64_t)tau * u.S);
         else *dst = NaN;
     }
@@ -370,9 +377,14 @@ __device__ __forceinline__ void s_stage_wait(uint64_t *bar, uint32_t &phase, boo
     __syncwarp();
 }
 
+// staged value at block position r of the line of lane l (see s_stage's layouts)
+__device__ __forceinline__ int s_at(int kind, int l, int r) {
+    if (kind == 0) return l * 32 + ((((r >> 2) ^ (l & 7)) << 2) | (r & 3));
+    if (kind == 1) return r * 32 + l;
+    return r * 36 + (kind == 2 ? 31 - l : l) + ((r + 1) & 3);
+}
 // the lane's staged values at positions 4g .. 4g + 3 (rb: the lane's read base)
-template <int kind>
-__device__ __forceinline__ float4 s_read4(const float *rb, int g, int sw) {
+__device__ __forceinline__ float4 s_read4(const float *rb, int kind, int g, int sw) {
     if (kind == 0) return *reinterpret_cast<const float4 *>(rb + ((g ^ sw) << 2));
     if (kind == 1) {
         const float *p = rb + g * 128;
@@ -381,12 +393,6 @@ __device__ __forceinline__ float4 s_read4(const float *rb, int g, int sw) {
     const float *p = rb + g * 144;
     return make_float4(p[1], p[36 + 2], p[72 + 3], p[108]);
 }
-template <int kind>
-__device__ __forceinline__ float s_read1(const float *rb, int r, int sw) {
-    if (kind == 0) return rb[((((r >> 2) ^ sw) << 2) | (r & 3))];
-    if (kind == 1) return rb[r * 32];
-    return rb[r * 36 + ((r + 1) & 3)];
-}
 // value at tau straight from global memory (NaN outside the line)
 __device__ __forceinline__ float s_gv(const SU &u, int32_t tau) {
     return (tau >= u.elo && tau < u.ehi) ? __ldg(u.Df + u.B + (int64_t)tau * u.S) : __int_as_float(0x7fc00000);
@@ -394,17 +400,16 @@ __device__ __forceinline__ float s_gv(const SU &u, int32_t tau) {
 
 // mask bits of one view for tau block k (bit r <-> tau = 32k + r), positions
 // outside the lane's line already cleared
-template <int KIND>
 __device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf, uint32_t word, int32_t k) {
     const int lane = u.lane;
     const int32_t H = u.H, W = u.W;
     if (mf.packed) {
         uint32_t *P = reinterpret_cast<uint32_t *>(Mv);
         const int32_t Wb = mf.Wb;
-        if (KIND == 0) {
+        if (u.kind == 0) {
             const int32_t y = u.l0 + lane;
             if (y < H && 32 * k >= 0 && 32 * k < W) P[(int64_t)y * Wb + k] = word;
-        } else if (KIND == 1) {
+        } else if (u.kind == 1) {
             const uint32_t t = s_transpose32(word, lane);
             const int32_t y = 32 * k + lane;
             if (y >= 0 && y < H && u.l0 < W) P[(int64_t)y * Wb + (u.l0 >> 5)] = t;
@@ -416,8 +421,8 @@ __device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf
                 if (r == lane) mine = b;
             }
             const int32_t tau = 32 * k + lane;
-            const int32_t y = KIND == 2 ? u.l0 + tau : u.l0 + 31 - tau;
-            const uint32_t run = KIND == 2 ? __brev(mine) : mine;      // bit j <-> x = tau - 31 + j
+            const int32_t y = u.kind == 2 ? u.l0 + tau : u.l0 + 31 - tau;
+            const uint32_t run = u.kind == 2 ? __brev(mine) : mine;      // bit j <-> x = tau - 31 + j
             if (run && y >= 0 && y < H) {
                 const int32_t x0 = tau - 31, w0 = x0 >> 5, sh = x0 & 31;
                 const uint32_t lo = run << sh, hi = sh ? (run >> (32 - sh)) : 0u;
@@ -427,46 +432,36 @@ __device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf
         }
         return;
     }
-    if (KIND == 0) {
-        const int32_t y = u.l0 + lane, x0 = 32 * k;
+    if (u.kind <= 1) {
+        // rows: the lane's 32 positions are one row segment; columns: the bit
+        // transpose gives lane r row 32k + r's 32 columns
+        const uint32_t t = u.kind == 0 ? word : s_transpose32(word, lane);
+        const int32_t y = u.kind == 0 ? u.l0 + lane : 32 * k + lane;
+        const int32_t x0 = u.kind == 0 ? 32 * k : u.l0;
         if (y >= H) return;
-        uint8_t *row = Mv + (int64_t)y * W;
+        uint8_t *row = Mv + (int64_t)y * W + x0;
         if ((W & 15) == 0 && x0 + 32 <= W) {
-            uint4 *d = reinterpret_cast<uint4 *>(row + x0);
-            __stcs(d, make_uint4(s_expand4(word & 15u), s_expand4((word >> 4) & 15u),
-                                 s_expand4((word >> 8) & 15u), s_expand4((word >> 12) & 15u)));
-            __stcs(d + 1, make_uint4(s_expand4((word >> 16) & 15u), s_expand4((word >> 20) & 15u),
-                                     s_expand4((word >> 24) & 15u), s_expand4(word >> 28)));
-        } else {
-            for (int r = 0; r < 32; ++r)
-                if (x0 + r < W) row[x0 + r] = (uint8_t)((word >> r) & 1u);
-        }
-    } else if (KIND == 1) {
-        const uint32_t t = s_transpose32(word, lane);      // lane r: row 32k + r, bit l = column l0 + l
-        const int32_t y = 32 * k + lane;
-        if (y >= H) return;
-        uint8_t *row = Mv + (int64_t)y * W + u.l0;
-        if ((W & 15) == 0 && u.l0 + 32 <= W) {
             uint4 *d = reinterpret_cast<uint4 *>(row);
             __stcs(d, make_uint4(s_expand4(t & 15u), s_expand4((t >> 4) & 15u), s_expand4((t >> 8) & 15u),
                                  s_expand4((t >> 12) & 15u)));
             __stcs(d + 1, make_uint4(s_expand4((t >> 16) & 15u), s_expand4((t >> 20) & 15u),
                                      s_expand4((t >> 24) & 15u), s_expand4(t >> 28)));
         } else {
-            for (int l = 0; l < 32; ++l)
-                if (u.l0 + l < W) row[l] = (uint8_t)((t >> l) & 1u);
+            for (int j = 0; j < 32; ++j)
+                if (x0 + j < W) row[j] = (uint8_t)((t >> j) & 1u);
         }
-    } else {
-        // one image row per tau: the 32 lanes write one contiguous run
-        uint8_t *dst = Mv + u.B + (int64_t)(32 * k) * u.S;
-        if (32 * k >= u.elo && 32 * k + 32 <= u.ehi) {
+        return;
+    }
+    // one image row per tau: the 32 lanes write one contiguous run
+    uint8_t *dst = Mv + u.B + (int64_t)(32 * k) * u.S;
+    const int64_t S = u.S;
+    if (32 * k >= u.elo && 32 * k + 32 <= u.ehi) {
 #pragma unroll 8
-            for (int r = 0; r < 32; ++r) __stcs(dst + (int64_t)r * u.S, (uint8_t)((word >> r) & 1u));
-        } else {
-            for (int r = 0; r < 32; ++r) {
-                const int32_t tau = 32 * k + r;
-                if (tau >= u.elo && tau < u.ehi) __stcs(dst + (int64_t)r * u.S, (uint8_t)((word >> r) & 1u));
-            }
+        for (int r = 0; r < 32; ++r) __stcs(dst + r * S, (uint8_t)((word >> r) & 1u));
+    } else {
+        for (int r = 0; r < 32; ++r) {
+            const int32_t tau = 32 * k + r;
+            if (tau >= u.elo && tau < u.ehi) __stcs(dst + r * S, (uint8_t)((word >> r) & 1u));
         }
     }
 }
@@ -485,10 +480,12 @@ __device__ __forceinline__ bool s_pair_far(float vq, float vp, int32_t j, float 
 }
 
 // exhaustive search of one survivor (queue full): offsets 3..J along the line
-__device__ __noinline__ bool s_exhaust(const SU &u, int32_t tau, int dir, int32_t J, float vp, float fs, int32_t s,
-                                       float tlo, float thi, const Params &p) {
+__device__ __noinline__ bool s_exhaust(const float *Df, int64_t B, int32_t S, int32_t elo, int32_t ehi, int32_t tau,
+                                       int dir, int32_t J, float vp, float fs, int32_t s, float tlo, float thi,
+                                       const Params &p) {
     for (int32_t j = 3; j <= J; ++j) {
-        const float vq = s_gv(u, tau + dir * j);
+        const int32_t t = tau + dir * j;
+        const float vq = (t >= elo && t < ehi) ? __ldg(Df + B + (int64_t)t * S) : __int_as_float(0x7fc00000);
         if (s_pair_far(vq, vp, j, fs, s, tlo, thi, p)) return true;
     }
     return false;
@@ -524,7 +521,7 @@ __device__ __forceinline__ int16_t s_rel(int32_t c, int32_t tau0, int32_t h) {
 }
 
 constexpr int kMaxSegBlocks = kSweepSeg / 32;
-constexpr int kListCap = 256;                 // dense survivor list (entries per block)
+constexpr int kListCap = 256;                 // dense survivor list (entries per pass)
 constexpr size_t kRecOff = sizeof(float) * kSlot * 2;
 constexpr size_t kListOff = kRecOff + sizeof(Rec) * 32 * kMaxSegBlocks;
 constexpr size_t kMarkOff = kListOff + sizeof(uint16_t) * kListCap;
@@ -534,9 +531,6 @@ size_t sweep_smem_bytes() { return kSweepWarpSmem; }
 
 __device__ __forceinline__ int32_t s_guess(float vw, float vp, float fs, int32_t J) {
     return min(max(__float2int_rn(fminf(fmaxf(__fmul_rn(fs, __fsub_rn(vw, vp)), -1e9f), 1e9f)), 3), J);
-}
-__device__ __forceinline__ float s_sel4(int r, float a0, float a1, float a2, float a3) {
-    return r >= 16 ? (r >= 24 ? a3 : a2) : (r >= 8 ? a1 : a0);
 }
 
 struct SurvCtx {
@@ -551,34 +545,16 @@ struct SurvCtx {
     int32_t vP, vN;
 };
 
-// value of lane src's line at block position r of the staged slot
-template <int kind>
-__device__ __forceinline__ float s_slot_at(const float *slot, int src, int r) {
-    if (kind == 0) return slot[src * 32 + ((((r >> 2) ^ (src & 7)) << 2) | (r & 3))];
-    if (kind == 1) return slot[r * 32 + src];
-    return slot[r * 36 + (kind == 2 ? 31 - src : src) + ((r + 1) & 3)];
-}
-
-// Dense resolution of one block's far survivors (Eq. 5 far pairs,
-// PAPER.md:131-142): the survivors of all lanes are listed lane-major in
-// shared memory (entry = r | view << 5 | lane << 6) and processed 32 per
-// round; a round reads the owner lane's window words and witnesses by
-// shuffles.  For survivor i of view +b (-b): the partner offset j must lie in
-// [3, J], J = dcov(i) (S8) clipped to the line; the probe is at the
-// witness guess j = s (v_w - v_i), then at the fixed point s (v(q) - v_i)
-// of the probed value; a miss goes to k_hard's queue.  Hits are OR-ed into
-// the owner's mask word through shared-memory atomics.
 // one listed survivor, decoded with its owner lane's context (warp-collective: shuffles)
 struct SurvDec {
     int64_t B;                 // owner line's pixel index at tau = 0
-    int32_t i, J, dir;         // position, largest partner offset, partner direction (+1: +b, -1: -b)
-    float vp, vw;              // v(i), witness value (partner guess)
+    int32_t i, J, dir, j1;     // position, largest partner offset, direction (+1: +b), probe offset
+    float vp;                  // v(i)
     int src, r, view;
     bool ok;                   // a listed survivor with J >= 3
 };
-template <int KIND>
 __device__ __forceinline__ SurvDec s_decode(const SU &u, const float *slot, const SurvCtx &c, const uint16_t *list,
-                                            uint32_t tot, uint32_t e) {
+                                            uint32_t tot, uint32_t e, uint32_t Blo, uint32_t Bhi) {
     SurvDec d;
     const bool valid = e < tot;
     const uint32_t ent = valid ? list[e] : 0u;
@@ -589,149 +565,127 @@ __device__ __forceinline__ SurvDec s_decode(const SU &u, const float *slot, cons
     const float q0 = __shfl_sync(FULL, c.Q0, src), q1 = __shfl_sync(FULL, c.Q1, src);
     const float q2 = __shfl_sync(FULL, c.Q2, src), q3 = __shfl_sync(FULL, c.Q3, src);
     const uint32_t vwb = __shfl_sync(FULL, *reinterpret_cast<const uint32_t *>(&c.VW), src);
-    int32_t elo, ehi;
-    s_extent(KIND, u.l0, src, u.H, u.W, elo, ehi);
-    d.B = s_base(KIND, u.l0, src, u.W);
+    const int32_t elo = __shfl_sync(FULL, u.elo, src), ehi = __shfl_sync(FULL, u.ehi, src);
+    d.B = (int64_t)(((uint64_t)__shfl_sync(FULL, Bhi, src) << 32) | __shfl_sync(FULL, Blo, src));
     d.i = c.tau0 + r;
-    d.vp = s_slot_at<KIND>(slot, src, r);
+    d.vp = slot[s_at(u.kind, src, r)];
+    float vw;
     if (d.view == 0) {
         const uint32_t m = wp & s_le(r);
         const int32_t pc = m ? c.tau0 + c.h + 31 - __clz(m) : pcl;
         d.J = min(pc + c.h - d.i, ehi - 1 - d.i);
         d.dir = 1;
-        d.vw = s_sel4(r, q0, q1, q2, q3);
+        vw = r >= 16 ? (r >= 24 ? q3 : q2) : (r >= 8 ? q1 : q0);
     } else {
         const uint32_t m = wn & s_ge(r);
         const int32_t nc = m ? c.tau0 - c.h + __ffs(m) - 1 : ncl;
         d.J = min(d.i + c.h - nc, d.i - elo);
         d.dir = -1;
         const __half2 h2 = *reinterpret_cast<const __half2 *>(&vwb);
-        d.vw = r >= 16 ? __high2float(h2) : __low2float(h2);
+        vw = r >= 16 ? __high2float(h2) : __low2float(h2);
     }
     d.ok = valid && d.J >= 3;
+    d.j1 = s_guess(vw, d.vp, c.fs, d.J);
     return d;
 }
 
-template <int KIND>
+// Dense resolution of one block's far survivors (Eq. 5 far pairs,
+// PAPER.md:131-142): the survivors of all lanes are listed lane-major in
+// shared memory (entry = r | view << 5 | lane << 6) and resolved 32 per
+// round, whatever lanes own them; a round reads the owner's window words,
+// witnesses and line by shuffles.  For survivor i of view +b (-b) the
+// partner offset j lies in [3, J], J = dcov(i) (S8) clipped to the line; the
+// probe is at the witness guess j = s (v_w - v_i) (all probes of the block in
+// flight together); a miss goes to k_hard's queue.  Hits are OR-ed into the
+// owner's mask word by shared-memory atomics.
 __device__ __noinline__ void s_resolve(const SweepArgs &a, const SU &u, const float *slot, const SurvCtx &c,
                                        uint32_t sP, uint32_t sN, uint32_t &mP, uint32_t &mN, uint16_t *list,
                                        uint32_t *marks) {
     const int lane = u.lane;
-    constexpr int kind = KIND;
     const float NaN = __int_as_float(0x7fc00000);
     marks[lane] = 0u;
     marks[32 + lane] = 0u;
     // (rare) more survivors than the list holds: blocks of 4 positions in
     // turn (at most 4 x 64 = 256 <= kListCap entries each)
-    const int rw = __reduce_add_sync(FULL, __popc(sP) + __popc(sN)) > (uint32_t)kListCap ? 4 : 32;
     static_assert(4 * 64 <= kListCap, "list capacity");
-    const uint32_t sP0 = sP, sN0 = sN;
+    const int rw = __reduce_add_sync(FULL, __popc(sP) + __popc(sN)) > (uint32_t)kListCap ? 4 : 32;
+    const uint32_t Blo = (uint32_t)u.B, Bhi = (uint32_t)((uint64_t)u.B >> 32);
     for (int rlo = 0; rlo < 32; rlo += rw) {
-    const uint32_t pm = s_ge(rlo) & s_le(rlo + rw - 1);
-    sP = sP0 & pm;
-    sN = sN0 & pm;
-    // lane-major list: counts, exclusive prefix
-    const uint32_t n = __popc(sP) + __popc(sN);
-    uint32_t inc = n;
+        const uint32_t pm = s_ge(rlo) & s_le(rlo + rw - 1);
+        const uint32_t tP = sP & pm, tN = sN & pm;
+        const uint32_t n = __popc(tP) + __popc(tN);
+        uint32_t inc = n;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, inc, o);
-        if (lane >= o) inc += t;
-    }
-    const uint32_t tot = __shfl_sync(FULL, inc, 31);
-    {
-        uint32_t o = inc - n;
-        const uint16_t tag = (uint16_t)(lane << 6);
-        uint32_t t = sP;
-        while (t) { list[o++] = (uint16_t)(tag | (__ffs(t) - 1)); t &= t - 1u; }
-        t = sN;
-        while (t) { list[o++] = (uint16_t)(tag | 32 | (__ffs(t) - 1)); t &= t - 1u; }
-    }
-    __syncwarp();
-    // rounds of 32 entries, 4 rounds at a time: all their probe loads are in
-    // flight together (the probes are L2 latency bound)
-    for (uint32_t b0 = 0; b0 < tot; b0 += 4 * 32) {
-        SurvDec d[4];
-        float vq[4], w2[4];
-        int32_t j1[4], j2[4];
-        bool hit[4], p2[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            d[q] = s_decode<KIND>(u, slot, c, list, tot, b0 + 32 * q + lane);
-            j1[q] = s_guess(d[q].vw, d[q].vp, c.fs, d[q].J);
-            vq[q] = d[q].ok ? __ldg(u.Df + d[q].B + (int64_t)(d[q].i + d[q].dir * j1[q]) * u.S) : NaN;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += t;
         }
-        bool any2 = false;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            hit[q] = d[q].ok && s_pair_far(vq[q], d[q].vp, j1[q], c.fs, c.s, c.tlo, c.thi, a.p);
-            SST(3 + d[q].view, hit[q]);
-            j2[q] = s_guess(vq[q], d[q].vp, c.fs, d[q].J);
-            p2[q] = d[q].ok && !hit[q] && vq[q] == vq[q] && j2[q] != j1[q];
-            any2 = any2 || p2[q];
+        const uint32_t tot = __shfl_sync(FULL, inc, 31);
+        {
+            uint32_t o = inc - n;
+            const uint32_t tag = (uint32_t)lane << 6;
+            uint32_t t = tP;
+            while (t) { list[o++] = (uint16_t)(tag | (__ffs(t) - 1)); t &= t - 1u; }
+            t = tN;
+            while (t) { list[o++] = (uint16_t)(tag | 32 | (__ffs(t) - 1)); t &= t - 1u; }
         }
-        SST(9, lane == 0);
-        if (__any_sync(FULL, any2)) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                w2[q] = p2[q] ? __ldg(u.Df + d[q].B + (int64_t)(d[q].i + d[q].dir * j2[q]) * u.S) : NaN;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const bool h2 = p2[q] && s_pair_far(w2[q], d[q].vp, j2[q], c.fs, c.s, c.tlo, c.thi, a.p);
-                SST(5 + d[q].view, h2);
-                hit[q] = hit[q] || h2;
+        __syncwarp();
+        for (uint32_t b0 = 0; b0 < tot; b0 += 32) {
+            const SurvDec d = s_decode(u, slot, c, list, tot, b0 + lane, Blo, Bhi);
+            const float vq = d.ok ? __ldg(u.Df + d.B + (int64_t)(d.i + d.dir * d.j1) * u.S) : NaN;
+            bool hit = d.ok && s_pair_far(vq, d.vp, d.j1, c.fs, c.s, c.tlo, c.thi, a.p);
+            SST(3 + d.view, hit);
+            SST(9, lane == 0);
+#ifndef SWEEP_PROBE2
+#define SWEEP_PROBE2 0
+#endif
+            if (SWEEP_PROBE2) {       // (measured slower: its latency costs more than k_hard's extra work)
+                const int32_t j2 = s_guess(vq, d.vp, c.fs, d.J);
+                const bool p2 = d.ok && !hit && vq == vq && j2 != d.j1;
+                if (__any_sync(FULL, p2)) {
+                    const float w2 = p2 ? __ldg(u.Df + d.B + (int64_t)(d.i + d.dir * j2) * u.S) : NaN;
+                    const bool h2 = p2 && s_pair_far(w2, d.vp, j2, c.fs, c.s, c.tlo, c.thi, a.p);
+                    SST(5 + d.view, h2);
+                    hit = hit || h2;
+                }
             }
-        }
-        uint32_t bq[4], nq = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (hit[q]) atomicOr(marks + 32 * d[q].view + d[q].src, 1u << d[q].r);
-            const bool miss = d[q].ok && !hit[q];
-            SST(7 + d[q].view, miss);
-            bq[q] = __ballot_sync(FULL, miss);
-            nq += __popc(bq[q]);
-        }
-        if (nq) {
-            uint32_t base = 0u;
-            if (lane == 0) base = atomicAdd(a.gq_count, nq);
-            base = __shfl_sync(FULL, base, 0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if ((bq[q] >> lane) & 1u) {
-                    const uint32_t slotq = base + __popc(bq[q] & ((1u << lane) - 1u));
-                    const int vid = d[q].view ? c.vN : c.vP;
+            if (hit) atomicOr(marks + 32 * d.view + d.src, 1u << d.r);
+            const bool q = d.ok && !hit;
+            SST(7 + d.view, q);
+            const uint32_t bq = __ballot_sync(FULL, q);
+            if (bq) {
+                uint32_t base = 0u;
+                if (lane == 0) base = atomicAdd(a.gq_count, __popc(bq));
+                base = __shfl_sync(FULL, base, 0);
+                if (q) {
+                    const uint32_t slotq = base + __popc(bq & ((1u << lane) - 1u));
+                    const int vid = d.view ? c.vN : c.vP;
                     if (slotq < (uint32_t)a.gq_cap) {
                         HardEntry he;
-                        he.pix = (int32_t)(d[q].B + (int64_t)d[q].i * u.S);
-                        he.meta = (uint32_t)d[q].J | ((uint32_t)u.f << 17) | ((uint32_t)vid << 25);
+                        he.pix = (int32_t)(d.B + (int64_t)d.i * u.S);
+                        he.meta = (uint32_t)d.J | ((uint32_t)u.f << 17) | ((uint32_t)vid << 25);
                         a.gq[slotq] = he;
                     } else {
-                        SU o = u;
-                        int32_t elo, ehi;
-                        s_extent(KIND, u.l0, d[q].src, u.H, u.W, elo, ehi);
-                        o.B = d[q].B; o.elo = elo; o.ehi = ehi;
-                        if (s_exhaust(o, d[q].i, d[q].dir, d[q].J, d[q].vp, c.fs, c.s, c.tlo, c.thi, a.p))
-                            atomicOr(marks + 32 * d[q].view + d[q].src, 1u << d[q].r);
+                        const int32_t elo = d.dir > 0 ? -(1 << 30) : d.i - d.J, ehi = d.dir > 0 ? d.i + d.J + 1 : (1 << 30);
+                        if (s_exhaust(u.Df, d.B, u.S, elo, ehi, d.i, d.dir, d.J, d.vp, c.fs, c.s, c.tlo, c.thi, a.p))
+                            atomicOr(marks + 32 * d.view + d.src, 1u << d.r);
                     }
                 }
-                base += __popc(bq[q]);
             }
         }
-    }
-    __syncwarp();
+        __syncwarp();
     }
     mP |= marks[lane];
     mN |= marks[32 + lane];
     __syncwarp();
 }
 
-template <int KIND>
 __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm, const SweepUnit &un,
                                         const GroupDesc &gd, int32_t f, unsigned char *smem, uint32_t *phase) {
     const FamilyDesc &fd = a.fams[gd.fam];
     SU u;
-    u.kind = KIND;
-    constexpr int kind = KIND;
+    u.kind = fd.kind;
+    const int kind = u.kind;
     u.l0 = un.l0;
     u.A = un.l0 >> 5;
     u.lane = threadIdx.x & 31;
@@ -748,7 +702,7 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kBarOff);
     const int32_t T0 = un.t0, T1 = un.t1;         // multiples of 32
     const int32_t kB = T0 >> 5, kT = (T1 >> 5) - 1;
-    // read base of the lane in a slot (kind 0: its row; 1: its column; 2, 3: its element of the row runs)
+    // the lane's read base in a slot (kind 0: its row; 1: its column; 2, 3: its element of the row runs)
     const int32_t rbo = kind == 0 ? lane * 32 : (kind == 2 ? 31 - lane : lane);
     const int sw = lane & 7;
 
@@ -777,7 +731,7 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
     {
         const float M = fmaxf(fabsf(key_float(fs.minkey)), fabsf(key_float(fs.maxkey)));
         const double P = 32.0 * (nbl + 2);
-        const double eps = ldexp(1.0, -23) * (double)(2 * nbl + 5) * ((double)s * (double)M + P + (double)a.p.t_dist + 1.0);
+        const double eps = ldexp(1.0, -23) * (double)(8 * nbl + 5) * ((double)s * (double)M + P + (double)a.p.t_dist + 1.0);
         T = __double2float_ru(__dadd_rn((double)a.p.t_dist, eps));
     }
     const float tlo = __fsub_rn(a.p.t_dist, 0x1p-10f), thi = __fadd_rn(a.p.t_dist, 0x1p-10f);
@@ -800,25 +754,25 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
 
     // ------------------------------------------------ pass 1 (ascending)
     // Far filter of view -b: SY = max over q <= i - 3 of A'(q) = s v(q) + (q -
-    // base), base = the current half-block's first position (A' shifted by
-    // -16 per half-block).  Also the last candidates the windows need.
+    // base), base = the first position of the current group of 4 (A' shifted
+    // by -4 per group).  Also the last candidates the windows need:
+    // P window [tau0 + h - 32, tau0 + h - 1] (word k + hq - 1, shift hr), N
+    // window [tau0 - h, tau0 + 31 - h] (word k + nq, shift nsh).
     {
         const int32_t kS = max(kB - nbr, kEmin);           // first staged block
-        // word tracking: P window [tau0 + h - 32, tau0 + h - 1] (word k + hq - 1,
-        // shift hr), N window [tau0 - h, tau0 + 31 - h] (word k + nq, shift nsh)
         const int32_t kW = min(kS, kB - ((2 * h + 63) >> 5));
         int32_t pcl = NONE_LO, lc = NONE_LO;
-        uint32_t pw_lo = s_word<KIND>(u, kW + hq - 1, 0), nw_lo = s_word<KIND>(u, kW + nq, 1);
-        uint32_t pw_nx = s_word<KIND>(u, kW + hq, 0), nw_nx = s_word<KIND>(u, kW + nq + 1, 1);   // prefetched
+        uint32_t pw_lo = s_word2(u, kW + hq - 1).x, nw_lo = s_word2(u, kW + nq).y;
+        uint32_t pw_nx = s_word2(u, kW + hq).x, nw_nx = s_word2(u, kW + nq + 1).y;   // prefetched
         float A1 = NaN, A2 = NaN, A3 = NaN, w1 = NaN, w2 = NaN, w3 = NaN, SY = -INFINITY, VM = NaN;
         uint32_t XN = 0u;
         int slot = 0;
         bool bt[2] = {false, false};
-        if (kS <= kT) bt[0] = s_stage<KIND>(u, tm, stg, bars, kS, tma);
+        if (kS <= kT) bt[0] = s_stage(u, tm, stg, bars, kS, tma);
         for (int32_t k = kW; k <= kT; ++k) {
             const uint32_t pw_hi = pw_nx, nw_hi = nw_nx;
-            pw_nx = s_word<KIND>(u, k + 1 + hq, 0);
-            nw_nx = s_word<KIND>(u, k + 1 + nq + 1, 1);
+            pw_nx = s_word2(u, k + 1 + hq).x;
+            nw_nx = s_word2(u, k + 1 + nq + 1).y;
             const uint32_t WP = __funnelshift_r(pw_lo, pw_hi, hr);
             pw_lo = pw_hi;
             if (WP) pcl = 32 * k + h - 32 + 31 - __clz(WP);
@@ -827,31 +781,29 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
             if (WN) lc = 32 * k - h + 31 - __clz(WN);
             if (k < kS) continue;
             s_stage_wait(bars + slot, phase[slot], bt[slot]);
-            if (k + 1 <= kT) bt[slot ^ 1] = s_stage<KIND>(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k + 1, tma);
+            if (k + 1 <= kT) bt[slot ^ 1] = s_stage(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k + 1, tma);
             const float *rb = stg + slot * kSlot + rbo;
             float Q0 = NaN, Q2 = NaN;
             if (vN >= 0) {
 #pragma unroll 1
-                for (int hb = 0; hb < 2; ++hb) {
-                    SY = __fsub_rn(SY, 16.0f);
-                    A1 = __fsub_rn(A1, 16.0f); A2 = __fsub_rn(A2, 16.0f); A3 = __fsub_rn(A3, 16.0f);
+                for (int g = 0; g < 8; ++g) {
+                    SY = __fsub_rn(SY, 4.0f);
+                    A1 = __fsub_rn(A1, 4.0f); A2 = __fsub_rn(A2, 4.0f); A3 = __fsub_rn(A3, 4.0f);
+                    const float4 q4 = s_read4(rb, kind, g, sw);
+                    const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
                     float qa = NaN;
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        const float4 q4 = s_read4<KIND>(rb, 4 * hb + g, sw);
-                        const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float v0 = vv[e];
-                            const float A0 = __fmaf_rn(fs_, v0, (float)(4 * g + e));
-                            if (A3 > SY) { SY = A3; VM = w3; }
-                            XN = s_push(XN, __fsub_rn(__fsub_rn(A0, T), SY));
-                            if (g == 0 && e == 0) qa = VM;
-                            A3 = A2; A2 = A1; A1 = A0;
-                            w3 = w2; w2 = w1; w1 = v0;
-                        }
+                    for (int e = 0; e < 4; ++e) {
+                        const float v0 = vv[e];
+                        const float A0 = __fmaf_rn(fs_, v0, (float)e);
+                        if (A3 > SY) { SY = A3; VM = w3; }
+                        XN = s_push(XN, __fsub_rn(__fsub_rn(A0, T), SY));
+                        if (e == 0) qa = VM;
+                        A3 = A2; A2 = A1; A1 = A0;
+                        w3 = w2; w2 = w1; w1 = v0;
                     }
-                    if (hb) Q2 = qa; else Q0 = qa;
+                    if (g == 0) Q0 = qa;
+                    if (g == 4) Q2 = qa;
                 }
             }
             __syncwarp();
@@ -874,18 +826,18 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
         const int32_t kS = min(kT + nbr, kEmax);            // first staged block (from the top)
         const int32_t kW = max(kS, kT + 2 + ((2 * h + 31) >> 5));
         int32_t fc = NONE_HI, ncl = NONE_HI;
-        uint32_t pw_hi = s_word<KIND>(u, kW + hq + 1, 0), nw_hi = s_word<KIND>(u, kW + nq + 1, 1);
-        uint32_t pw_nx = s_word<KIND>(u, kW + hq, 0), nw_nx = s_word<KIND>(u, kW + nq, 1);   // prefetched
+        uint32_t pw_hi = s_word2(u, kW + hq + 1).x, nw_hi = s_word2(u, kW + nq + 1).y;
+        uint32_t pw_nx = s_word2(u, kW + hq).x, nw_nx = s_word2(u, kW + nq).y;   // prefetched
         uint32_t WNprev = 0u;
         float v1 = NaN, v2 = NaN, v3 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY, VM = NaN;
         int slot = 0;
         bool bt[2] = {false, false};
-        bt[0] = s_stage<KIND>(u, tm, stg, bars, kS, tma);
+        bt[0] = s_stage(u, tm, stg, bars, kS, tma);
         for (int32_t k = kW; k >= kB; --k) {
             const int32_t tau0 = 32 * k;
             const uint32_t pw_lo = pw_nx, nw_lo = nw_nx;
-            pw_nx = s_word<KIND>(u, k - 1 + hq, 0);
-            nw_nx = s_word<KIND>(u, k - 1 + nq, 1);
+            pw_nx = s_word2(u, k - 1 + hq).x;
+            nw_nx = s_word2(u, k - 1 + nq).y;
             const uint32_t WP = __funnelshift_r(pw_lo, pw_hi, hr);      // +b candidates [tau0 + h, tau0 + h + 31]
             pw_hi = pw_lo;
             if (WP) fc = tau0 + h + __ffs(WP) - 1;
@@ -895,26 +847,23 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
             WNprev = WN;
             if (k > kS) continue;
             s_stage_wait(bars + slot, phase[slot], bt[slot]);
-            if (k - 1 >= kB) bt[slot ^ 1] = s_stage<KIND>(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k - 1, tma);
+            if (k - 1 >= kB) bt[slot ^ 1] = s_stage(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k - 1, tma);
             const float *rb = stg + slot * kSlot + rbo;
             if (k > kT) {
                 // warm-up: far filter of +b only
 #pragma unroll 1
-                for (int hb = 1; hb >= 0; --hb) {
-                    SX = __fsub_rn(SX, 16.0f);
-                    A1 = __fsub_rn(A1, 16.0f); A2 = __fsub_rn(A2, 16.0f); A3 = __fsub_rn(A3, 16.0f);
+                for (int g = 7; g >= 0; --g) {
+                    SX = __fsub_rn(SX, 4.0f);
+                    A1 = __fsub_rn(A1, 4.0f); A2 = __fsub_rn(A2, 4.0f); A3 = __fsub_rn(A3, 4.0f);
+                    const float4 q4 = s_read4(rb, kind, g, sw);
+                    const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-                    for (int g = 3; g >= 0; --g) {
-                        const float4 q4 = s_read4<KIND>(rb, 4 * hb + g, sw);
-                        const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-                        for (int e = 3; e >= 0; --e) {
-                            const float v0 = vv[e];
-                            const float A0 = __fmaf_rn(fs_, v0, -(float)(4 * g + e));
-                            if (A3 > SX) { SX = A3; VM = v3; }
-                            A3 = A2; A2 = A1; A1 = A0;
-                            v3 = v2; v2 = v1; v1 = v0;
-                        }
+                    for (int e = 3; e >= 0; --e) {
+                        const float v0 = vv[e];
+                        const float A0 = __fmaf_rn(fs_, v0, -(float)e);
+                        if (A3 > SX) { SX = A3; VM = v3; }
+                        A3 = A2; A2 = A1; A1 = A0;
+                        v3 = v2; v2 = v1; v1 = v0;
                     }
                 }
                 __syncwarp();
@@ -926,36 +875,35 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
             uint32_t Xs1 = 0, Xg1 = 0, Xl1 = 0, Xlf = 0, Xs2 = 0, Xg2 = 0, Xl2 = 0, XFR = 0;
             float Q0 = NaN, Q1 = NaN, Q2 = NaN, Q3 = NaN;   // +b witness values after positions 7, 15, 23, 31
 #pragma unroll 1
-            for (int hb = 1; hb >= 0; --hb) {
-                SX = __fsub_rn(SX, 16.0f);
-                A1 = __fsub_rn(A1, 16.0f); A2 = __fsub_rn(A2, 16.0f); A3 = __fsub_rn(A3, 16.0f);
-                float qa = NaN, qb = NaN;
+            for (int g = 7; g >= 0; --g) {
+                SX = __fsub_rn(SX, 4.0f);
+                A1 = __fsub_rn(A1, 4.0f); A2 = __fsub_rn(A2, 4.0f); A3 = __fsub_rn(A3, 4.0f);
+                const float4 q4 = s_read4(rb, kind, g, sw);
+                const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
+                float qa = NaN;
 #pragma unroll
-                for (int g = 3; g >= 0; --g) {
-                    const float4 q4 = s_read4<KIND>(rb, 4 * hb + g, sw);
-                    const float vv[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-                    for (int e = 3; e >= 0; --e) {
-                        const float v0 = vv[e];
-                        const float d1 = __fsub_rn(v1, v0), d2 = __fsub_rn(v2, v0);
-                        const float e1 = fabsf(d1), e2 = fabsf(d2);
-                        Xs1 = s_push(Xs1, d1);
-                        Xg1 = s_push(Xg1, __fsub_rn(e1, a1n));
-                        Xl1 = s_push(Xl1, __fsub_rn(e1, bhi0));
-                        Xlf = s_push(Xlf, __fsub_rn(e1, fhi0));
-                        Xs2 = s_push(Xs2, d2);
-                        Xg2 = s_push(Xg2, __fsub_rn(e2, a2n));
-                        Xl2 = s_push(Xl2, __fsub_rn(e2, bhi1));
-                        const float A0 = __fmaf_rn(fs_, v0, -(float)(4 * g + e));
-                        if (A3 > SX) { SX = A3; VM = v3; }
-                        XFR = s_push(XFR, __fsub_rn(__fsub_rn(A0, T), SX));
-                        if (g == 3 && e == 3) qb = VM;
-                        if (g == 1 && e == 3) qa = VM;
-                        A3 = A2; A2 = A1; A1 = A0;
-                        v3 = v2; v2 = v1; v1 = v0;
-                    }
+                for (int e = 3; e >= 0; --e) {
+                    const float v0 = vv[e];
+                    const float d1 = __fsub_rn(v1, v0), d2 = __fsub_rn(v2, v0);
+                    const float e1 = fabsf(d1), e2 = fabsf(d2);
+                    Xs1 = s_push(Xs1, d1);
+                    Xg1 = s_push(Xg1, __fsub_rn(e1, a1n));
+                    Xl1 = s_push(Xl1, __fsub_rn(e1, bhi0));
+                    Xlf = s_push(Xlf, __fsub_rn(e1, fhi0));
+                    Xs2 = s_push(Xs2, d2);
+                    Xg2 = s_push(Xg2, __fsub_rn(e2, a2n));
+                    Xl2 = s_push(Xl2, __fsub_rn(e2, bhi1));
+                    const float A0 = __fmaf_rn(fs_, v0, -(float)e);
+                    if (A3 > SX) { SX = A3; VM = v3; }
+                    XFR = s_push(XFR, __fsub_rn(__fsub_rn(A0, T), SX));
+                    if (e == 3) qa = VM;
+                    A3 = A2; A2 = A1; A1 = A0;
+                    v3 = v2; v2 = v1; v1 = v0;
                 }
-                if (hb) { Q2 = qa; Q3 = qb; } else { Q0 = qa; Q1 = qb; }
+                if (g == 7) Q3 = qa;
+                if (g == 5) Q2 = qa;
+                if (g == 3) Q1 = qa;
+                if (g == 1) Q0 = qa;
             }
             // v1 = v(tau0), v2 = v(tau0 + 1)
             const float d1m = __fsub_rn(v1, vm1), d2m1 = __fsub_rn(v2, vm1), d2m2 = __fsub_rn(v1, vm2);
@@ -990,39 +938,35 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
             uint32_t mN = (n1 & cN1) | (n2 & cN2);
             if (NFWD) mN |= (TF & ~Xs1) & cNf;
             mN &= ext;
-            uint32_t sP = vP >= 0 ? (XFR & cP3 & ~mP & ext) : 0u;
-            uint32_t sN = vN >= 0 ? (rr.XN & cN3 & ~mN & ext) : 0u;
+            const uint32_t sP = vP >= 0 ? (XFR & cP3 & ~mP & ext) : 0u;
+            const uint32_t sN = vN >= 0 ? (rr.XN & cN3 & ~mN & ext) : 0u;
             SST(0, __popc(ext));
             SST(1, __popc(sP));
             SST(2, __popc(sN));
             SST(10, __popc(mP));
             SST(11, __popc(mN));
-            // far survivors: a witness-guided exact probe, then one fixed-point
-            // step j <- s (v(q) - v(i)) from the probed value; the rest to k_hard.
-            // Densely: the warp's survivors are listed (lane-major) and resolved
-            // 32 per round, whatever lanes they belong to.
             if (__any_sync(FULL, (sP | sN) != 0u)) {
                 SurvCtx sc;
                 sc.tau0 = tau0; sc.h = h; sc.WP = WP; sc.WN = WN; sc.pcl = pcl; sc.ncl = ncl;
                 sc.Q0 = Q0; sc.Q1 = Q1; sc.Q2 = Q2; sc.Q3 = Q3; sc.VW = rr.VW;
                 sc.fs = fs_; sc.s = s; sc.tlo = tlo; sc.thi = thi; sc.vP = vP; sc.vN = vN;
-                s_resolve<KIND>(a, u, stg + slot * kSlot, sc, sP, sN, mP, mN,
-                          reinterpret_cast<uint16_t *>(smem + kListOff), reinterpret_cast<uint32_t *>(smem + kMarkOff));
+                s_resolve(a, u, stg + slot * kSlot, sc, sP, sN, mP, mN, reinterpret_cast<uint16_t *>(smem + kListOff),
+                          reinterpret_cast<uint32_t *>(smem + kMarkOff));
             }
             __syncwarp();
             slot ^= 1;
-            if (vP >= 0) s_store<KIND>(u, MP, a.mf, mP, k);
-            if (vN >= 0) s_store<KIND>(u, MN, a.mf, mN, k);
+            if (vP >= 0) s_store(u, MP, a.mf, mP, k);
+            if (vN >= 0) s_store(u, MN, a.mf, mN, k);
         }
     }
 }
 
-// grid: CTAs of 4 warps, one unit per warp.  Work order: frame groups of
-// fgroup frames; inside a group all units of kind 0, then 1, 2, 3 (longest
-// first), each over the group's frames.  The warps in flight then run one or
-// two kinds on a few frames (D and the words stay in L2).
-constexpr int kSweepWarps = 4;
-__global__ void __launch_bounds__(32 * kSweepWarps, 4) k_sweep(const __grid_constant__ SweepArgs a,
+// grid: CTAs of kSweepWarps warps, one unit per warp.  Work order: frame
+// groups of fgroup frames; inside a group all units of kind 0, then 1, 2, 3
+// (longest first), each over the group's frames: the warps in flight work
+// on a few frames, whose D and words stay in L2.
+constexpr int kSweepWarps = 1;
+__global__ void __launch_bounds__(32 * kSweepWarps, 16) k_sweep(const __grid_constant__ SweepArgs a,
                                                                  const __grid_constant__ SweepMaps tm) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t wid = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
@@ -1046,12 +990,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, 4) k_sweep(const __grid_cons
     }
     __syncwarp();
     uint32_t phase[2] = {0u, 0u};
-    switch (a.fams[gd.fam].kind) {
-        case 0: sweep_unit<0>(a, tm, un, gd, f, sm, phase); break;
-        case 1: sweep_unit<1>(a, tm, un, gd, f, sm, phase); break;
-        case 2: sweep_unit<2>(a, tm, un, gd, f, sm, phase); break;
-        default: sweep_unit<3>(a, tm, un, gd, f, sm, phase); break;
-    }
+    sweep_unit(a, tm, un, gd, f, sm, phase);
 }
 
 // host: TMA descriptors of the chunk's D ([frames][H][W] fp32)
