@@ -522,7 +522,11 @@ __device__ __forceinline__ int16_t s_rel(int32_t c, int32_t tau0, int32_t h) {
 
 constexpr int kMaxSegBlocks = kSweepSeg / 32;
 constexpr int kListCap = 256;                 // dense survivor list (entries per pass)
-constexpr size_t kRecOff = sizeof(float) * kSlot * 2;
+#ifndef SWEEP_NSLOT
+#define SWEEP_NSLOT 1
+#endif
+constexpr int kNSlot = SWEEP_NSLOT;        // staging slots per warp (2: prefetch the next block)
+constexpr size_t kRecOff = sizeof(float) * kSlot * kNSlot;
 constexpr size_t kListOff = kRecOff + sizeof(Rec) * 32 * kMaxSegBlocks;
 constexpr size_t kMarkOff = kListOff + sizeof(uint16_t) * kListCap;
 constexpr size_t kBarOff = kMarkOff + sizeof(uint32_t) * 64;
@@ -781,7 +785,7 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
             if (WN) lc = 32 * k - h + 31 - __clz(WN);
             if (k < kS) continue;
             s_stage_wait(bars + slot, phase[slot], bt[slot]);
-            if (k + 1 <= kT) bt[slot ^ 1] = s_stage(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k + 1, tma);
+            if (kNSlot == 2 && k + 1 <= kT) bt[slot ^ 1] = s_stage(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k + 1, tma);
             const float *rb = stg + slot * kSlot + rbo;
             float Q0 = NaN, Q2 = NaN;
             if (vN >= 0) {
@@ -807,7 +811,8 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
                 }
             }
             __syncwarp();
-            slot ^= 1;
+            if (kNSlot == 2) slot ^= 1;
+            else if (k + 1 <= kT) bt[0] = s_stage(u, tm, stg, bars, k + 1, tma);
             if (k >= kB) {
                 Rec rr;
                 rr.XN = __brev(XN);
@@ -847,7 +852,7 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
             WNprev = WN;
             if (k > kS) continue;
             s_stage_wait(bars + slot, phase[slot], bt[slot]);
-            if (k - 1 >= kB) bt[slot ^ 1] = s_stage(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k - 1, tma);
+            if (kNSlot == 2 && k - 1 >= kB) bt[slot ^ 1] = s_stage(u, tm, stg + (slot ^ 1) * kSlot, bars + (slot ^ 1), k - 1, tma);
             const float *rb = stg + slot * kSlot + rbo;
             if (k > kT) {
                 // warm-up: far filter of +b only
@@ -867,7 +872,8 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
                     }
                 }
                 __syncwarp();
-                slot ^= 1;
+                if (kNSlot == 2) slot ^= 1;
+                else if (k - 1 >= kB) bt[0] = s_stage(u, tm, stg, bars, k - 1, tma);
                 continue;
             }
             // tails for the pairs reaching below the block (d1 at tau0 - 1, d2 at tau0 - 1, tau0 - 2)
@@ -954,7 +960,8 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
                           reinterpret_cast<uint32_t *>(smem + kMarkOff));
             }
             __syncwarp();
-            slot ^= 1;
+            if (kNSlot == 2) slot ^= 1;
+            else if (k - 1 >= kB) bt[0] = s_stage(u, tm, stg, bars, k - 1, tma);
             if (vP >= 0) s_store(u, MP, a.mf, mP, k);
             if (vN >= 0) s_store(u, MN, a.mf, mN, k);
         }
@@ -966,7 +973,10 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
 // (longest first), each over the group's frames: the warps in flight work
 // on a few frames, whose D and words stay in L2.
 constexpr int kSweepWarps = 1;
-__global__ void __launch_bounds__(32 * kSweepWarps, 16) k_sweep(const __grid_constant__ SweepArgs a,
+#ifndef SWEEP_MINB
+#define SWEEP_MINB 20
+#endif
+__global__ void __launch_bounds__(32 * kSweepWarps, SWEEP_MINB) k_sweep(const __grid_constant__ SweepArgs a,
                                                                  const __grid_constant__ SweepMaps tm) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t wid = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);

@@ -316,7 +316,7 @@ void build_tiles(occ_ctx *c) {
     const int32_t H = c->H, W = c->W;
     std::vector<char> eligible(c->groups.size(), 0);
     // k_sweep (default) or the round-1 k_line + k_cand path (OCC_SWEEP=0, kept for A/B runs)
-    static const bool sweep = [] { const char *ev = getenv("OCC_SWEEP"); return ev && atoi(ev) != 0; }();
+    static const bool sweep = [] { const char *ev = getenv("OCC_SWEEP"); return !(ev && atoi(ev) == 0); }();
     for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi) {
         eligible[gi] = line_eligible(c, c->groups[gi]);
         if (eligible[gi] && !sweep) add_line_units(c, gi);
@@ -330,7 +330,7 @@ void build_tiles(occ_ctx *c) {
             for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi)
                 if (eligible[gi]) add_sweep_units(c, gi, seg);
             if (seg <= 32 || (double)c->sunits.size() * c->max_batch >= 148.0 * 16) break;
-            seg /= 2;
+            seg = std::max(32, (seg / 2) & ~31);
         }
         // by kind, longest first inside a kind (k_sweep's work order, k_sweep.cu)
         auto kind_of = [&](const SweepUnit &x) { return c->fams[c->groups[x.group].fam].kind; };

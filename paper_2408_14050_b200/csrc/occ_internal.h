@@ -199,7 +199,10 @@ cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames
 struct SweepUnit {
     int32_t group, l0, t0, t1;
 };
-constexpr int kSweepSeg = 256;
+#ifndef SWEEP_SEG
+#define SWEEP_SEG 256
+#endif
+constexpr int kSweepSeg = SWEEP_SEG;
 inline int64_t sweep_words_per_frame(int32_t H, int32_t W) {
     return (int64_t)((H + 31) / 32) * ((W + 31) / 32) * 12 * 32;
 }
