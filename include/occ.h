@@ -125,6 +125,14 @@ int occ_status(occ_ctx *ctx, int32_t *frame_status);
  * h_per_view has n_views entries.  Any output pointer may be NULL. */
 int occ_frame_info(occ_ctx *ctx, int32_t frame, float *dmin, float *dmax, int32_t *h_per_view);
 
+/* Eq. 3 (S5 of SURVEY §8.0) for given frame statistics:
+ * h = floor(min(max_scan, ceil(2 s R)) / 2) per view, R = fl32(dmax - dmin),
+ * s = the view's ||b||_inf (real-valued directions: 2 rho R).  dmin <= dmax
+ * finite, or non-finite stats give h = max_scan / 2.  h_per_view: host,
+ * n_views entries.  No device work.  OCC_OK or OCC_ERR_INVALID_ARG.  Used
+ * to size the halos of single-frame spatial sharding (spatial.py). */
+int occ_scan_half_lengths(const occ_ctx *ctx, float dmin, float dmax, int32_t *h_per_view);
+
 /* Mask output format (occ_set_mask_format), NEXT #4 of SURVEY §8(f):
  *   OCC_MASK_U8   (default) uint8 [batch][n_views][H][W], each byte 0 or 1;
  *   OCC_MASK_BITS bit-packed uint32 words [batch][n_views][H][ceil(W/32)]:

@@ -27,8 +27,23 @@ __device__ __forceinline__ void cex(float &a, float &b) {
     b = hi;
 }
 
+// The signed zero a stable sort (equal values keep input order, as the
+// oracle's insertion sort) puts at sorted position idx, given that position
+// holds a zero: the (idx - #negatives)-th zero of the pixel's inputs.  The
+// min/max network orders the values but not -0 / +0 among themselves.
+__device__ __noinline__ float stable_zero(const float *col, int64_t stride, int K, int idx) {
+    int neg = 0;
+    for (int k = 0; k < K; ++k) neg += __ldg(col + (int64_t)k * stride) < 0.0f ? 1 : 0;
+    int want = idx - neg;
+    for (int k = 0; k < K; ++k) {
+        const float x = __ldg(col + (int64_t)k * stride);
+        if (x == 0.0f && want-- == 0) return x;
+    }
+    return 0.0f;
+}
+
 template <int K>
-__device__ __forceinline__ float median_of(float (&v)[K], bool bad) {
+__device__ __forceinline__ float median_of(float (&v)[K], bool bad, const float *col, int64_t stride) {
     // odd-even transposition sort: K rounds of disjoint neighbour exchanges
 #pragma unroll
     for (int r = 0; r < K; ++r) {
@@ -36,8 +51,15 @@ __device__ __forceinline__ float median_of(float (&v)[K], bool bad) {
         for (int i = (r & 1); i + 1 < K; i += 2) cex(v[i], v[i + 1]);
     }
     float m;
-    if (K & 1) m = v[K / 2];
-    else m = __fmul_rn(__fadd_rn(v[K / 2 - 1], v[K / 2]), 0.5f);
+    if (K & 1) {
+        m = v[K / 2];
+        if (m == 0.0f) m = stable_zero(col, stride, K, K / 2);
+    } else {
+        float lo = v[K / 2 - 1], hi = v[K / 2];
+        if (lo == 0.0f) lo = stable_zero(col, stride, K, K / 2 - 1);
+        if (hi == 0.0f) hi = stable_zero(col, stride, K, K / 2);
+        m = __fmul_rn(__fadd_rn(lo, hi), 0.5f);
+    }
     return bad ? __int_as_float(0x7fc00000) : m;
 }
 
@@ -61,8 +83,9 @@ __global__ void __launch_bounds__(256) k_fuse(const float *__restrict__ stack, i
                 a[k] = q.x; b[k] = q.y; c[k] = q.z; d[k] = q.w;
                 ba |= !isfinite(q.x); bb |= !isfinite(q.y); bc |= !isfinite(q.z); bd |= !isfinite(q.w);
             }
-            __stcs(o4 + i, make_float4(median_of<K>(a, ba), median_of<K>(b, bb), median_of<K>(c, bc),
-                                       median_of<K>(d, bd)));
+            const float *col = stack + 4 * i;
+            __stcs(o4 + i, make_float4(median_of<K>(a, ba, col, n), median_of<K>(b, bb, col + 1, n),
+                                       median_of<K>(c, bc, col + 2, n), median_of<K>(d, bd, col + 3, n)));
         }
         return;
     }
@@ -74,7 +97,7 @@ __global__ void __launch_bounds__(256) k_fuse(const float *__restrict__ stack, i
             a[k] = __ldg(stack + (int64_t)k * n + i);
             bad |= !isfinite(a[k]);
         }
-        out[i] = median_of<K>(a, bad);
+        out[i] = median_of<K>(a, bad, stack + i, n);
     }
 }
 

@@ -898,8 +898,10 @@ int occ_detect_host(occ_ctx *c, const float *Dh, uint8_t *Mh, int32_t batch, voi
     CK(cudaSetDevice(c->device));
     const size_t HW = (size_t)c->H * c->W;
     if (!c->d_stage_D) {
+        // masks in either format: uint8 H*W or packed H*ceil(W/32)*4 bytes per plane
+        const size_t plane = std::max(HW, (size_t)c->H * (size_t)((c->W + 31) / 32) * 4);
         if (cudaMalloc(&c->d_stage_D, (size_t)c->max_batch * HW * sizeof(float)) != cudaSuccess ||
-            cudaMalloc(&c->d_stage_M, (size_t)c->max_batch * c->V * HW) != cudaSuccess) {
+            cudaMalloc(&c->d_stage_M, (size_t)c->max_batch * c->V * plane) != cudaSuccess) {
             cudaGetLastError();
             return OCC_ERR_OOM;
         }
@@ -1006,6 +1008,17 @@ int occ_frame_info(occ_ctx *c, int32_t frame, float *dmin, float *dmax, int32_t 
             if (!(L <= (double)c->params.max_scan)) L = c->params.max_scan;
             h_per_view[v] = fs.nonfinite ? 0 : ((int32_t)L) / 2;
         }
+    }
+    return OCC_OK;
+}
+
+int occ_scan_half_lengths(const occ_ctx *c, float dmin, float dmax, int32_t *h_per_view) {
+    if (!c || !h_per_view) return OCC_ERR_INVALID_ARG;
+    const float R = dmax - dmin;            // fl32 (host SSE, no contraction)
+    for (int32_t v = 0; v < c->V; ++v) {
+        double L = std::ceil((2.0 * c->views[v].rho) * (double)R);
+        if (!(L <= (double)c->params.max_scan)) L = c->params.max_scan;
+        h_per_view[v] = ((int32_t)L) / 2;
     }
     return OCC_OK;
 }

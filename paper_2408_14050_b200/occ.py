@@ -29,7 +29,7 @@ EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", 
            "occ_frame_info", "occ_set_path", "occ_last_launches", "occ_destroy", "occ_strerror",
            "occ_version", "occ_profile", "occ_profile_read", "occ_fuse_median", "occ_set_mask_format",
            "occ_mask_bytes", "occ_set_neighbors", "occ_get_neighbors", "occ_frame_stats",
-           "occ_set_frame_stats", "occ_create_dirs"]
+           "occ_set_frame_stats", "occ_create_dirs", "occ_scan_half_lengths"]
 MASK_FORMATS = {"u8": 0, "bits": 1}
 KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5, "nwin": 6}
 
@@ -109,6 +109,8 @@ def lib() -> ctypes.CDLL:
         L.occ_frame_stats.restype = ctypes.c_int
         L.occ_set_frame_stats.argtypes = [vp, vp, vp, vp, i32]
         L.occ_set_frame_stats.restype = ctypes.c_int
+        L.occ_scan_half_lengths.argtypes = [vp, ctypes.c_float, ctypes.c_float, vp]
+        L.occ_scan_half_lengths.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -189,6 +191,14 @@ class Detector:
         self.Wb = (self.W + 31) // 32
         self.set_neighbors(neighbors)
 
+    def scan_half_lengths(self, dmin: float, dmax: float) -> List[int]:
+        """Eq. 3's h per view for the given frame statistics (occ_scan_half_lengths)."""
+        h = np.zeros(self.V, np.int32)
+        rc = lib().occ_scan_half_lengths(self._h, float(dmin), float(dmax), h.ctypes.data)
+        if rc != OCC_OK:
+            raise OccError(rc, "occ_scan_half_lengths")
+        return [int(x) for x in h]
+
     def frame_stats(self, D, stream=None):
         """Exact per-frame (dmin, dmax, nonfinite) numpy arrays of device frames
         D [B, H, W] (occ_frame_stats; synchronises)."""
@@ -256,9 +266,15 @@ class Detector:
         D = np.ascontiguousarray(D, dtype=np.float32)
         if D.ndim == 2:
             D = D[None]
+        if D.ndim != 3 or tuple(D.shape[1:]) != (self.H, self.W):
+            raise ValueError(f"expected D [B, {self.H}, {self.W}], got {tuple(D.shape)}")
         B = D.shape[0]
+        mdt = np.uint8 if self.mask_format == "u8" else np.uint32
         if out is None:
-            out = np.empty(self.mask_shape(B), dtype=np.uint8 if self.mask_format == "u8" else np.uint32)
+            out = np.empty(self.mask_shape(B), dtype=mdt)
+        elif (out.dtype != mdt or not out.flags["C_CONTIGUOUS"] or not out.flags["WRITEABLE"]
+              or out.nbytes < lib().occ_mask_bytes(self._h, B)):
+            raise ValueError(f"out must be a writeable C-contiguous {np.dtype(mdt).name} array {self.mask_shape(B)}")
         sp = 0
         if stream is not None:
             sp = stream.cuda_stream
@@ -346,6 +362,9 @@ def fuse_median(stack, out=None, stream=None):
     n = stack.numel() // max(1, K)
     if out is None:
         out = torch.empty(stack.shape[1:], dtype=torch.float32, device=stack.device)
+    elif not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.numel() >= n
+              and out.device == stack.device):
+        raise ValueError(f"out must be a contiguous float32 CUDA tensor of {n} elements on {stack.device}")
     s = stream or torch.cuda.current_stream(stack.device)
     rc = lib().occ_fuse_median(stack.data_ptr(), K, n, out.data_ptr(), s.cuda_stream)
     if rc != OCC_OK:

@@ -38,21 +38,12 @@ def bands(H: int, world: int) -> List[Tuple[int, int]]:
     return out
 
 
-def scan_half_lengths(dmin: float, dmax: float, views: Sequence[Tuple[int, int]], max_scan: int = 4096) -> List[int]:
-    """Eq. 3 per view (S5): h = floor(min(cap, ceil(2 s R)) / 2), R = fl32(dmax - dmin)."""
-    R = float(np.float32(np.float32(dmax) - np.float32(dmin)))
-    hs = []
-    for bx, by in views:
-        s = max(abs(bx), abs(by))
-        L = np.ceil(2.0 * s * R) if np.isfinite(R) else np.inf
-        L = max_scan if not (L <= max_scan) else int(L)
-        hs.append(int(L) // 2)
-    return hs
-
-
-def halo_rows(dmin: float, dmax: float, views, max_scan: int = 4096) -> int:
-    """Rows of halo each side of a band: 2 max(h) + 2 (see the module doc)."""
-    return 2 * max(scan_half_lengths(dmin, dmax, views, max_scan)) + 2
+def halo_rows(h_per_view: Sequence[int]) -> int:
+    """Rows of halo each side of a band: 2 max(h) + 2 (see the module doc).
+    h_per_view: Eq. 3's scan half-lengths under the whole frame's statistics
+    (occ_scan_half_lengths through device_fns' h_fn; this module computes no
+    part of the method)."""
+    return 2 * max(h_per_view) + 2
 
 
 def extended(r0: int, r1: int, halo: int, H: int) -> Tuple[int, int]:
@@ -112,10 +103,11 @@ def exchange_halos(band, r0: int, r1: int, halo: int, H: int, all_bands: List[Tu
 
 
 def detect_band(band, r0: int, r1: int, H: int, views, rank: int, world: int,
-                stats_fn: Callable, detect_fn: Callable, max_scan: int = 4096):
+                stats_fn: Callable, detect_fn: Callable, h_fn: Callable):
     """One rank's part of a sharded frame.
 
     stats_fn(band) -> (dmin, dmax, nonfinite) of the band;
+    h_fn(dmin, dmax) -> Eq. 3's h per view under those statistics;
     detect_fn(ext, dmin, dmax, nonfinite) -> masks [V, e1 - e0, W] of the
     extended band under the imposed whole-frame statistics.
     Returns (interior masks [V, r1 - r0, W], (dmin, dmax, nonfinite))."""
@@ -123,7 +115,7 @@ def detect_band(band, r0: int, r1: int, H: int, views, rank: int, world: int,
     dmin, dmax, nbad = global_stats(lo, hi, bad, device=band.device)
     all_bands = bands(H, world)
     assert all_bands[rank] == (r0, r1)
-    halo = 0 if nbad else halo_rows(dmin, dmax, views, max_scan)
+    halo = 0 if nbad else halo_rows(h_fn(dmin, dmax))
     ext, e0, e1 = exchange_halos(band, r0, r1, halo, H, all_bands, rank)
     m = detect_fn(ext, dmin, dmax, nbad)
     return m[:, r0 - e0:r1 - e0], (dmin, dmax, nbad)
@@ -150,9 +142,10 @@ def gather_rows(part, r0: int, r1: int, H: int, world: int, rank: int, dst: int 
 
 
 def device_fns(views, **detector_kw):
-    """stats_fn / detect_fn over libocc: occ_frame_stats on the band and
+    """stats_fn / detect_fn / h_fn over libocc: occ_frame_stats on the band,
     occ_detect with occ_set_frame_stats on the extended band (a Detector per
-    band shape, created on first use; detector_kw as for Detector)."""
+    band shape, created on first use; detector_kw as for Detector) and
+    occ_scan_half_lengths."""
     from .occ import Detector
     cache = {}
 
@@ -172,8 +165,11 @@ def device_fns(views, **detector_kw):
         det.set_frame_stats()
         return m[0]
 
+    def h_fn(dmin, dmax):
+        return det_for(2, 2).scan_half_lengths(dmin, dmax)
+
     def close():
         for d in cache.values():
             d.close()
         cache.clear()
-    return stats_fn, detect_fn, close
+    return stats_fn, detect_fn, h_fn, close

@@ -72,3 +72,17 @@ def test_fuse_then_detect(torch_cuda):
     views = scenes.VIEWS_3X3
     g, _ = run_gpu(torch_cuda, fused_gpu, views)
     assert_same(g[0], oracle.detect(fused_orc, views), "masks of the fused map")
+
+
+@pytest.mark.parametrize("K", [2, 3, 4, 5, 7, 8, 9, 16, 17])
+def test_fuse_signed_zeros(torch_cuda, K):
+    """-0 and +0 compare equal; the oracle's stable insertion sort keeps them in
+    input order, so the median's zero sign is that of the zero a stable sort
+    places in the middle.  Every pixel mixes -0, +0 and
+    small integers; the check is bitwise."""
+    rng = scenes.SplitMix64(1304, K)
+    n = 8192
+    u = rng.uniform(K * n).reshape(K, n)
+    st = np.where(u < 0.3, -0.0, np.where(u < 0.6, 0.0, np.floor((u - 0.6) * 10) - 2.0)).astype(np.float32)
+    assert (np.signbit(st) & (st == 0)).any() and ((~np.signbit(st)) & (st == 0)).any()
+    same_f32(gpu_fuse(torch_cuda, st), oracle.fuse_median(st), f"K={K} signed zeros")

@@ -38,10 +38,10 @@ def test_frame_stats_exact(torch_cuda):
 
 def emulate(torch, D, world, views, N=0, fmt="u8"):
     H = D.shape[0]
-    stats_fn, detect_fn, close = spatial.device_fns(views, neighbors=N, mask_format=fmt)
+    stats_fn, detect_fn, h_fn, close = spatial.device_fns(views, neighbors=N, mask_format=fmt)
     los, his, bads = zip(*[stats_fn(torch.from_numpy(D[r0:r1].copy()).cuda()) for r0, r1 in spatial.bands(H, world)])
     dmin, dmax, nbad = min(los), max(his), sum(bads)
-    halo = 0 if nbad else spatial.halo_rows(dmin, dmax, views)
+    halo = 0 if nbad else spatial.halo_rows(h_fn(dmin, dmax))
     parts = []
     for r0, r1 in spatial.bands(H, world):
         e0, e1 = spatial.extended(r0, r1, halo, H)
@@ -75,3 +75,15 @@ def test_bands_nonfinite(torch_cuda):
     D = frame(12)
     D[80, 3] = np.nan
     assert emulate(torch_cuda, D, 3, VIEWS).sum() == 0
+
+
+def test_scan_half_lengths_match_oracle(torch_cuda):
+    """occ_scan_half_lengths (Eq. 3) vs the oracle's scan length."""
+    from paper_2408_14050_b200.occ import Detector
+    views = scenes.VIEWS_5X5
+    det = Detector(16, 16, views, max_scan=300)
+    for lo, hi in [(1.0, 12.3), (0.0, 0.0), (-3.5, 64.9), (1.0, 3000.0), (-3e38, 3e38)]:
+        got = det.scan_half_lengths(lo, hi)
+        want = [oracle.scan_length(lo, hi, max(abs(bx), abs(by)), 300) // 2 for bx, by in views]
+        assert got == want, (lo, hi)
+    det.close()

