@@ -1147,16 +1147,19 @@ __global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
 #define HARD_MINB 1
 #endif
 __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
-                                              MaskFmt mf, int32_t W, int64_t HW, int32_t nviews,
+                                              MaskFmt mf, int32_t W, int64_t HW, int32_t frames, int32_t nviews,
                                               const ViewDesc *__restrict__ views,
                                               Params p, const HardEntry *__restrict__ gq,
                                               const uint32_t *__restrict__ gq_count, int32_t gq_cap,
                                               const FrameStats *__restrict__ st) {
     const uint32_t n = min(*gq_count, (uint32_t)gq_cap);
     const float NaN = __int_as_float(0x7fc00000);
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    // newest entries first: their frames were swept last and are still in L2
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const uint32_t e = n - 1u - t;
         const HardEntry he = gq[e];
         const int32_t f = (int32_t)((he.meta >> 17) & 255u), v = (int32_t)(he.meta >> 25);
+        OCC_CHECK(f < frames && v < nviews && he.pix >= 0 && (int64_t)he.pix < HW);
         const ViewDesc &vdv = views[v];
         const int32_t s = vdv.s;
         const int32_t step = (vdv.sg > 0 ? 1 : -1) * line_stride(vdv.lkind, W);
@@ -1176,7 +1179,11 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
         for (int32_t j0 = 3; j0 <= jm && !hit; j0 += HARD_BATCH) {
             float vq[HARD_BATCH];
 #pragma unroll
-            for (int u = 0; u < HARD_BATCH; ++u) vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * step) : NaN;
+            for (int u = 0; u < HARD_BATCH; ++u) {
+                OCC_CHECK(j0 + u > jm || ((int64_t)he.pix + (int64_t)(j0 + u) * step >= 0 &&
+                                          (int64_t)he.pix + (int64_t)(j0 + u) * step < HW));
+                vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * step) : NaN;
+            }
             // branch-free fast test of the HARD_BATCH offsets (fp32 with the 2^-10
             // band, as pair_far); offsets inside the band take the exact test
             float mn = INFINITY;
@@ -1198,11 +1205,11 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
     }
 }
 
-cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW,
+cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW, int32_t frames,
                         int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
                         const FrameStats *st, int32_t nsm, cudaStream_t s) {
-    k_hard<<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, nviews, views, p, gq, gq_count, gq_cap, st);
+    k_hard<<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, frames, nviews, views, p, gq, gq_count, gq_cap, st);
     return cudaGetLastError();
 }
 

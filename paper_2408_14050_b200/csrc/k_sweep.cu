@@ -349,6 +349,7 @@ __device__ __noinline__ bool s_stage(const SU &u, const SweepMaps &tm, float *sl
             const int32_t y = (u.kind == 2 ? u.l0 + r : u.l0 + 31 - r) + dy;
             const int32_t x = 32 * k + ((r - 31) & ~3) + 4 * q;
             float *dst = slot + r * 36 + 4 * q;
+            OCC_CHECK(r < 32 && q < 9 && r * 36 + 4 * q + 4 <= kSlot);
             if ((uint32_t)x < (uint32_t)W && (uint32_t)y < (uint32_t)H) s_cp16(dst, u.Df + (int64_t)y * W + x);
             else *reinterpret_cast<float4 *>(dst) = make_float4(NaN, NaN, NaN, NaN);
         }
@@ -455,6 +456,13 @@ __device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf
     // one image row per tau: the 32 lanes write one contiguous run
     uint8_t *dst = Mv + u.B + (int64_t)(32 * k) * u.S;
     const int64_t S = u.S;
+#ifdef OCC_CHECKS
+    for (int r = 0; r < 32; ++r) {
+        const int32_t tau = 32 * k + r;
+        const int64_t pix = u.B + (int64_t)tau * u.S;
+        OCC_CHECK(tau < u.elo || tau >= u.ehi || (pix >= 0 && pix < (int64_t)H * W));
+    }
+#endif
     if (32 * k >= u.elo && 32 * k + 32 <= u.ehi) {
 #pragma unroll 8
         for (int r = 0; r < 32; ++r) __stcs(dst + r * S, (uint8_t)((word >> r) & 1u));
@@ -629,13 +637,15 @@ __device__ __noinline__ void s_resolve(const SweepArgs &a, const SU &u, const fl
             uint32_t o = inc - n;
             const uint32_t tag = (uint32_t)lane << 6;
             uint32_t t = tP;
-            while (t) { list[o++] = (uint16_t)(tag | (__ffs(t) - 1)); t &= t - 1u; }
+            while (t) { OCC_CHECK(o < (uint32_t)kListCap); list[o++] = (uint16_t)(tag | (__ffs(t) - 1)); t &= t - 1u; }
             t = tN;
-            while (t) { list[o++] = (uint16_t)(tag | 32 | (__ffs(t) - 1)); t &= t - 1u; }
+            while (t) { OCC_CHECK(o < (uint32_t)kListCap); list[o++] = (uint16_t)(tag | 32 | (__ffs(t) - 1)); t &= t - 1u; }
         }
         __syncwarp();
         for (uint32_t b0 = 0; b0 < tot; b0 += 32) {
             const SurvDec d = s_decode(u, slot, c, list, tot, b0 + lane, Blo, Bhi);
+            OCC_CHECK(!d.ok || (d.j1 >= 3 && d.j1 <= d.J && d.B + (int64_t)(d.i + d.dir * d.j1) * u.S >= 0 &&
+                                d.B + (int64_t)(d.i + d.dir * d.j1) * u.S < (int64_t)u.H * u.W));
             const float vq = d.ok ? __ldg(u.Df + d.B + (int64_t)(d.i + d.dir * d.j1) * u.S) : NaN;
             bool hit = d.ok && s_pair_far(vq, d.vp, d.j1, c.fs, c.s, c.tlo, c.thi, a.p);
             SST(3 + d.view, hit);
@@ -819,6 +829,7 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
                 rr.pclP = s_rel(pcl, 32 * k, h);
                 rr.lcN = s_rel(lc, 32 * k, h);
                 rr.VW = __floats2half2_rn(Q0, Q2);
+                OCC_CHECK(k - kB < kMaxSegBlocks);
                 rec[(k - kB) * 32 + lane] = rr;
             }
         }
@@ -921,6 +932,7 @@ __device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm,
             const uint32_t s2m1 = s_sgn(d2m1), s2m2 = s_sgn(d2m2);
             const uint32_t T1 = ~Xg1 & Xl1, T2 = ~Xg2 & Xl2, TF = NFWD ? (~Xg1 & Xlf) : 0u;
             const uint32_t ext = s_ge(u.elo - tau0) & s_le(u.ehi - 1 - tau0);
+            OCC_CHECK(k >= kB && k - kB < kMaxSegBlocks);
             const Rec rr = rec[(k - kB) * 32 + lane];
             // view +b: pairs (i, i + j) covered <=> a +b candidate in [i + j - h, i + h]
             const int32_t pcl = tau0 + rr.pclP;

@@ -806,16 +806,23 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
     if (sweep) {
         ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
+#ifdef OCC_CHECKS
+        // poison the queue: a slot k_hard reads that this chunk did not write fails its checks
+        CK(cudaMemsetAsync(c->d_gq, 0xFF, sizeof(HardEntry) * (size_t)c->gq_cap, s));
+#endif
         CK(launch_sweep(Dc, c->H, c->W, n, c->d_sunits, (int32_t)c->sunits.size(), c->d_groups, c->d_views, c->V,
                         c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_words, c->d_gq, c->d_gq_count,
                         c->gq_cap, c->skstart, c->sfgroup, c->d_dbg, s));
-        CK(launch_hard(Dc, Mc, c->mf, c->W, HW, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
+        CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
                        c->gq_cap, c->d_stats + c0, c->nsm, s));
         launches += 2;
         pl.end();
     } else if (!tiled_only && !c->units.empty()) {
         ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
+#ifdef OCC_CHECKS
+        CK(cudaMemsetAsync(c->d_gq, 0xFF, sizeof(HardEntry) * (size_t)c->gq_cap, s));
+#endif
         if (c->d_cand) {
             CK(launch_cand(Dc, c->H, c->W, n, c->d_codes, c->code_bytes, c->d_candfam, c->nfam,
                            c->cand_per_frame, c->d_cand, s));
@@ -824,7 +831,7 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         CK(launch_line(Dc, c->H, c->W, n, c->d_units, (int32_t)c->units.size(), c->d_groups,
                        c->d_views, c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_codes,
                        c->code_bytes, c->d_dbg, c->d_gq, c->d_gq_count, c->gq_cap, c->d_cand, c->d_candfam, s));
-        CK(launch_hard(Dc, Mc, c->mf, c->W, HW, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
+        CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
                        c->gq_cap, c->d_stats + c0, c->nsm, s));
         launches += 2;
         pl.end();

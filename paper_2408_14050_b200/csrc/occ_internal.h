@@ -7,6 +7,24 @@
 
 #include "../../include/occ.h"
 
+// OCC_CHECKS builds (OCC_DEFINES=-DOCC_CHECKS): device-side bounds checks
+// of every queue entry, staged / listed index and mask write, before the
+// access (compute-sanitizer is closed on the GPU pool).  A failed check
+// prints the condition and traps (the call then reports OCC_ERR_CUDA).
+#ifdef OCC_CHECKS
+#include <cstdio>
+#define OCC_CHECK(c)                                                                          \
+    do {                                                                                      \
+        if (!(c)) {                                                                           \
+            printf("OCC_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                        \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define OCC_CHECK(c) do { } while (0)
+#endif
+
 namespace occ {
 
 constexpr int kMaxViews = 64;
@@ -166,7 +184,7 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
                         const MaskFmt &mf, const void *codes, int32_t code_bytes, unsigned long long *dbg,
                         HardEntry *gq, uint32_t *gq_count, int32_t gq_cap, const uint32_t *cand,
                         const CandFam *candfam, cudaStream_t s);
-cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW,
+cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW, int32_t frames,
                         int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
                         const FrameStats *st, int32_t nsm, cudaStream_t s);
