@@ -114,17 +114,23 @@ __global__ void __launch_bounds__(128) k_words(WordsArgs a) {
     const float *Df = a.D + (int64_t)f * H * W;
     int32_t lo = 0x7FFFFFFF, hi = (int32_t)0x80000000;
     uint32_t bad = 0;
-    if (kx < a.nxb) {
+    {   // (warps past the last x-block run with every load off: no divergent branch around the ballots)
+        const bool wok = kx < a.nxb;
         const int32_t x = 32 * kx + lane, y0 = 32 * m;
-        const bool xin = x < W, xr = x + 1 < W;
-        float v = (xin && y0 < H) ? __ldg(Df + (int64_t)y0 * W + x) : 0.0f;
+        const bool xin = wok && x < W, xr = xin && x + 1 < W;
+        // (branch-free body: the ballots stay convergent)
+        const float *col = Df + x;
+        float v = (xin && y0 < H) ? __ldg(col + (int64_t)y0 * W) : 0.0f;
+        const bool l31 = lane == 31;
 #pragma unroll 4
         for (int r = 0; r < 32; ++r) {
             const int32_t y = y0 + r;
-            const bool in = xin && y < H, yb = y + 1 < H;
-            const float below = (xin && yb) ? __ldg(Df + (int64_t)(y + 1) * W + x) : 0.0f;
-            float right = __shfl_down_sync(FULL, v, 1);
-            if (lane == 31) right = (xr && y < H) ? __ldg(Df + (int64_t)y * W + x + 1) : 0.0f;
+            const bool yin = y < H, yb = y + 1 < H;
+            const bool in = xin && yin;
+            const float below = (xin && yb) ? __ldg(col + (int64_t)(y + 1) * W) : 0.0f;
+            const float r31 = (l31 && xr && yin) ? __ldg(col + (int64_t)y * W + 1) : 0.0f;
+            const float sh = __shfl_down_sync(FULL, v, 1);
+            const float right = l31 ? r31 : sh;
             const float ex = xr ? __fsub_rn(right, v) : 0.0f;
             const float ey = yb ? __fsub_rn(below, v) : 0.0f;
             const float e2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
@@ -139,15 +145,12 @@ __global__ void __launch_bounds__(128) k_words(WordsArgs a) {
                 *reinterpret_cast<uint4 *>(&rw[warp][r][0]) = make_uint4(b0, b1, b2, b3);
                 *reinterpret_cast<uint4 *>(&rw[warp][r][4]) = make_uint4(b4, b5, b6, b7);
             }
-            if (in) {
-                if (isfinite(v)) {
-                    const int32_t k = float_key(v);
-                    lo = min(lo, k);
-                    hi = max(hi, k);
-                } else {
-                    ++bad;
-                }
-            }
+            // statistics (exact min / max through ordered keys, non-finite count)
+            const bool fin = in && isfinite(v);
+            const int32_t key = float_key(v);
+            lo = fin ? min(lo, key) : lo;
+            hi = fin ? max(hi, key) : hi;
+            bad += (in && !fin) ? 1u : 0u;
             v = below;
         }
         __syncwarp();
@@ -172,8 +175,10 @@ __global__ void __launch_bounds__(128) k_words(WordsArgs a) {
             o[10] = t6 & ~gea; o[11] = t7 & ~gea;
         }
         uint32_t *dst = a.words + ((((int64_t)f * a.nyb + m) * a.nxb + kx) * kWordSlots) * 32 + lane;
+        if (wok) {
 #pragma unroll
-        for (int s = 0; s < kWordSlots; ++s) dst[s * 32] = o[s];
+            for (int s = 0; s < kWordSlots; ++s) dst[s * 32] = o[s];
+        }
     }
     if (!a.do_stats) return;
 #pragma unroll
@@ -610,7 +615,7 @@ __device__ __forceinline__ SurvDec s_decode(const SU &u, const float *slot, cons
 // probe is at the witness guess j = s (v_w - v_i) (all probes of the block in
 // flight together); a miss goes to k_hard's queue.  Hits are OR-ed into the
 // owner's mask word by shared-memory atomics.
-__device__ __noinline__ void s_resolve(const SweepArgs &a, const SU &u, const float *slot, const SurvCtx &c,
+__device__ __forceinline__ void s_resolve(const SweepArgs &a, const SU &u, const float *slot, const SurvCtx &c,
                                        uint32_t sP, uint32_t sN, uint32_t &mP, uint32_t &mN, uint16_t *list,
                                        uint32_t *marks) {
     const int lane = u.lane;
@@ -694,7 +699,7 @@ __device__ __noinline__ void s_resolve(const SweepArgs &a, const SU &u, const fl
     __syncwarp();
 }
 
-__device__ __noinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm, const SweepUnit &un,
+__device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm, const SweepUnit &un,
                                         const GroupDesc &gd, int32_t f, unsigned char *smem, uint32_t *phase) {
     const FamilyDesc &fd = a.fams[gd.fam];
     SU u;

@@ -352,6 +352,7 @@ void build_tiles(occ_ctx *c) {
         const int32_t by_wave = (int32_t)std::ceil(148.0 * 16 / std::max(1, kmin));
         const int32_t by_l2 = std::max(1, (int32_t)(80.0e6 / fbytes));
         c->sfgroup = std::max(1, std::min(by_wave, by_l2));
+        if (const char *ev = getenv("OCC_SWEEP_FGROUP")) c->sfgroup = std::max(1, atoi(ev));   // tuning knob
     }
     // segment length: 256 positions, shorter when a call of max_batch frames
     // would not fill the GPU (a unit is one warp's serial work, ~0.1 ms at
