@@ -527,6 +527,8 @@ __device__ __noinline__ void flush_queue(const int DIR, const Ctx &c, const int3
             HardEntry he;
             he.pix = (int32_t)(line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S);
             he.meta = (uint32_t)jm | ((uint32_t)c.f << 17) | ((uint32_t)vid << 25);
+            he.guess = 0;
+            he.vq = 0.0f;
             c.gq[base + (uint32_t)e] = he;
         }
         __syncwarp();
@@ -1176,6 +1178,23 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
         const double jv = floor(__dadd_rn(__dmul_rn((double)s, (double)__fsub_rn(vmax, vp)), (double)p.t_dist));
         const int32_t jm = (int32_t)fmin((double)(he.meta & 0x1FFFFu), jv);
         bool hit = false;
+        if (he.guess >= 3 && jm >= 3) {
+            // the sweep's probe at he.guess read he.vq and missed: a slanted
+            // occluder puts the partner near the fixed point j = s (vq - v_p)
+            const double jf = rint(__dmul_rn((double)s, (double)__fsub_rn(he.vq, vp)));
+            const int32_t j2 = (int32_t)fmin(fmax(jf, 3.0), (double)jm);
+            float w[5];
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+                const int32_t j = j2 - 2 + u;
+                w[u] = (j >= 3 && j <= jm) ? __ldg(Ds + (int64_t)j * step) : NaN;
+            }
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+                const int32_t j = j2 - 2 + u;
+                if (!hit && j >= 3 && j <= jm) hit = pair_far(w[u], vp, j, vk, p);
+            }
+        }
         for (int32_t j0 = 3; j0 <= jm && !hit; j0 += HARD_BATCH) {
             float vq[HARD_BATCH];
 #pragma unroll

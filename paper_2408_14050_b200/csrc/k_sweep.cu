@@ -406,10 +406,10 @@ __device__ __forceinline__ float s_gv(const SU &u, int32_t tau) {
 
 // mask bits of one view for tau block k (bit r <-> tau = 32k + r), positions
 // outside the lane's line already cleared
-__device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf, uint32_t word, int32_t k) {
+__device__ __noinline__ void s_store_packed(const SU &u, uint8_t *Mv, const MaskFmt &mf, uint32_t word, int32_t k) {
     const int lane = u.lane;
     const int32_t H = u.H, W = u.W;
-    if (mf.packed) {
+    {
         uint32_t *P = reinterpret_cast<uint32_t *>(Mv);
         const int32_t Wb = mf.Wb;
         if (u.kind == 0) {
@@ -436,6 +436,15 @@ __device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf
                 if (hi && w0 + 1 >= 0 && w0 + 1 < Wb) atomicOr(P + (int64_t)y * Wb + w0 + 1, hi);
             }
         }
+        return;
+    }
+}
+
+__device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf, uint32_t word, int32_t k) {
+    const int lane = u.lane;
+    const int32_t H = u.H, W = u.W;
+    if (mf.packed) {
+        s_store_packed(u, Mv, mf, word, k);
         return;
     }
     if (u.kind <= 1) {
@@ -683,6 +692,8 @@ __device__ __forceinline__ void s_resolve(const SweepArgs &a, const SU &u, const
                         HardEntry he;
                         he.pix = (int32_t)(d.B + (int64_t)d.i * u.S);
                         he.meta = (uint32_t)d.J | ((uint32_t)u.f << 17) | ((uint32_t)vid << 25);
+                        he.guess = d.j1;
+                        he.vq = vq;
                         a.gq[slotq] = he;
                     } else {
                         const int32_t elo = d.dir > 0 ? -(1 << 30) : d.i - d.J, ehi = d.dir > 0 ? d.i + d.J + 1 : (1 << 30);

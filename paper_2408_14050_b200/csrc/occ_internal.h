@@ -158,7 +158,7 @@ constexpr int kLineCandMarginWords = 4;  // candidate words staged beyond the se
 struct LineUnit {
     int32_t group, l0, t0, t1;
 };
-// An exhaustive far-partner search deferred to k_hard (8 bytes): survivor at
+// An exhaustive far-partner search deferred to k_hard (16 bytes): survivor at
 // pixel index pix of frame f (of the chunk), view v; partners at
 // pix + j * sg(v) * stride(kind(v)), j = 3 .. jm (dcov clipped to the image).
 // meta = jm | f << 17 | v << 25 (jm <= 2 * (65536 / 2) < 2^17, f < 256,
@@ -166,6 +166,8 @@ struct LineUnit {
 struct HardEntry {
     int32_t pix;
     uint32_t meta;
+    int32_t guess;      // offset of the sweep's failed probe (0: none)
+    float vq;           // the value it read (k_hard starts at its fixed point s (vq - v_p))
 };
 constexpr int kMaxChunkFrames = 255;     // f field of HardEntry
 // Candidate words precomputed per chunk by k_cand (one entry per family;
