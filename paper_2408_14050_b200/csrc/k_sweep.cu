@@ -301,26 +301,18 @@ __device__ __forceinline__ int32_t s_stride(int kind, int32_t W) {
     return kind == 0 ? 1 : (kind == 1 ? W : (kind == 2 ? W + 1 : 1 - W));
 }
 
-// candidate words of both views (x: +b0, y: -b0) for tau block k of the unit's lines
-__device__ __forceinline__ uint2 s_word2(const SU &u, int32_t k) {
-    const uint32_t *Wl = u.Wf + u.lane;
+// candidate word of one view (v = 0: +b0, 1: -b0) for tau block k
+__device__ __forceinline__ uint32_t s_word1(const SU &u, int32_t k, int v) {
+    const uint32_t *Wl = u.Wf + u.lane + 32 * v;
     constexpr int St = kWordSlots * 32;
-    if (u.kind == 0) {
-        if ((uint32_t)k >= (uint32_t)u.nxb) return make_uint2(0u, 0u);
-        const uint32_t *p = Wl + (u.A * u.nxb + k) * St;
-        return make_uint2(__ldg(p), __ldg(p + 32));
-    }
-    if (u.kind == 1) {
-        if ((uint32_t)k >= (uint32_t)u.nyb) return make_uint2(0u, 0u);
-        const uint32_t *p = Wl + (k * u.nxb + u.A) * St + 64;
-        return make_uint2(__ldg(p), __ldg(p + 32));
-    }
+    if (u.kind == 0) return (uint32_t)k < (uint32_t)u.nxb ? __ldg(Wl + (u.A * u.nxb + k) * St) : 0u;
+    if (u.kind == 1) return (uint32_t)k < (uint32_t)u.nyb ? __ldg(Wl + (k * u.nxb + u.A) * St + 64) : 0u;
     const int32_t m = u.kind == 2 ? u.A + k : u.A - k;
-    uint2 w = make_uint2(0u, 0u);
-    if ((uint32_t)m >= (uint32_t)u.nyb) return w;
+    if ((uint32_t)m >= (uint32_t)u.nyb) return 0u;
     const uint32_t *p = Wl + (m * u.nxb + k) * St + (u.kind == 2 ? 4 * 32 : 8 * 32);
-    if ((uint32_t)k < (uint32_t)u.nxb) { w.x = __ldg(p); w.y = __ldg(p + 32); }
-    if ((uint32_t)(k - 1) < (uint32_t)u.nxb) { w.x |= __ldg(p - St + 64); w.y |= __ldg(p - St + 96); }
+    uint32_t w = 0u;
+    if ((uint32_t)k < (uint32_t)u.nxb) w = __ldg(p);
+    if ((uint32_t)(k - 1) < (uint32_t)u.nxb) w |= __ldg(p - St + 64);
     return w;
 }
 
@@ -792,17 +784,19 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
         const int32_t kS = max(kB - nbr, kEmin);           // first staged block
         const int32_t kW = min(kS, kB - ((2 * h + 63) >> 5));
         int32_t pcl = NONE_LO, lc = NONE_LO;
-        uint32_t pw_lo = s_word2(u, kW + hq - 1).x, nw_lo = s_word2(u, kW + nq).y;
-        uint32_t pw_nx = s_word2(u, kW + hq).x, nw_nx = s_word2(u, kW + nq + 1).y;   // prefetched
+        uint32_t pw_lo = s_word1(u, kW + hq - 1, 0), nw_lo = s_word1(u, kW + nq, 1);
+        // words prefetched 3 blocks ahead (the first iterations only track windows)
+        uint32_t pq0 = s_word1(u, kW + hq, 0), pq1 = s_word1(u, kW + 1 + hq, 0), pq2 = s_word1(u, kW + 2 + hq, 0);
+        uint32_t nq0 = s_word1(u, kW + nq + 1, 1), nq1 = s_word1(u, kW + nq + 2, 1), nq2 = s_word1(u, kW + nq + 3, 1);
         float A1 = NaN, A2 = NaN, A3 = NaN, w1 = NaN, w2 = NaN, w3 = NaN, SY = -INFINITY, VM = NaN;
         uint32_t XN = 0u;
         int slot = 0;
         bool bt[2] = {false, false};
         if (kS <= kT) bt[0] = s_stage(u, tm, stg, bars, kS, tma);
         for (int32_t k = kW; k <= kT; ++k) {
-            const uint32_t pw_hi = pw_nx, nw_hi = nw_nx;
-            pw_nx = s_word2(u, k + 1 + hq).x;
-            nw_nx = s_word2(u, k + 1 + nq + 1).y;
+            const uint32_t pw_hi = pq0, nw_hi = nq0;
+            pq0 = pq1; pq1 = pq2; pq2 = s_word1(u, k + 3 + hq, 0);
+            nq0 = nq1; nq1 = nq2; nq2 = s_word1(u, k + 3 + nq + 1, 1);
             const uint32_t WP = __funnelshift_r(pw_lo, pw_hi, hr);
             pw_lo = pw_hi;
             if (WP) pcl = 32 * k + h - 32 + 31 - __clz(WP);
@@ -858,8 +852,9 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
         const int32_t kS = min(kT + nbr, kEmax);            // first staged block (from the top)
         const int32_t kW = max(kS, kT + 2 + ((2 * h + 31) >> 5));
         int32_t fc = NONE_HI, ncl = NONE_HI;
-        uint32_t pw_hi = s_word2(u, kW + hq + 1).x, nw_hi = s_word2(u, kW + nq + 1).y;
-        uint32_t pw_nx = s_word2(u, kW + hq).x, nw_nx = s_word2(u, kW + nq).y;   // prefetched
+        uint32_t pw_hi = s_word1(u, kW + hq + 1, 0), nw_hi = s_word1(u, kW + nq + 1, 1);
+        uint32_t pq0 = s_word1(u, kW + hq, 0), pq1 = s_word1(u, kW - 1 + hq, 0), pq2 = s_word1(u, kW - 2 + hq, 0);
+        uint32_t nq0 = s_word1(u, kW + nq, 1), nq1 = s_word1(u, kW - 1 + nq, 1), nq2 = s_word1(u, kW - 2 + nq, 1);
         uint32_t WNprev = 0u;
         float v1 = NaN, v2 = NaN, v3 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY, VM = NaN;
         int slot = 0;
@@ -867,9 +862,9 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
         bt[0] = s_stage(u, tm, stg, bars, kS, tma);
         for (int32_t k = kW; k >= kB; --k) {
             const int32_t tau0 = 32 * k;
-            const uint32_t pw_lo = pw_nx, nw_lo = nw_nx;
-            pw_nx = s_word2(u, k - 1 + hq).x;
-            nw_nx = s_word2(u, k - 1 + nq).y;
+            const uint32_t pw_lo = pq0, nw_lo = nq0;
+            pq0 = pq1; pq1 = pq2; pq2 = s_word1(u, k - 3 + hq, 0);
+            nq0 = nq1; nq1 = nq2; nq2 = s_word1(u, k - 3 + nq, 1);
             const uint32_t WP = __funnelshift_r(pw_lo, pw_hi, hr);      // +b candidates [tau0 + h, tau0 + h + 31]
             pw_hi = pw_lo;
             if (WP) fc = tau0 + h + __ffs(WP) - 1;
