@@ -316,6 +316,9 @@ __device__ __forceinline__ uint32_t s_word1(const SU &u, int32_t k, int v) {
     return w;
 }
 
+#ifndef SWEEP_ROWCOPY
+#define SWEEP_ROWCOPY 1
+#endif
 // Stages tau block k (32 positions of the 32 lines) into a slot:
 //   kind 0: [line][32 positions] with the 128-byte swizzle (16-byte chunk c of row l at c ^ (l & 7));
 //   kind 1: [position][32 lines];
@@ -339,6 +342,24 @@ __device__ __noinline__ bool s_stage(const SU &u, const SweepMaps &tm, float *sl
         return true;
     }
     if (tma) {                       // kinds 2, 3: 16-byte copies of the 4-aligned row runs
+#if SWEEP_ROWCOPY
+        // lane r copies row r's 9 chunks (one address per lane, immediate offsets)
+        const int r = lane;
+        const int32_t y = u.kind == 2 ? u.l0 + 32 * k + r : u.l0 + 31 - 32 * k - r;
+        const int32_t x0 = 32 * k + ((r - 31) & ~3);
+        float *dst = slot + r * 36;
+        const float *src = u.Df + (int64_t)y * W + x0;
+        if ((uint32_t)y < (uint32_t)H && x0 >= 0 && x0 + 36 <= W) {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) s_cp16(dst + 4 * q, src + 4 * q);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                if ((uint32_t)y < (uint32_t)H && (uint32_t)(x0 + 4 * q) < (uint32_t)W) s_cp16(dst + 4 * q, src + 4 * q);
+                else *reinterpret_cast<float4 *>(dst + 4 * q) = make_float4(NaN, NaN, NaN, NaN);
+            }
+        }
+#else
         const int32_t dy = u.kind == 2 ? 32 * k : -32 * k;
 #pragma unroll 3
         for (int i = 0; i < 9; ++i) {
@@ -350,6 +371,7 @@ __device__ __noinline__ bool s_stage(const SU &u, const SweepMaps &tm, float *sl
             if ((uint32_t)x < (uint32_t)W && (uint32_t)y < (uint32_t)H) s_cp16(dst, u.Df + (int64_t)y * W + x);
             else *reinterpret_cast<float4 *>(dst) = make_float4(NaN, NaN, NaN, NaN);
         }
+#endif
         s_commit();
         return false;
     }
