@@ -200,7 +200,8 @@ int32_t occ_last_launches(const occ_ctx *ctx);
  * synchronises and returns, for one kernel kind, the summed device time in
  * milliseconds and the number of launches since the last reset. */
 enum { OCC_KERNEL_INIT = 0, OCC_KERNEL_STATS = 1, OCC_KERNEL_TILE = 2, OCC_KERNEL_DIRECT = 3,
-       OCC_KERNEL_CAND = 4, OCC_KERNEL_LINE = 5, OCC_KERNEL_NWIN = 6, OCC_KERNEL_KINDS = 7 };
+       OCC_KERNEL_CAND = 4, OCC_KERNEL_LINE = 5, OCC_KERNEL_NWIN = 6, OCC_KERNEL_HARD = 7,
+       OCC_KERNEL_KINDS = 8 };
 int occ_profile(occ_ctx *ctx, int32_t enable);
 int occ_profile_read(occ_ctx *ctx, int32_t kind, double *total_ms, int32_t *launches);
 

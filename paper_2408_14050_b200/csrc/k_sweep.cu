@@ -996,7 +996,9 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
             SST(2, __popc(sN));
             SST(10, __popc(mP));
             SST(11, __popc(mN));
+            SST(13, lane == 0);
             if (__any_sync(FULL, (sP | sN) != 0u)) {
+                SST(12, lane == 0);
                 SurvCtx sc;
                 sc.tau0 = tau0; sc.h = h; sc.WP = WP; sc.WN = WN; sc.pcl = pcl; sc.ncl = ncl;
                 sc.Q0 = Q0; sc.Q1 = Q1; sc.Q2 = Q2; sc.Q3 = Q3; sc.VW = rr.VW;

@@ -325,11 +325,12 @@ void build_tiles(occ_ctx *c) {
         // segment length: 256 positions, halved while one call of max_batch
         // frames would not fill the GPU (148 SMs x 16 warps)
         int32_t seg = kSweepSeg;
+        static const int fill = [] { const char *ev = getenv("OCC_SWEEP_FILL"); return ev ? atoi(ev) : 16; }();
         for (;;) {
             c->sunits.clear();
             for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi)
                 if (eligible[gi]) add_sweep_units(c, gi, seg);
-            if (seg <= 32 || (double)c->sunits.size() * c->max_batch >= 148.0 * 16) break;
+            if (seg <= 32 || (double)c->sunits.size() * c->max_batch >= 148.0 * fill) break;
             seg = std::max(32, (seg / 2) & ~31);
         }
         // by kind, longest first inside a kind (k_sweep's work order, k_sweep.cu)
@@ -814,10 +815,12 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         CK(launch_sweep(Dc, c->H, c->W, n, c->d_sunits, (int32_t)c->sunits.size(), c->d_groups, c->d_views, c->V,
                         c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_words, c->d_gq, c->d_gq_count,
                         c->gq_cap, c->skstart, c->sfgroup, c->d_dbg, s));
+        pl.end();
+        ProfScope ph(c, OCC_KERNEL_HARD, s);
         CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
                        c->gq_cap, c->d_stats + c0, c->nsm, s));
         launches += 2;
-        pl.end();
+        ph.end();
     } else if (!tiled_only && !c->units.empty()) {
         ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));

@@ -14,7 +14,18 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("OCC_LIB") or os.path.join(_HERE, "libocc.so")   # OCC_LIB: A/B builds
+def _lib_path() -> str:
+    """libocc.so, or an A/B build: OCC_LIB names a library, OCC_DEFINES (and
+    OCC_LINE_STATS) select the instrumented build of build.lib_path()."""
+    if os.environ.get("OCC_LIB"):
+        return os.environ["OCC_LIB"]
+    if os.environ.get("OCC_DEFINES") or os.environ.get("OCC_LINE_STATS"):
+        from . import build
+        return build.lib_path()
+    return os.path.join(_HERE, "libocc.so")
+
+
+LIB_PATH = _lib_path()
 
 OCC_OK = 0
 OCC_ERR_INVALID_ARG = -1
@@ -31,7 +42,7 @@ EXPORTS = ["occ_default_params", "occ_create", "occ_detect", "occ_detect_host", 
            "occ_mask_bytes", "occ_set_neighbors", "occ_get_neighbors", "occ_frame_stats",
            "occ_set_frame_stats", "occ_create_dirs", "occ_scan_half_lengths"]
 MASK_FORMATS = {"u8": 0, "bits": 1}
-KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5, "nwin": 6}
+KERNEL_KINDS = {"init": 0, "stats": 1, "tile": 2, "direct": 3, "cand": 4, "line": 5, "nwin": 6, "hard": 7}
 
 
 class occ_baseline(ctypes.Structure):
