@@ -1145,8 +1145,10 @@ __global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
 #ifndef HARD_BATCH
 #define HARD_BATCH 16        // offsets (loads in flight) per k_hard step
 #endif
+// C5 k_hard ms per 256 frames (one B200, A/B): MINB 1 (71 registers) 3.49,
+// 2 3.52, 4 (64) 3.23, 5 (48) 3.53, 6 (40, spills) 3.82
 #ifndef HARD_MINB
-#define HARD_MINB 1
+#define HARD_MINB 4
 #endif
 __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
                                               MaskFmt mf, int32_t W, int64_t HW, int32_t frames, int32_t nviews,

@@ -1020,8 +1020,12 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
 // (longest first), each over the group's frames: the warps in flight work
 // on a few frames, whose D and words stay in L2.
 constexpr int kSweepWarps = 1;
+// minimum CTAs per SM of the launch bounds: a code-generation knob (the
+// kernel keeps 96 registers either way; 18 gives the smaller stack frame):
+// C5 A/B on one B200, ms per 256 frames: 16 22.06, 17 20.18, 18 20.23,
+// 19 20.66, 20 20.88, 22 / 24 (80 registers, spills) 22.8
 #ifndef SWEEP_MINB
-#define SWEEP_MINB 20
+#define SWEEP_MINB 18
 #endif
 __global__ void __launch_bounds__(32 * kSweepWarps, SWEEP_MINB) k_sweep(const __grid_constant__ SweepArgs a,
                                                                  const __grid_constant__ SweepMaps tm) {
