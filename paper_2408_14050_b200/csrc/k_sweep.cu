@@ -122,7 +122,12 @@ __global__ void __launch_bounds__(128) k_words(WordsArgs a) {
         const float *col = Df + x;
         float v = (xin && y0 < H) ? __ldg(col + (int64_t)y0 * W) : 0.0f;
         const bool l31 = lane == 31;
-#pragma unroll 4
+#ifndef WORDS_UNROLL
+#define WORDS_UNROLL 32           // (C5 k_words ms per 256 frames: unroll 2 1.52, 4 1.57, 8 1.72, 32 1.50)
+#endif
+#define S_PRAGMA(x) _Pragma(#x)
+#define S_UNROLL(n) S_PRAGMA(unroll n)
+        S_UNROLL(WORDS_UNROLL)
         for (int r = 0; r < 32; ++r) {
             const int32_t y = y0 + r;
             const bool yin = y < H, yb = y + 1 < H;

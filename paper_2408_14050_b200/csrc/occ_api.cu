@@ -345,13 +345,14 @@ void build_tiles(occ_ctx *c) {
             c->skstart[k] = n;
         }
         // frames per group: every kind's share of a group about one resident
-        // wave (148 SMs x 16 warps), and a group's D + words within ~80 MB of L2
+        // wave (148 SMs x 16 warps), and a group's D + words within ~40 MB of L2
         int32_t kmin = INT32_MAX;
         for (int k = 0; k < 4; ++k)
             if (c->skstart[k + 1] > c->skstart[k]) kmin = std::min(kmin, c->skstart[k + 1] - c->skstart[k]);
         const double fbytes = (double)H * W * 4.0 + 4.0 * (double)sweep_words_per_frame(H, W);
         const int32_t by_wave = (int32_t)std::ceil(148.0 * 16 / std::max(1, kmin));
-        const int32_t by_l2 = std::max(1, (int32_t)(80.0e6 / fbytes));
+        // (C5, 256 frames, ms: 1 19.99, 2 19.95, 3 19.90, 4 19.98, 7 20.02, 10 20.09, 14 20.29)
+        const int32_t by_l2 = std::max(1, (int32_t)(40.0e6 / fbytes));
         c->sfgroup = std::max(1, std::min(by_wave, by_l2));
         if (const char *ev = getenv("OCC_SWEEP_FGROUP")) c->sfgroup = std::max(1, atoi(ev));   // tuning knob
     }

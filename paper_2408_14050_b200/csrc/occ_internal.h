@@ -219,8 +219,10 @@ cudaError_t launch_prologue(const float *D, int32_t H, int32_t W, int32_t frames
 struct SweepUnit {
     int32_t group, l0, t0, t1;
 };
+// k_sweep unit length (positions; multiple of 32): C5 ms per 256 frames on
+// one B200 (A/B): 256 20.03, 320 19.52, 384 19.30, 448 20.14, 512 20.13
 #ifndef SWEEP_SEG
-#define SWEEP_SEG 256
+#define SWEEP_SEG 384
 #endif
 constexpr int kSweepSeg = SWEEP_SEG;
 inline int64_t sweep_words_per_frame(int32_t H, int32_t W) {

@@ -12,8 +12,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 # the main step only (warm-up + timed steps of the C5 detection): kernel shares of the step
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-fuse --nwin 0 --no-dirs --no-small --no-e2e > gpurun_out/plain_main.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_main.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-fuse --nwin 0 --no-dirs --no-small --no-e2e > gpurun_out/ncu_launch_main.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_line -s 2 -c 1 -o gpurun_out/prof_line python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hard -s 2 -c 1 -o gpurun_out/prof_hard python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full_hard.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cand -s 2 -c 1 -o gpurun_out/prof_cand python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full_cand.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_nwin -s 2 -c 1 -o gpurun_out/prof_nwin python bench.py --steps 2 --warmup 3 --no-cpu --no-fuse > gpurun_out/ncu_full_nwin.log 2>&1
+M="--steps 2 --warmup 3 --no-cpu --no-fuse --nwin 0 --no-dirs --no-small --no-e2e"
+grep -q '"metric"' gpurun_out/plain_main.log && for k in k_sweep k_words k_hard; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_$k python bench.py $M > gpurun_out/ncu_full_$k.log 2>&1
+done
 echo done

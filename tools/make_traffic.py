@@ -1,7 +1,8 @@
 """Write profiles/ncu_traffic.json from `ncu --set full` captures of one
-25-frame chunk: DRAM bytes (read + write) of k_line + k_hard, the kernels of
-bench.py's "line" scope (k_cand + k_line + k_hard).
-Usage: make_traffic.py [--frames N] rep1.ncu-rep rep2.ncu-rep ..."""
+frame chunk: DRAM bytes (read + write) of the dominant kernel of bench.py's
+roofline ("line" = k_sweep), with the other kernels of the chunk listed
+beside it (k_words, k_hard).
+Usage: make_traffic.py --frames N sweep.ncu-rep [words.ncu-rep hard.ncu-rep ...]"""
 import csv
 import io
 import json
@@ -24,16 +25,18 @@ def dram(rep):
 
 
 args = sys.argv[1:]
-frames = 207                                 # first chunk at the default 2 GiB
+frames = 128
 if args and args[0] == "--frames":
     frames = int(args[1])
     args = args[2:]
 parts = [dram(r) for r in args]
 H, W, V = 1080, 1920, 8
-res = {"kernel": "line", "bytes_per_launch": sum(p[0] for p in parts),
-       "alg_bytes_per_launch": frames * H * W * (4 + V),
+alg = frames * H * W * (4 + V)
+res = {"kernel": "line", "bytes_per_launch": parts[0][0], "alg_bytes_per_launch": alg,
+       "ratio": parts[0][0] / alg,
        "parts": {p[1][:60]: p[0] for p in parts},
-       "source": f"ncu --set full --clock-control none, one {frames}-frame C5 chunk (bench --steps 2 --warmup 3)"}
+       "source": f"ncu --set full --clock-control none, one {frames}-frame C5 chunk "
+                 f"(bench --steps 2 --warmup 3, main step only)"}
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 with open(os.path.join(root, "profiles", "ncu_traffic.json"), "w") as f:
     json.dump(res, f, indent=1)
