@@ -460,6 +460,50 @@ def small_leg():
     return res
 
 
+H_SWEEP = (4, 8, 16, 48, 96, 150, 300, 600)
+
+
+def h_sweep_leg(frames_np, views, peak, frames=32, reps=3):
+    """Eq. 3's h sets each window's length; the paper's own
+    data (SceneFlow) spans small to large disparity ranges.
+    The bench's C5 frames scaled to a target h (scenes.scale_disparity, the
+    C3 scene with every disparity mapped d -> 1 + k (d - 1)); device ms per
+    frame and the time per pixel-view relative to the unscaled frames."""
+    import torch
+    from paper_2408_14050_b200 import scenes
+    from paper_2408_14050_b200.occ import Detector
+    B = min(frames, frames_np.shape[0])
+    _, h, w = frames_np.shape
+    det = Detector(h, w, views, max_batch=B)
+    out = torch.empty((B, len(views), h, w), dtype=torch.uint8, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def run(D):
+        d = torch.from_numpy(D).cuda()
+        det.detect(d, out=out)
+        torch.cuda.synchronize()
+        hv = det.frame_info(0)[2]
+        e0.record()
+        for _ in range(reps):
+            det.detect(d, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps, hv
+
+    base_ms, base_h = run(frames_np[:B])
+    rows = []
+    for ht in H_SWEEP:
+        k = ht / float(max(1, base_h[0]))
+        ms, hv = run(scenes.scale_disparity(frames_np[:B], k))
+        rows.append({"h_target": ht, "h": hv[0], "ms_per_frame": ms / B,
+                     "mpvs": B * h * w * len(views) / (ms / 1e3) / 1e6,
+                     "time_per_pv_vs_base": ms / base_ms})
+    det.close()
+    return {"frames": B, "base": {"h": base_h[0], "ms_per_frame": base_ms / B,
+                                  "mpvs": B * h * w * len(views) / (base_ms / 1e3) / 1e6},
+            "scaled": rows}
+
+
 def c4_leg(peak, frames=2):
     """BASELINE config 4 (4096x3072, 5x5 array, 24 views incl. s = 2 and the
     knight families): device time of one occ_detect over `frames` frames."""
@@ -688,6 +732,7 @@ def main():
     dirs = None if args.no_dirs else dirs_leg(d, masks, nf, args)
     small = None if (args.no_small or rank != 0) else small_leg()
     c4 = None if (args.no_small or rank != 0) else c4_leg(peak)
+    hsw = None if (args.no_small or rank != 0) else h_sweep_leg(frames, views, peak)
 
     if rank != 0:
         return
@@ -708,7 +753,7 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_bits": e2e_bits, "device_bits": dev_bits,
         "parity": parity, "clocks": clk.summary(),
         "gpu_launches": launches, "path": args.path,
-        "fuse_median": fuse, "finite_n": nwin, "directions": dirs, "small_configs": small, "c4": c4, "mask_gather": gather,
+        "fuse_median": fuse, "finite_n": nwin, "directions": dirs, "small_configs": small, "c4": c4, "h_sweep": hsw, "mask_gather": gather,
     }
     print(json.dumps(line), flush=True)
 

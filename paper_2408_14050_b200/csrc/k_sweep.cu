@@ -26,6 +26,7 @@
 //   kind 2 diagonals b0 = ( 1, 1): pixel (tau - l, l0 + tau)          line y - x
 //   kind 3 anti-diag b0 = ( 1,-1): pixel (tau - 31 + l, l0 + 31 - tau) line x + y
 // View +b0 ("P") has its occluders at larger tau, view -b0 ("N") at smaller.
+#include <algorithm>
 #include <climits>
 
 #include <cuda.h>
@@ -66,6 +67,25 @@ __device__ __forceinline__ uint32_t s_transpose32(uint32_t x, int lane) {
         x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
     }
     return x;
+}
+// bits [st, st + 32) of the OR-dilation of the 96-bit x = x0 | x1 << 32 |
+// x2 << 64 by a window of w bits (bit t = OR of x[t .. t + w - 1]);
+// 1 <= w <= 33, 0 <= st, st + 31 + w - 1 < 96 (window coverage for h < 17)
+__device__ __forceinline__ uint32_t s_dil(uint32_t x0, uint32_t x1, uint32_t x2, int32_t w, int32_t st) {
+    int32_t c = 1;
+    while (2 * c <= w) {
+        x0 |= __funnelshift_r(x0, x1, c);
+        x1 |= __funnelshift_r(x1, x2, c);
+        x2 |= x2 >> c;
+        c *= 2;
+    }
+    if (c < w) {
+        const int32_t k = w - c;
+        x0 |= __funnelshift_r(x0, x1, k);
+        x1 |= __funnelshift_r(x1, x2, k);
+        x2 |= x2 >> k;
+    }
+    return st < 32 ? __funnelshift_r(x0, x1, st) : __funnelshift_r(x1, x2, st - 32);
 }
 __device__ __forceinline__ void s_cp16(float *dst, const float *src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -729,6 +749,7 @@ __device__ __forceinline__ void s_resolve(const SweepArgs &a, const SU &u, const
     __syncwarp();
 }
 
+template <bool SMALLH>
 __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm, const SweepUnit &un,
                                         const GroupDesc &gd, int32_t f, unsigned char *smem, uint32_t *phase) {
     const FamilyDesc &fd = a.fams[gd.fam];
@@ -768,10 +789,11 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
         s_direct(u, a, gd, fd, T0, T1, true);
         return;
     }
-    if (h < 17) {                                 // window coverage below needs 2h >= 34
-        s_direct(u, a, gd, fd, T0, T1, false);
-        return;
-    }
+    // h < 17: window coverage from OR-dilations of the raw candidate words
+    // (s_dil) instead of the first / last candidate thresholds (which need
+    // 2h >= 34); those units run in k_sweep_small
+    if (!SMALLH && h < 17) return;
+    constexpr bool smallh = SMALLH;
     const int32_t reach = partner_reach(a.p.t_dist, s, R, h);
     const int32_t nbr = (reach + 3 + 31) >> 5;    // staged warm-up blocks per pass
     const int32_t nbl = (T1 - T0) / 32 + nbr;     // blocks per pass
@@ -882,7 +904,7 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
         uint32_t pw_hi = s_word1(u, kW + hq + 1, 0), nw_hi = s_word1(u, kW + nq + 1, 1);
         uint32_t pq0 = s_word1(u, kW + hq, 0), pq1 = s_word1(u, kW - 1 + hq, 0), pq2 = s_word1(u, kW - 2 + hq, 0);
         uint32_t nq0 = s_word1(u, kW + nq, 1), nq1 = s_word1(u, kW - 1 + nq, 1), nq2 = s_word1(u, kW - 2 + nq, 1);
-        uint32_t WNprev = 0u;
+        uint32_t WNprev = 0u, nw_hh = 0u;
         float v1 = NaN, v2 = NaN, v3 = NaN, A1 = NaN, A2 = NaN, A3 = NaN, SX = -INFINITY, VM = NaN;
         int slot = 0;
         bool bt[2] = {false, false};
@@ -893,9 +915,13 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
             pq0 = pq1; pq1 = pq2; pq2 = s_word1(u, k - 3 + hq, 0);
             nq0 = nq1; nq1 = nq2; nq2 = s_word1(u, k - 3 + nq, 1);
             const uint32_t WP = __funnelshift_r(pw_lo, pw_hi, hr);      // +b candidates [tau0 + h, tau0 + h + 31]
+            const uint32_t rP2 = pw_hi;                                 // (small h: raw word of block k + 1)
             pw_hi = pw_lo;
             if (WP) fc = tau0 + h + __ffs(WP) - 1;
             const uint32_t WN = __funnelshift_r(nw_lo, nw_hi, nsh);     // -b candidates [tau0 - h, tau0 - h + 31]
+            // raw candidate words of blocks k - 1, k, k + 1 (small h: hq = 0, nq = -1)
+            const uint32_t rP0 = pq0, rP1 = pw_lo, rN0 = nw_lo, rN1 = nw_hi, rN2 = nw_hh;
+            nw_hh = nw_hi;
             nw_hi = nw_lo;
             if (WNprev) ncl = tau0 + 32 - h + __ffs(WNprev) - 1;
             WNprev = WN;
@@ -974,21 +1000,36 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
             const Rec rr = rec[(k - kB) * 32 + lane];
             // view +b: pairs (i, i + j) covered <=> a +b candidate in [i + j - h, i + h]
             const int32_t pcl = tau0 + rr.pclP;
-            const uint32_t cPa = s_ge(fc - h - tau0);
-            const uint32_t cP1 = cPa | s_le(pcl + h - 1 - tau0);
-            const uint32_t cP2 = cPa | s_le(pcl + h - 2 - tau0);
-            const uint32_t cP3 = cPa | s_le(pcl + h - 3 - tau0);
-            const uint32_t cPf = s_ge(fc - h + 1 - tau0) | s_le(pcl + h - tau0);
+            uint32_t cP1, cP2, cP3, cPf, cN1, cN2, cN3, cNf;
+            const int32_t lc = tau0 + rr.lcN;
+            if (!smallh) {
+                const uint32_t cPa = s_ge(fc - h - tau0);
+                cP1 = cPa | s_le(pcl + h - 1 - tau0);
+                cP2 = cPa | s_le(pcl + h - 2 - tau0);
+                cP3 = cPa | s_le(pcl + h - 3 - tau0);
+                cPf = s_ge(fc - h + 1 - tau0) | s_le(pcl + h - tau0);
+                const uint32_t cNa = s_le(lc + h - tau0);
+                cN1 = cNa | s_ge(ncl + 1 - h - tau0);
+                cN2 = cNa | s_ge(ncl + 2 - h - tau0);
+                cN3 = cNa | s_ge(ncl + 3 - h - tau0);
+                cNf = s_le(lc + h - 1 - tau0) | s_ge(ncl - h - tau0);
+            } else {
+                // pair (a, b), a < b, covered <=> a candidate in [b - h, a + h]
+                // (S8/S9): bit r of a window mask = OR of the block's
+                // candidate bits over [r + lo, r + lo + w - 1]
+                cP1 = s_dil(rP0, rP1, rP2, 2 * h, 32 + 1 - h);        // (i, i + j): [i + j - h, i + h]
+                cP2 = s_dil(rP0, rP1, rP2, 2 * h - 1, 32 + 2 - h);
+                cP3 = s_dil(rP0, rP1, rP2, 2 * h - 2, 32 + 3 - h);
+                cPf = s_dil(rP0, rP1, rP2, 2 * h, 32 - h);            // (i - 1, i): [i - h, i - 1 + h]
+                cN1 = s_dil(rN0, rN1, rN2, 2 * h, 32 - h);            // (i - j, i): [i - h, i - j + h]
+                cN2 = s_dil(rN0, rN1, rN2, 2 * h - 1, 32 - h);
+                cN3 = s_dil(rN0, rN1, rN2, 2 * h - 2, 32 - h);
+                cNf = s_dil(rN0, rN1, rN2, 2 * h, 32 + 1 - h);        // (i, i + 1): [i + 1 - h, i + h]
+            }
             uint32_t mP = ((T1 & ~Xs1) & cP1) | ((T2 & ~Xs2) & cP2);
             if (NFWD) mP |= (((TF & Xs1) << 1) | (tfm & s1m)) & cPf;
             mP &= ext;
             // view -b: pairs (i - j, i) covered <=> a -b candidate in [i - h, i - j + h]
-            const int32_t lc = tau0 + rr.lcN;
-            const uint32_t cNa = s_le(lc + h - tau0);
-            const uint32_t cN1 = cNa | s_ge(ncl + 1 - h - tau0);
-            const uint32_t cN2 = cNa | s_ge(ncl + 2 - h - tau0);
-            const uint32_t cN3 = cNa | s_ge(ncl + 3 - h - tau0);
-            const uint32_t cNf = s_le(lc + h - 1 - tau0) | s_ge(ncl - h - tau0);
             const uint32_t n1 = ((T1 & Xs1) << 1) | (t1m & s1m);
             const uint32_t n2 = ((T2 & Xs2) << 2) | ((t2m1 & s2m1) << 1) | (t2m2 & s2m2);
             uint32_t mN = (n1 & cN1) | (n2 & cN2);
@@ -1056,7 +1097,39 @@ __global__ void __launch_bounds__(32 * kSweepWarps, SWEEP_MINB) k_sweep(const __
     }
     __syncwarp();
     uint32_t phase[2] = {0u, 0u};
-    sweep_unit(a, tm, un, gd, f, sm, phase);
+    sweep_unit<false>(a, tm, un, gd, f, sm, phase);
+}
+
+// The units of frames with 0 < h < 17 (the ones k_sweep skips): persistent
+// warps walk the frames, and every (small-h frame, unit) pair is taken by one
+// warp in turn.  smin = the smallest s of the sweep's groups (h grows with s).
+__global__ void __launch_bounds__(32, SWEEP_MINB) k_sweep_small(const __grid_constant__ SweepArgs a,
+                                                       const __grid_constant__ SweepMaps tm, int32_t smin) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kBarOff);
+    if ((threadIdx.x & 31) == 0) {
+        s_mbar_init(bars, 1);
+        s_mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t phase[2] = {0u, 0u};
+    uint32_t item = 0;
+    for (int32_t f = 0; f < a.frames; ++f) {
+        const FrameStats fs = a.st[f];
+        const float R = frame_range(fs);
+        if (fs.nonfinite || view_h(R, smin, a.p.max_scan) >= 17) continue;
+        // this warp's units of the frame: items item + i with (item + i) % grid == block
+        const uint32_t G = gridDim.x;
+        const uint32_t i0 = (blockIdx.x + G - item % G) % G;
+        item += (uint32_t)a.nunits;
+        for (uint32_t i = i0; i < (uint32_t)a.nunits; i += G) {
+            const SweepUnit un = a.units[i];
+            const GroupDesc gd = a.groups[un.group];
+            const int32_t h = view_h(R, a.views[gd.view[0]].s, a.p.max_scan);
+            if (h > 0 && h < 17) sweep_unit<true>(a, tm, un, gd, f, smem, phase);
+        }
+    }
 }
 
 // host: TMA descriptors of the chunk's D ([frames][H][W] fp32)
@@ -1089,7 +1162,7 @@ cudaError_t launch_sweep(const float *D, int32_t H, int32_t W, int32_t frames, c
                          const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
                          const MaskFmt &mf, const uint32_t *words, HardEntry *gq, uint32_t *gq_count,
                          int32_t gq_cap, const int32_t *kstart, int32_t fgroup, unsigned long long *dbg,
-                         cudaStream_t s) {
+                         int32_t smin_hint, cudaStream_t s) {
     if (nunits <= 0 || frames <= 0) return cudaSuccess;
     SweepArgs a{};
     for (int k = 0; k < 5; ++k) a.kstart[k] = kstart[k];
@@ -1110,6 +1183,14 @@ cudaError_t launch_sweep(const float *D, int32_t H, int32_t W, int32_t frames, c
     cudaFuncSetAttribute(k_sweep, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     const int64_t nw = (int64_t)nunits * frames;
     k_sweep<<<(unsigned)((nw + kSweepWarps - 1) / kSweepWarps), 32 * kSweepWarps, smem, s>>>(a, tm);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // units of frames with h < 17 (data dependent: known on the device only)
+    const int32_t smin = std::max(1, smin_hint);
+    e = cudaFuncSetAttribute(k_sweep_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepWarpSmem);
+    if (e != cudaSuccess) return e;
+    // one resident wave of 1-warp CTAs (148 SMs x SWEEP_MINB)
+    k_sweep_small<<<(unsigned)std::min<int64_t>(nw, 148 * SWEEP_MINB), 32, kSweepWarpSmem, s>>>(a, tm, smin);
     return cudaGetLastError();
 }
 

@@ -47,6 +47,7 @@ struct occ_ctx {
     uint32_t *d_words = nullptr;          // k_words -> k_sweep candidate words, one chunk of frames
     int32_t skstart[5] = {0, 0, 0, 0, 0}; // sunits of kind k at [skstart[k], skstart[k + 1])
     int32_t sfgroup = 1;                  // k_sweep work order: frames per group
+    int32_t ssmin = 1;                    // smallest s of the k_sweep groups (k_sweep_small's frame filter)
     std::vector<LineUnit> units;          // k_line work (eligible groups, OCC_SWEEP=0)
     std::vector<TileDesc> all_tiles;      // k_tile work for every group (OCC_PATH_TILED)
     LineUnit *d_units = nullptr;
@@ -333,6 +334,9 @@ void build_tiles(occ_ctx *c) {
             if (seg <= 32 || (double)c->sunits.size() * c->max_batch >= 148.0 * fill) break;
             seg = std::max(32, (seg / 2) & ~31);
         }
+        c->ssmin = INT32_MAX;
+        for (const SweepUnit &x : c->sunits) c->ssmin = std::min(c->ssmin, c->views[c->groups[x.group].view[0]].s);
+        if (c->sunits.empty()) c->ssmin = 1;
         // by kind, longest first inside a kind (k_sweep's work order, k_sweep.cu)
         auto kind_of = [&](const SweepUnit &x) { return c->fams[c->groups[x.group].fam].kind; };
         std::stable_sort(c->sunits.begin(), c->sunits.end(), [&](const SweepUnit &x, const SweepUnit &y) {
@@ -440,13 +444,17 @@ void build_tiles(occ_ctx *c) {
     }
 }
 
-// Capacity of the k_line / k_sweep -> k_hard queue: 1/16 of a chunk's
-// pixel-views, clamped to [64 Ki, 256 Mi] entries.  OCC_GQ_CAP (test knob, read at
-// occ_create) overrides it, e.g. to force the capacity-overflow path.
+// Capacity of the k_line / k_sweep -> k_hard queue: 1/2 of a chunk's
+// pixel-views, clamped to [64 Ki, 512 Mi] entries (16 B each: at most 8 GiB
+// of the 180 GB).  Survivors grow with the occluded fraction, which grows
+// with h: C5 frames (h ~ 66) queue 1.4 % of their pixel-views, the same
+// frames scaled to h ~ 300 about 10 %, to h ~ 600 about 30 %; past the
+// capacity the sweep warps search in-warp (exact, ~30x slower at h = 300).  OCC_GQ_CAP (test knob,
+// read at occ_create) overrides it, e.g. to force the capacity-overflow path.
 int32_t gq_capacity(int32_t chunk, int32_t H, int32_t W, int32_t n_views) {
     const char *ev = getenv("OCC_GQ_CAP");
     if (ev && atoi(ev) > 0) return atoi(ev);
-    return (int32_t)std::min<double>(256.0 * 1048576.0, std::max(65536.0, (double)chunk * H * W * n_views / 16.0));
+    return (int32_t)std::min<double>(512.0 * 1048576.0, std::max(65536.0, (double)chunk * H * W * n_views / 2.0));
 }
 
 }  // namespace
@@ -815,12 +823,12 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
 #endif
         CK(launch_sweep(Dc, c->H, c->W, n, c->d_sunits, (int32_t)c->sunits.size(), c->d_groups, c->d_views, c->V,
                         c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_words, c->d_gq, c->d_gq_count,
-                        c->gq_cap, c->skstart, c->sfgroup, c->d_dbg, s));
+                        c->gq_cap, c->skstart, c->sfgroup, c->d_dbg, c->ssmin, s));
         pl.end();
         ProfScope ph(c, OCC_KERNEL_HARD, s);
         CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
                        c->gq_cap, c->d_stats + c0, c->nsm, s));
-        launches += 2;
+        launches += 3;       // k_sweep, k_sweep_small, k_hard
         ph.end();
     } else if (!tiled_only && !c->units.empty()) {
         ProfScope pl(c, OCC_KERNEL_LINE, s);

@@ -236,6 +236,6 @@ cudaError_t launch_sweep(const float *D, int32_t H, int32_t W, int32_t frames, c
                          const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
                          const MaskFmt &mf, const uint32_t *words, HardEntry *gq, uint32_t *gq_count,
                          int32_t gq_cap, const int32_t *kstart, int32_t fgroup, unsigned long long *dbg,
-                         cudaStream_t s);
+                         int32_t smin, cudaStream_t s);
 
 }  // namespace occ

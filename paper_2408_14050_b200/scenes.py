@@ -180,6 +180,14 @@ def make_scene(cfg: int, seed: int = 0, frame: int = 0) -> np.ndarray:
     return img.astype(np.float32)
 
 
+def scale_disparity(D: np.ndarray, scale: float) -> np.ndarray:
+    """The same layered scene with every disparity mapped d -> 1 + scale*(d - 1)
+    (fp64, one fp32 rounding).  Scaling the C3 recipe sets the frame's
+    disparity range, and with it Eq. 3's scan half-length h (about 66*scale
+    for C3 frames); bench.py's h sweep and the GPU h tests use it."""
+    return (1.0 + float(scale) * (np.asarray(D, dtype=np.float64) - 1.0)).astype(np.float32)
+
+
 def c1_rect_origin(seed: int = 0, frame: int = 0) -> Tuple[int, int]:
     rng = SplitMix64(1, seed, frame)
     x0 = rng.randint(7, 44)

@@ -1,0 +1,56 @@
+"""GPU parity across Eq. 3's scan half-length h.
+
+h follows the frame's disparity range, so the window length, the far-partner
+reach and the kernels' warm-up spans change with the data.  The C3 recipe is
+scaled (scenes.scale_disparity) so each crop's own range gives h near the
+targets of bench.py's h sweep (4 .. 600); the masks must equal the oracle's
+bit for bit in every case, including batches whose frames have different h.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2408_14050_b200 import scenes
+from test_gpu_parity import assert_same, run_gpu, torch_cuda  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+H_TARGETS = [4, 8, 16, 17, 48, 96, 150, 300, 600]
+
+
+def scaled_crop(h_target, y0, x0, hh, ww, frame=0):
+    D = scenes.make_scene(3, 0, frame)[y0:y0 + hh, x0:x0 + ww].astype(np.float64)
+    R = float(D.max() - D.min())
+    # d -> 1 + k (d - 1) scales the range by k; h = floor(ceil(2 R') / 2) ~ R'
+    return scenes.scale_disparity(D, h_target / R)
+
+
+@pytest.mark.parametrize("h_target", H_TARGETS)
+def test_h_range_3x3(torch_cuda, h_target):
+    hh, ww = (256, 512) if h_target <= 150 else (160, 320)
+    D = scaled_crop(h_target, 300, 700, hh, ww)
+    views = scenes.VIEWS_3X3
+    o = oracle.detect(D, views)
+    g, st = run_gpu(torch_cuda, D, views)
+    assert st == [0]
+    assert_same(g[0], o, f"h target {h_target}")
+
+
+def test_h_range_mixed_batch(torch_cuda):
+    # one call, frames with h ~ 5, 66 (unscaled), 200: every frame its own h
+    D = np.stack([scaled_crop(5, 100, 100, 200, 400, 1), scaled_crop(66, 500, 900, 200, 400, 2),
+                  scaled_crop(200, 700, 1300, 200, 400, 3)])
+    views = scenes.VIEWS_3X3
+    g, st = run_gpu(torch_cuda, D, views)
+    assert st == [0, 0, 0]
+    for f in range(3):
+        assert_same(g[f], oracle.detect(D[f], views), f"frame {f}")
+
+
+@pytest.mark.parametrize("h_target", [6, 40])
+def test_h_range_s2(torch_cuda, h_target):
+    # s = 2 views: h doubles (Eq. 3 in major-axis pixels, reading Q6)
+    D = scaled_crop(h_target, 200, 400, 192, 384)
+    views = [(2, 0), (-2, 0), (0, 2), (2, 2), (1, 0)]
+    g, st = run_gpu(torch_cuda, D, views)
+    assert_same(g[0], oracle.detect(D, views), f"s=2 h target {h_target}")
