@@ -1150,12 +1150,17 @@ __global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
 #ifndef HARD_MINB
 #define HARD_MINB 4
 #endif
+// SHEAR: the entries of a knight family swept through its sheared copy
+// (k_shear): D, W, HW are the sheared frame's, the line step is 1 (rows) or
+// W (columns), and the mask pixel is un-sheared (ShearDesc, occ_internal.h)
+__device__ __forceinline__ int32_t h_fdiv(int32_t a, int32_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+template <bool SHEAR>
 __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
                                               MaskFmt mf, int32_t W, int64_t HW, int32_t frames, int32_t nviews,
                                               const ViewDesc *__restrict__ views,
                                               Params p, const HardEntry *__restrict__ gq,
                                               const uint32_t *__restrict__ gq_count, int32_t gq_cap,
-                                              const FrameStats *__restrict__ st) {
+                                              const FrameStats *__restrict__ st, ShearDesc sh) {
     const uint32_t n = min(*gq_count, (uint32_t)gq_cap);
     const float NaN = __int_as_float(0x7fc00000);
     // newest entries first: their frames were swept last and are still in L2
@@ -1166,7 +1171,7 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
         OCC_CHECK(f < frames && v < nviews && he.pix >= 0 && (int64_t)he.pix < HW);
         const ViewDesc &vdv = views[v];
         const int32_t s = vdv.s;
-        const int32_t step = (vdv.sg > 0 ? 1 : -1) * line_stride(vdv.lkind, W);
+        const int32_t step = (vdv.sg > 0 ? 1 : -1) * (SHEAR ? (sh.kind == 0 ? 1 : W) : line_stride(vdv.lkind, W));
         ViewK vk;
         vk.s = s; vk.h = 0; vk.fs = (float)s; vk.T = 0.0f;
         vk.tlo = __fsub_rn(p.t_dist, 0x1p-10f);
@@ -1222,15 +1227,28 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
                         hit = pair_exact_slow(__ldg(Ds + (int64_t)(j0 + u) * step), vp, j0 + u, s, p.t_dist, p.t_disp);
             }
         }
-        if (hit) mask_put(masks + ((int64_t)f * nviews + v) * mf.vbytes, mf, W, he.pix % W, he.pix / W, true);
+        if (hit) {
+            uint8_t *Mv = masks + ((int64_t)f * nviews + v) * mf.vbytes;
+            if constexpr (SHEAR) {
+                const int32_t q = he.pix / W, r = he.pix % W;
+                if (sh.kind == 0) mask_put(Mv, mf, sh.Wo, r, q + sh.lmin + h_fdiv(r * sh.num, sh.den), true);
+                else mask_put(Mv, mf, sh.Wo, r + sh.lmin + h_fdiv(q * sh.num, sh.den), q, true);
+            } else {
+                mask_put(Mv, mf, W, he.pix % W, he.pix / W, true);
+            }
+        }
     }
 }
 
 cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW, int32_t frames,
                         int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
-                        const FrameStats *st, int32_t nsm, cudaStream_t s) {
-    k_hard<<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, frames, nviews, views, p, gq, gq_count, gq_cap, st);
+                        const FrameStats *st, int32_t nsm, cudaStream_t s, const ShearDesc *sh) {
+    if (sh)
+        k_hard<true><<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, frames, nviews, views, p, gq, gq_count, gq_cap, st, *sh);
+    else
+        k_hard<false><<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, frames, nviews, views, p, gq, gq_count, gq_cap, st,
+                                              ShearDesc{});
     return cudaGetLastError();
 }
 

@@ -251,6 +251,12 @@ struct SweepArgs {
     uint32_t *gq_count;
     int32_t gq_cap;
     int32_t tma;               // 1: TMA staging (W % 4 == 0, 16-byte aligned frames); 0: 4-byte cp.async
+    // Sheared family (knight baselines, k_shear): D is the sheared copy whose
+    // rows (shkind 0, x-major) or columns (shkind 1, y-major) are the
+    // family's digital lines; line l' of it is the image line l = l' + sh_lmin,
+    // whose pixel at position tau is (tau, l + floor(tau num / den)) or
+    // (l + floor(tau num / den), tau) of the Ho x Wo image the masks cover.
+    int32_t shkind, sh_num, sh_den, sh_lmin, Ho, Wo;
     unsigned long long *dbg;   // event counters (SWEEP_STATS builds), or null
 };
 // TMA descriptors of D viewed as [frames][H][W] fp32 (out-of-image boxes read NaN)
@@ -527,6 +533,43 @@ __device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf
     }
 }
 
+__device__ __forceinline__ int32_t s_fdiv(int32_t a, int32_t b) {      // floor(a / b), b > 0
+    return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+// masks of a sheared family (knight baselines): bit r of the lane's word is
+// line l0 + lane at tau = 32k + r; un-shear to the image pixel and write it
+// (uint8: every in-image byte of the unit's lines; packed: set bits)
+__device__ __noinline__ void s_store_sh(const SU &u, const SweepArgs &a, uint8_t *Mv, uint32_t word, int32_t k) {
+    const int lane = u.lane;
+    const int32_t Ho = a.Ho, Wo = a.Wo;
+    const bool packed = a.mf.packed != 0;
+    uint32_t *P = reinterpret_cast<uint32_t *>(Mv);
+    if (u.kind == 0) {                    // x-major: pixel (tau, l + f(tau))
+        if (u.l0 + lane >= u.H) return;
+        const int32_t L = u.l0 + lane + a.sh_lmin;
+        for (int r = 0; r < 32; ++r) {
+            const int32_t x = 32 * k + r;
+            const int32_t y = L + s_fdiv(x * a.sh_num, a.sh_den);
+            if (x < 0 || x >= Wo || (uint32_t)y >= (uint32_t)Ho) continue;
+            const uint32_t b = (word >> r) & 1u;
+            if (!packed) __stcs(Mv + (int64_t)y * Wo + x, (uint8_t)b);
+            else if (b) atomicOr(P + (int64_t)y * a.mf.Wb + (x >> 5), 1u << (x & 31));
+        }
+    } else {                              // y-major: lane r <- row tau = 32k + r, bit j = line l0 + j
+        const uint32_t t = s_transpose32(word, lane);
+        const int32_t y = 32 * k + lane;
+        if (y < 0 || y >= Ho) return;
+        const int32_t x0 = u.l0 + a.sh_lmin + s_fdiv(y * a.sh_num, a.sh_den);
+        for (int j = 0; j < 32; ++j) {
+            const int32_t x = x0 + j;
+            if (u.l0 + j >= u.W || (uint32_t)x >= (uint32_t)Wo) continue;
+            const uint32_t b = (t >> j) & 1u;
+            if (!packed) __stcs(Mv + (int64_t)y * Wo + x, (uint8_t)b);
+            else if (b) atomicOr(P + (int64_t)y * a.mf.Wb + (x >> 5), 1u << (x & 31));
+        }
+    }
+}
+
 // Eq. 5 for a far pair (offset j >= jstar: delta > t_disp is implied):
 // |s fl(vq - vp) - j| < t_dist; fp32 with a 2^-10 band, binary64 inside it.
 __device__ __noinline__ bool s_pair_slow(float vq, float vp, int32_t j, int32_t s, float t_dist, float t_disp) {
@@ -749,12 +792,12 @@ __device__ __forceinline__ void s_resolve(const SweepArgs &a, const SU &u, const
     __syncwarp();
 }
 
-template <bool SMALLH>
+template <bool SMALLH, bool SHEAR>
 __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &tm, const SweepUnit &un,
                                         const GroupDesc &gd, int32_t f, unsigned char *smem, uint32_t *phase) {
     const FamilyDesc &fd = a.fams[gd.fam];
     SU u;
-    u.kind = fd.kind;
+    u.kind = SHEAR ? a.shkind : fd.kind;
     const int kind = u.kind;
     u.l0 = un.l0;
     u.A = un.l0 >> 5;
@@ -786,7 +829,14 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
     const int32_t s = vd0.s;
     const int32_t h = view_h(R, s, a.p.max_scan);
     if (fs.nonfinite || h <= 0) {                 // SPEC.md:76 reject / Q17: zero masks
-        s_direct(u, a, gd, fd, T0, T1, true);
+        if constexpr (SHEAR) {        // zeros through the un-shearing store
+            for (int32_t k = T0 >> 5; k < (T1 >> 5); ++k) {
+                if (vP >= 0) s_store_sh(u, a, a.masks + ((int64_t)f * a.nviews + vP) * a.mf.vbytes, 0u, k);
+                if (vN >= 0) s_store_sh(u, a, a.masks + ((int64_t)f * a.nviews + vN) * a.mf.vbytes, 0u, k);
+            }
+        } else {
+            s_direct(u, a, gd, fd, T0, T1, true);
+        }
         return;
     }
     // h < 17: window coverage from OR-dilations of the raw candidate words
@@ -1055,8 +1105,13 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
             __syncwarp();
             if (kNSlot == 2) slot ^= 1;
             else if (k - 1 >= kB) bt[0] = s_stage(u, tm, stg, bars, k - 1, tma);
-            if (vP >= 0) s_store(u, MP, a.mf, mP, k);
-            if (vN >= 0) s_store(u, MN, a.mf, mN, k);
+            if constexpr (SHEAR) {
+                if (vP >= 0) s_store_sh(u, a, MP, mP, k);
+                if (vN >= 0) s_store_sh(u, a, MN, mN, k);
+            } else {
+                if (vP >= 0) s_store(u, MP, a.mf, mP, k);
+                if (vN >= 0) s_store(u, MN, a.mf, mN, k);
+            }
         }
     }
 }
@@ -1073,6 +1128,7 @@ constexpr int kSweepWarps = 1;
 #ifndef SWEEP_MINB
 #define SWEEP_MINB 18
 #endif
+template <bool SHEAR>
 __global__ void __launch_bounds__(32 * kSweepWarps, SWEEP_MINB) k_sweep(const __grid_constant__ SweepArgs a,
                                                                  const __grid_constant__ SweepMaps tm) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -1097,12 +1153,13 @@ __global__ void __launch_bounds__(32 * kSweepWarps, SWEEP_MINB) k_sweep(const __
     }
     __syncwarp();
     uint32_t phase[2] = {0u, 0u};
-    sweep_unit<false>(a, tm, un, gd, f, sm, phase);
+    sweep_unit<false, SHEAR>(a, tm, un, gd, f, sm, phase);
 }
 
 // The units of frames with 0 < h < 17 (the ones k_sweep skips): persistent
 // warps walk the frames, and every (small-h frame, unit) pair is taken by one
 // warp in turn.  smin = the smallest s of the sweep's groups (h grows with s).
+template <bool SHEAR>
 __global__ void __launch_bounds__(32, SWEEP_MINB) k_sweep_small(const __grid_constant__ SweepArgs a,
                                                        const __grid_constant__ SweepMaps tm, int32_t smin) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -1127,7 +1184,7 @@ __global__ void __launch_bounds__(32, SWEEP_MINB) k_sweep_small(const __grid_con
             const SweepUnit un = a.units[i];
             const GroupDesc gd = a.groups[un.group];
             const int32_t h = view_h(R, a.views[gd.view[0]].s, a.p.max_scan);
-            if (h > 0 && h < 17) sweep_unit<true>(a, tm, un, gd, f, smem, phase);
+            if (h > 0 && h < 17) sweep_unit<true, SHEAR>(a, tm, un, gd, f, smem, phase);
         }
     }
 }
@@ -1162,9 +1219,14 @@ cudaError_t launch_sweep(const float *D, int32_t H, int32_t W, int32_t frames, c
                          const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
                          const MaskFmt &mf, const uint32_t *words, HardEntry *gq, uint32_t *gq_count,
                          int32_t gq_cap, const int32_t *kstart, int32_t fgroup, unsigned long long *dbg,
-                         int32_t smin_hint, cudaStream_t s) {
+                         int32_t smin_hint, const ShearDesc *sh, cudaStream_t s) {
     if (nunits <= 0 || frames <= 0) return cudaSuccess;
     SweepArgs a{};
+    a.shkind = -1;
+    if (sh) {
+        a.shkind = sh->kind; a.sh_num = sh->num; a.sh_den = sh->den; a.sh_lmin = sh->lmin;
+        a.Ho = sh->Ho; a.Wo = sh->Wo;
+    }
     for (int k = 0; k < 5; ++k) a.kstart[k] = kstart[k];
     a.fgroup = fgroup;
     a.D = D; a.H = H; a.W = W; a.nxb = (W + 31) / 32; a.nyb = (H + 31) / 32;
@@ -1178,19 +1240,105 @@ cudaError_t launch_sweep(const float *D, int32_t H, int32_t W, int32_t frames, c
     a.tma = (!no_tma && (W & 3) == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0 && make_maps(D, H, W, frames, tm))
                 ? 1 : 0;
     const size_t smem = kSweepWarpSmem * kSweepWarps;
-    cudaError_t e = cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kmain = sh ? k_sweep<true> : k_sweep<false>;
+    auto ksmall = sh ? k_sweep_small<true> : k_sweep_small<false>;
+    cudaError_t e = cudaFuncSetAttribute(kmain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(k_sweep, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kmain, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     const int64_t nw = (int64_t)nunits * frames;
-    k_sweep<<<(unsigned)((nw + kSweepWarps - 1) / kSweepWarps), 32 * kSweepWarps, smem, s>>>(a, tm);
+    kmain<<<(unsigned)((nw + kSweepWarps - 1) / kSweepWarps), 32 * kSweepWarps, smem, s>>>(a, tm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // units of frames with h < 17 (data dependent: known on the device only)
     const int32_t smin = std::max(1, smin_hint);
-    e = cudaFuncSetAttribute(k_sweep_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepWarpSmem);
+    e = cudaFuncSetAttribute(ksmall, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepWarpSmem);
     if (e != cudaSuccess) return e;
     // one resident wave of 1-warp CTAs (148 SMs x SWEEP_MINB)
-    k_sweep_small<<<(unsigned)std::min<int64_t>(nw, 148 * SWEEP_MINB), 32, kSweepWarpSmem, s>>>(a, tm, smin);
+    ksmall<<<(unsigned)std::min<int64_t>(nw, 148 * SWEEP_MINB), 32, kSweepWarpSmem, s>>>(a, tm, smin);
+    return cudaGetLastError();
+}
+
+// ================================================================ k_shear
+// Knight baselines ((2, +-1), (1, +-2)): their digital lines (S6, reading
+// Q8: l = y - floor(x by / bx), x-major; l = x - floor(y bx / by), y-major)
+// are not arithmetic progressions in memory.  k_shear copies D into a
+// sheared frame whose rows (x-major) or columns (y-major) ARE the family's
+// lines -- Ds[l'][x] = D[l' + lmin + f(x)][x] or Ds[y][l'] = D[y][l' + lmin +
+// f(y)], f(t) = floor(t num / den), NaN outside the image (a NaN sample
+// never pairs and is never a candidate: the dropped samples of reading Q10)
+// -- and writes the family's Eq. 1-2 candidate bits (PAPER.md:92-109,
+// computed on the image's own neighbours) in the k_words layout of sweep
+// kind 0 (rows) or 1 (columns) of that frame.  k_sweep then runs the family
+// as rows / columns and un-shears its mask stores (s_store_sh).
+struct ShearArgs {
+    const float *D;
+    int32_t H, W;              // image
+    int32_t Hs, Ws, nxb, nyb;  // sheared frame and its 32 x 32 blocks
+    int32_t xmajor, num, den, lmin, b0x, b0y;
+    float e2_thresh;
+    float *Ds;
+    uint32_t *words;           // [frame][nyb][nxb][12][32] (slots 0, 1 or 2, 3 used)
+};
+__global__ void __launch_bounds__(128) k_shear(ShearArgs a) {
+    __shared__ uint2 rw[4][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t kx = blockIdx.x * 4 + warp, m = blockIdx.y, f = blockIdx.z;
+    const bool wok = kx < a.nxb;
+    const float NaN = __int_as_float(0x7fc00000);
+    const float *Df = a.D + (int64_t)f * a.H * a.W;
+    float *Dsf = a.Ds + (int64_t)f * a.Hs * a.Ws;
+    const int32_t col = 32 * kx + lane;
+    for (int r = 0; r < 32; ++r) {
+        const int32_t row = 32 * m + r;
+        const bool ins = wok && col < a.Ws && row < a.Hs;
+        int32_t x, y;
+        if (a.xmajor) { x = col; y = row + a.lmin + s_fdiv(col * a.num, a.den); }
+        else { y = row; x = col + a.lmin + s_fdiv(row * a.num, a.den); }
+        const bool in = ins && (uint32_t)x < (uint32_t)a.W && (uint32_t)y < (uint32_t)a.H;
+        const float v = in ? __ldg(Df + (int64_t)y * a.W + x) : NaN;
+        if (ins) Dsf[(int64_t)row * a.Ws + col] = v;
+        const bool hr = in && x + 1 < a.W, hb = in && y + 1 < a.H;
+        const float right = hr ? __ldg(Df + (int64_t)y * a.W + x + 1) : 0.0f;
+        const float below = hb ? __ldg(Df + (int64_t)(y + 1) * a.W + x) : 0.0f;
+        // Eq. 1 (reading Q1) and the exact E^2 threshold (Q4), as k_words
+        const float ex = hr ? __fsub_rn(right, v) : 0.0f;
+        const float ey = hb ? __fsub_rn(below, v) : 0.0f;
+        const float e2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+        const bool edge = in && e2 > a.e2_thresh;
+        // Eq. 2 <=> b0 . (E_x, E_y) > 0, exact sign: components in {1, 2}
+        // make both fp32 products exact unless they overflow (then binary64)
+        const float px = __fmul_rn((float)a.b0x, ex), py = __fmul_rn((float)a.b0y, ey);
+        bool pos, neg;
+        if (isfinite(px) && isfinite(py)) {
+            const float dot = __fadd_rn(px, py);
+            pos = dot > 0.0f; neg = dot < 0.0f;
+        } else {
+            const double dot = __dadd_rn(__dmul_rn((double)a.b0x, (double)ex), __dmul_rn((double)a.b0y, (double)ey));
+            pos = dot > 0.0; neg = dot < 0.0;
+        }
+        const uint32_t bp = __ballot_sync(FULL, edge && pos), bn = __ballot_sync(FULL, edge && neg);
+        if (lane == 0) rw[warp][r] = make_uint2(bp, bn);
+    }
+    __syncwarp();
+    const uint2 q = rw[warp][lane];
+    if (!wok) return;
+    uint32_t *dst = a.words + (((int64_t)f * a.nyb + m) * a.nxb + kx) * kWordSlots * 32 + lane;
+    if (a.xmajor) {          // kind 0: lane = line (row of the block), bit = position (column)
+        dst[0] = q.x;
+        dst[32] = q.y;
+    } else {                 // kind 1: lane = line (column), bit = position (row)
+        dst[64] = s_transpose32(q.x, lane);
+        dst[96] = s_transpose32(q.y, lane);
+    }
+}
+
+cudaError_t launch_shear(const float *D, int32_t H, int32_t W, int32_t frames, const ShearDesc &sh, int32_t Hs,
+                         int32_t Ws, int32_t b0x, int32_t b0y, float e2_thresh, float *Ds, uint32_t *words,
+                         cudaStream_t s) {
+    ShearArgs a{D, H, W, Hs, Ws, (Ws + 31) / 32, (Hs + 31) / 32, sh.kind == 0 ? 1 : 0, sh.num, sh.den, sh.lmin,
+                b0x, b0y, e2_thresh, Ds, words};
+    dim3 grid((unsigned)((a.nxb + 3) / 4), (unsigned)a.nyb, (unsigned)frames);
+    k_shear<<<grid, 128, 0, s>>>(a);
     return cudaGetLastError();
 }
 

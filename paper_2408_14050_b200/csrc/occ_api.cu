@@ -48,6 +48,18 @@ struct occ_ctx {
     int32_t skstart[5] = {0, 0, 0, 0, 0}; // sunits of kind k at [skstart[k], skstart[k + 1])
     int32_t sfgroup = 1;                  // k_sweep work order: frames per group
     int32_t ssmin = 1;                    // smallest s of the k_sweep groups (k_sweep_small's frame filter)
+    // knight families swept through a sheared copy of D (k_shear + k_sweep)
+    struct ShearFam {
+        int32_t fam = 0, Hs = 0, Ws = 0;   // family, sheared frame
+        ShearDesc sd{};
+        std::vector<SweepUnit> units;
+        SweepUnit *d_units = nullptr;
+        int32_t kstart[5] = {0, 0, 0, 0, 0};
+        int32_t fgroup = 1, smin = 1;
+    };
+    std::vector<ShearFam> shear;
+    float *d_shD = nullptr;               // sheared D of one family, one chunk of frames
+    uint32_t *d_shW = nullptr;            // its candidate words
     std::vector<LineUnit> units;          // k_line work (eligible groups, OCC_SWEEP=0)
     std::vector<TileDesc> all_tiles;      // k_tile work for every group (OCC_PATH_TILED)
     LineUnit *d_units = nullptr;
@@ -200,9 +212,19 @@ struct ProfScope {
 // anti-diagonals, its views use the default near/far split (near backward
 // offsets {1, 2}, far >= 3, <= 1 near forward offset whose lower bound equals
 // the backward one), and the two views (if two) are +-b with equal s.
+bool views_line_ok(const occ_ctx *c, const GroupDesc &g);
 bool line_eligible(const occ_ctx *c, const GroupDesc &g) {
     const FamilyDesc &fd = c->fams[g.fam];
     if (fd.kind < 0 || fd.kind > 3 || g.nv < 1 || g.nv > 2) return false;
+    return views_line_ok(c, g);
+}
+// the knight families (2, +-1), (1, +-2) through k_shear: the same view conditions
+bool shear_eligible(const occ_ctx *c, const GroupDesc &g) {
+    const FamilyDesc &fd = c->fams[g.fam];
+    if (fd.kind < 4 || fd.kind > 7 || g.nv < 1 || g.nv > 2) return false;
+    return views_line_ok(c, g);
+}
+bool views_line_ok(const occ_ctx *c, const GroupDesc &g) {
     for (int32_t k = 0; k < g.nv; ++k) {
         const ViewDesc &v = c->views[g.view[k]];
         if (v.nback != 2 || v.jstar != 3 || v.nfwd > 1) return false;
@@ -318,9 +340,12 @@ void build_tiles(occ_ctx *c) {
     std::vector<char> eligible(c->groups.size(), 0);
     // k_sweep (default) or the round-1 k_line + k_cand path (OCC_SWEEP=0, kept for A/B runs)
     static const bool sweep = [] { const char *ev = getenv("OCC_SWEEP"); return !(ev && atoi(ev) == 0); }();
+    std::vector<char> sheared(c->groups.size(), 0);
+    static const bool shear_on = [] { const char *ev = getenv("OCC_SHEAR"); return !(ev && atoi(ev) == 0); }();
     for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi) {
         eligible[gi] = line_eligible(c, c->groups[gi]);
         if (eligible[gi] && !sweep) add_line_units(c, gi);
+        sheared[gi] = sweep && shear_on && shear_eligible(c, c->groups[gi]);
     }
     if (sweep) {
         // segment length: 256 positions, halved while one call of max_batch
@@ -359,6 +384,58 @@ void build_tiles(occ_ctx *c) {
         const int32_t by_l2 = std::max(1, (int32_t)(40.0e6 / fbytes));
         c->sfgroup = std::max(1, std::min(by_wave, by_l2));
         if (const char *ev = getenv("OCC_SWEEP_FGROUP")) c->sfgroup = std::max(1, atoi(ev));   // tuning knob
+        // knight families: one sheared frame per family; its lines become the
+        // rows (x-major) or columns (y-major) of that frame
+        for (int32_t fm = 0; fm < (int32_t)c->fams.size(); ++fm) {
+            std::vector<int32_t> gs;
+            for (int32_t gi = 0; gi < (int32_t)c->groups.size(); ++gi)
+                if (sheared[gi] && c->groups[gi].fam == fm) gs.push_back(gi);
+            if (gs.empty()) continue;
+            const FamilyDesc &fd = c->fams[fm];
+            occ_ctx::ShearFam sf;
+            sf.fam = fm;
+            ShearDesc &sd = sf.sd;
+            sd.kind = fd.xmajor ? 0 : 1;
+            sd.num = fd.num; sd.den = fd.den; sd.Ho = H; sd.Wo = W;
+            const int32_t PM = fd.xmajor ? W : H, QM = fd.xmajor ? H : W;
+            auto fdv = [&](int32_t t) { return floordiv(t * fd.num, fd.den); };
+            const int32_t f0 = fdv(0), f1 = fdv(PM - 1);
+            sd.lmin = -std::max(f0, f1);
+            const int32_t nl = QM - 1 - std::min(f0, f1) - sd.lmin + 1;     // lines
+            sf.Hs = fd.xmajor ? nl : H;
+            sf.Ws = fd.xmajor ? W : nl;
+            // units: 32-line blocks x seg positions over the block's in-image extent
+            for (int32_t gi : gs) {
+                for (int32_t l0 = 0; l0 < nl; l0 += 32) {
+                    int32_t lo = INT32_MAX, hi = INT32_MIN;
+                    for (int32_t l = l0; l < std::min(nl, l0 + 32); l += std::max(1, std::min(31, nl - 1 - l))) {
+                        const int32_t L = l + sd.lmin;
+                        for (int32_t t = 0; t < PM; ++t) {
+                            const int32_t q = L + fdv(t);
+                            if (q >= 0 && q < QM) { lo = std::min(lo, t); hi = std::max(hi, t + 1); }
+                        }
+                    }
+                    if (lo >= hi) continue;
+                    const int32_t a0 = lo & ~31, b0 = (hi + 31) & ~31;
+                    for (int32_t t0 = a0; t0 < b0; t0 += seg) {
+                        SweepUnit u{};
+                        u.group = gi; u.l0 = l0; u.t0 = t0; u.t1 = std::min(t0 + seg, b0);
+                        sf.units.push_back(u);
+                    }
+                }
+            }
+            std::stable_sort(sf.units.begin(), sf.units.end(),
+                             [](const SweepUnit &x, const SweepUnit &y) { return x.t1 - x.t0 > y.t1 - y.t0; });
+            const int32_t nu = (int32_t)sf.units.size();
+            sf.kstart[0] = 0;
+            for (int k = 1; k <= 4; ++k) sf.kstart[k] = nu;
+            const double sbytes = (double)sf.Hs * sf.Ws * 4.0 + 4.0 * (double)sweep_words_per_frame(sf.Hs, sf.Ws);
+            const int32_t sw = (int32_t)std::ceil(148.0 * 16 / std::max(1, nu));
+            sf.fgroup = std::max(1, std::min(sw, std::max(1, (int32_t)(40.0e6 / sbytes))));
+            sf.smin = INT32_MAX;
+            for (int32_t gi : gs) sf.smin = std::min(sf.smin, c->views[c->groups[gi].view[0]].s);
+            c->shear.push_back(std::move(sf));
+        }
     }
     // segment length: 256 positions, shorter when a call of max_batch frames
     // would not fill the GPU (a unit is one warp's serial work, ~0.1 ms at
@@ -438,7 +515,7 @@ void build_tiles(occ_ctx *c) {
                 TileDesc t{};
                 t.group = gi; t.l0 = l0; t.p0 = p0; t.p1 = std::min(p0 + kTilePositions, phi + 1);
                 c->all_tiles.push_back(t);
-                if (!eligible[gi]) c->tiles.push_back(t);
+                if (!eligible[gi] && !sheared[gi]) c->tiles.push_back(t);
             }
         }
     }
@@ -483,6 +560,23 @@ const char *occ_strerror(int code) {
     }
 }
 
+// device buffers of the sheared (knight) families: one sheared frame and its
+// words per chunk frame (sized for the largest family), unit lists
+bool alloc_shear(occ_ctx *c) {
+    if (c->shear.empty()) return true;
+    size_t dmax = 0, wmax = 0;
+    for (auto &sf : c->shear) {
+        dmax = std::max(dmax, (size_t)sf.Hs * sf.Ws);
+        wmax = std::max(wmax, (size_t)sweep_words_per_frame(sf.Hs, sf.Ws));
+        if (cudaMalloc(&sf.d_units, sizeof(SweepUnit) * std::max<size_t>(1, sf.units.size())) != cudaSuccess ||
+            (sf.units.size() && cudaMemcpy(sf.d_units, sf.units.data(), sizeof(SweepUnit) * sf.units.size(),
+                                           cudaMemcpyHostToDevice) != cudaSuccess))
+            return false;
+    }
+    return cudaMalloc(&c->d_shD, sizeof(float) * (size_t)c->chunk * dmax) == cudaSuccess &&
+           cudaMalloc(&c->d_shW, sizeof(uint32_t) * (size_t)c->chunk * wmax) == cudaSuccess;
+}
+
 // Device side of a context whose views (and families) are set up: work
 // lists, chunking, device copies, offset tables.  Frees c on failure.
 int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_batch, occ_ctx **out) {
@@ -493,8 +587,12 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         // sets the launch count (L2 locality is per frame); measured at C5:
         // 256 MiB (25 frames) 53.1 ms/step, 1 GiB 51.5, 2 GiB (207 frames)
         // 51.3, 4 GiB (one launch) 52.4
+        double shear_per = 0.0;
+        for (const auto &sf : c->shear)
+            shear_per = std::max(shear_per, (double)sf.Hs * sf.Ws * 4.0 + 4.0 * (double)sweep_words_per_frame(sf.Hs, sf.Ws));
         const double per = (double)H * W * (4.0 + c->code_bytes) +
-                           (c->sunits.empty() ? 0.0 : 4.0 * (double)sweep_words_per_frame(H, W));
+                           (c->sunits.empty() && c->shear.empty() ? 0.0 : 4.0 * (double)sweep_words_per_frame(H, W)) +
+                           shear_per;
         const char *ev = getenv("OCC_CHUNK_MIB");          // tuning knob (default 2 GiB)
         const double budget = (ev ? std::max(1, atoi(ev)) : 2048) * 1048576.0;
         c->chunk = (int32_t)std::max(1.0, std::min((double)kMaxChunkFrames, std::floor(budget / per)));
@@ -511,12 +609,13 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         cudaMalloc(&c->d_units, sizeof(LineUnit) * std::max<size_t>(1, c->units.size())) != cudaSuccess ||
         cudaMalloc(&c->d_stats, sizeof(FrameStats) * (size_t)max_batch) != cudaSuccess ||
         cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
-        ((!c->units.empty() || !c->sunits.empty()) &&
+        ((!c->units.empty() || !c->sunits.empty() || !c->shear.empty()) &&
          (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = gq_capacity(c->chunk, H, W, n_views))) != cudaSuccess ||
           cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess)) ||
-        (!c->sunits.empty() &&
-         (cudaMalloc(&c->d_sunits, sizeof(SweepUnit) * c->sunits.size()) != cudaSuccess ||
-          cudaMalloc(&c->d_words, sizeof(uint32_t) * (size_t)c->chunk * (size_t)sweep_words_per_frame(H, W)) != cudaSuccess))) {
+        ((!c->sunits.empty() || !c->shear.empty()) &&
+         (cudaMalloc(&c->d_sunits, sizeof(SweepUnit) * std::max<size_t>(1, c->sunits.size())) != cudaSuccess ||
+          cudaMalloc(&c->d_words, sizeof(uint32_t) * (size_t)c->chunk * (size_t)sweep_words_per_frame(H, W)) != cudaSuccess)) ||
+        !alloc_shear(c)) {
         cudaGetLastError();
         occ_destroy(c);
         return OCC_ERR_OOM;
@@ -784,7 +883,7 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
     uint8_t *Mc = M + (int64_t)c0 * c->V * c->mf.vbytes;
     const bool tiled_only = c->path == OCC_PATH_TILED;
     const bool nwin = c->neighbors > 0 || c->angles;
-    const bool sweep = !tiled_only && !nwin && !c->sunits.empty();
+    const bool sweep = !tiled_only && !nwin && (!c->sunits.empty() || !c->shear.empty());
     const TileDesc *tl = tiled_only ? c->d_all_tiles : c->d_tiles;
     const int32_t nt = (int32_t)(tiled_only ? c->all_tiles.size() : c->tiles.size());
     {
@@ -821,15 +920,37 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         // poison the queue: a slot k_hard reads that this chunk did not write fails its checks
         CK(cudaMemsetAsync(c->d_gq, 0xFF, sizeof(HardEntry) * (size_t)c->gq_cap, s));
 #endif
-        CK(launch_sweep(Dc, c->H, c->W, n, c->d_sunits, (int32_t)c->sunits.size(), c->d_groups, c->d_views, c->V,
-                        c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_words, c->d_gq, c->d_gq_count,
-                        c->gq_cap, c->skstart, c->sfgroup, c->d_dbg, c->ssmin, s));
-        pl.end();
-        ProfScope ph(c, OCC_KERNEL_HARD, s);
-        CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
-                       c->gq_cap, c->d_stats + c0, c->nsm, s));
-        launches += 3;       // k_sweep, k_sweep_small, k_hard
-        ph.end();
+        if (!c->sunits.empty()) {
+            CK(launch_sweep(Dc, c->H, c->W, n, c->d_sunits, (int32_t)c->sunits.size(), c->d_groups, c->d_views, c->V,
+                            c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_words, c->d_gq, c->d_gq_count,
+                            c->gq_cap, c->skstart, c->sfgroup, c->d_dbg, c->ssmin, nullptr, s));
+            pl.end();
+            ProfScope ph(c, OCC_KERNEL_HARD, s);
+            CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
+                           c->gq_cap, c->d_stats + c0, c->nsm, s));
+            launches += 3;       // k_sweep, k_sweep_small, k_hard
+            ph.end();
+        } else {
+            pl.end();
+        }
+        // knight families: sheared copy + words (k_shear), the sweep over its
+        // rows / columns, the far-partner searches of its queue
+        for (const auto &sf : c->shear) {
+            ProfScope ps2(c, OCC_KERNEL_LINE, s);
+            const FamilyDesc &fd = c->fams[(size_t)sf.fam];
+            CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
+            CK(launch_shear(Dc, c->H, c->W, n, sf.sd, sf.Hs, sf.Ws, fd.b0x, fd.b0y, c->params.e2_thresh, c->d_shD,
+                            c->d_shW, s));
+            CK(launch_sweep(c->d_shD, sf.Hs, sf.Ws, n, sf.d_units, (int32_t)sf.units.size(), c->d_groups, c->d_views,
+                            c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_shW, c->d_gq,
+                            c->d_gq_count, c->gq_cap, sf.kstart, sf.fgroup, c->d_dbg, sf.smin, &sf.sd, s));
+            ps2.end();
+            ProfScope ph2(c, OCC_KERNEL_HARD, s);
+            CK(launch_hard(c->d_shD, Mc, c->mf, sf.Ws, (int64_t)sf.Hs * sf.Ws, n, c->V, c->d_views, c->params, c->d_gq,
+                           c->d_gq_count, c->gq_cap, c->d_stats + c0, c->nsm, s, &sf.sd));
+            ph2.end();
+            launches += 4;       // k_shear, k_sweep, k_sweep_small, k_hard
+        }
     } else if (!tiled_only && !c->units.empty()) {
         ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
@@ -1119,6 +1240,9 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_units);
     cudaFree(c->d_sunits);
     cudaFree(c->d_words);
+    for (auto &sf : c->shear) cudaFree(sf.d_units);
+    cudaFree(c->d_shD);
+    cudaFree(c->d_shW);
     cudaFree(c->d_dbg);
     cudaFree(c->d_gq);
     cudaFree(c->d_gq_count);

@@ -163,6 +163,12 @@ struct LineUnit {
 // pix + j * sg(v) * stride(kind(v)), j = 3 .. jm (dcov clipped to the image).
 // meta = jm | f << 17 | v << 25 (jm <= 2 * (65536 / 2) < 2^17, f < 256,
 // v < 64).
+// A knight family served by k_sweep through a sheared copy of D (k_shear):
+// kind = the sweep kind its lines become (0 rows: x-major, 1 columns:
+// y-major); image line l = sheared line + lmin; f(t) = floor(t num / den).
+struct ShearDesc {
+    int32_t kind, num, den, lmin, Ho, Wo;
+};
 struct HardEntry {
     int32_t pix;
     uint32_t meta;
@@ -189,7 +195,8 @@ cudaError_t launch_line(const float *D, int32_t H, int32_t W, int32_t batch, con
 cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32_t W, int64_t HW, int32_t frames,
                         int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
-                        const FrameStats *st, int32_t nsm, cudaStream_t s);
+                        const FrameStats *st, int32_t nsm, cudaStream_t s,
+                        const ShearDesc *sh = nullptr);
 // Pixel-wise median fusion (k_fuse.cu): stack [K][n] -> out [n].
 constexpr int kFuseMaxK = 64;
 cudaError_t launch_fuse_median(const float *stack, int32_t K, int64_t n, float *out, int nsm, cudaStream_t s);
@@ -236,6 +243,9 @@ cudaError_t launch_sweep(const float *D, int32_t H, int32_t W, int32_t frames, c
                          const FamilyDesc *fams, const FrameStats *st, const Params &p, uint8_t *masks,
                          const MaskFmt &mf, const uint32_t *words, HardEntry *gq, uint32_t *gq_count,
                          int32_t gq_cap, const int32_t *kstart, int32_t fgroup, unsigned long long *dbg,
-                         int32_t smin, cudaStream_t s);
+                         int32_t smin, const ShearDesc *sh, cudaStream_t s);
+cudaError_t launch_shear(const float *D, int32_t H, int32_t W, int32_t frames, const ShearDesc &sh, int32_t Hs,
+                         int32_t Ws, int32_t b0x, int32_t b0y, float e2_thresh, float *Ds, uint32_t *words,
+                         cudaStream_t s);
 
 }  // namespace occ
