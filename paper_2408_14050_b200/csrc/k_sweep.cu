@@ -538,34 +538,56 @@ __device__ __forceinline__ int32_t s_fdiv(int32_t a, int32_t b) {      // floor(
 }
 // masks of a sheared family (knight baselines): bit r of the lane's word is
 // line l0 + lane at tau = 32k + r; un-shear to the image pixel and write it
-// (uint8: every in-image byte of the unit's lines; packed: set bits)
+// (uint8: every in-image byte of the unit's lines once; packed: set bits).
+// Every warp store covers consecutive x of one image row:
+//   y-major (kind 1): at tau = row y the 32 lines are 32 consecutive x;
+//   x-major (kind 0): lane c writes column 32k + c of each row the block's
+//   lines cross, taking the bit from the line that owns that pixel (shuffle).
 __device__ __noinline__ void s_store_sh(const SU &u, const SweepArgs &a, uint8_t *Mv, uint32_t word, int32_t k) {
     const int lane = u.lane;
     const int32_t Ho = a.Ho, Wo = a.Wo;
     const bool packed = a.mf.packed != 0;
     uint32_t *P = reinterpret_cast<uint32_t *>(Mv);
-    if (u.kind == 0) {                    // x-major: pixel (tau, l + f(tau))
-        if (u.l0 + lane >= u.H) return;
-        const int32_t L = u.l0 + lane + a.sh_lmin;
+    if (u.kind == 1) {                    // pixel (l + f(tau), tau)
+        const bool lok = u.l0 + lane < u.W;
+        const int32_t xl = u.l0 + lane + a.sh_lmin;
         for (int r = 0; r < 32; ++r) {
-            const int32_t x = 32 * k + r;
-            const int32_t y = L + s_fdiv(x * a.sh_num, a.sh_den);
-            if (x < 0 || x >= Wo || (uint32_t)y >= (uint32_t)Ho) continue;
+            const int32_t y = 32 * k + r;
+            if (y < 0 || y >= Ho) continue;                       // warp-uniform
+            const int32_t x = xl + s_fdiv(y * a.sh_num, a.sh_den);
+            const bool ok = lok && (uint32_t)x < (uint32_t)Wo;
             const uint32_t b = (word >> r) & 1u;
-            if (!packed) __stcs(Mv + (int64_t)y * Wo + x, (uint8_t)b);
-            else if (b) atomicOr(P + (int64_t)y * a.mf.Wb + (x >> 5), 1u << (x & 31));
+            if (!packed) {
+                if (ok) __stcs(Mv + (int64_t)y * Wo + x, (uint8_t)b);
+            } else {
+                const uint32_t run = __ballot_sync(FULL, ok && b);    // bit j <-> x = x(lane 0) + j
+                const int32_t x0 = __shfl_sync(FULL, x, 0);               // lanes are consecutive x
+                if (lane == 0 && run) {
+                    const int32_t xs = x0, w0 = s_fdiv(xs, 32), sh = xs - 32 * w0;
+                    const uint32_t lo = run << sh, hi = sh ? (run >> (32 - sh)) : 0u;
+                    if (lo && w0 >= 0 && w0 < a.mf.Wb) atomicOr(P + (int64_t)y * a.mf.Wb + w0, lo);
+                    if (hi && w0 + 1 >= 0 && w0 + 1 < a.mf.Wb) atomicOr(P + (int64_t)y * a.mf.Wb + w0 + 1, hi);
+                }
+            }
         }
-    } else {                              // y-major: lane r <- row tau = 32k + r, bit j = line l0 + j
-        const uint32_t t = s_transpose32(word, lane);
-        const int32_t y = 32 * k + lane;
-        if (y < 0 || y >= Ho) return;
-        const int32_t x0 = u.l0 + a.sh_lmin + s_fdiv(y * a.sh_num, a.sh_den);
-        for (int j = 0; j < 32; ++j) {
-            const int32_t x = x0 + j;
-            if (u.l0 + j >= u.W || (uint32_t)x >= (uint32_t)Wo) continue;
-            const uint32_t b = (t >> j) & 1u;
-            if (!packed) __stcs(Mv + (int64_t)y * Wo + x, (uint8_t)b);
-            else if (b) atomicOr(P + (int64_t)y * a.mf.Wb + (x >> 5), 1u << (x & 31));
+        return;
+    }
+    // x-major: pixel (tau, l + f(tau)); lane c writes column x = 32k + c
+    const int32_t x = 32 * k + lane;
+    const int32_t fc = s_fdiv(x * a.sh_num, a.sh_den);
+    const int32_t fa = s_fdiv(32 * k * a.sh_num, a.sh_den), fb = s_fdiv((32 * k + 31) * a.sh_num, a.sh_den);
+    const int32_t Lb = u.l0 + a.sh_lmin;  // image line of lane 0
+    const bool xok = x < Wo;
+    for (int32_t y = max(0, Lb + min(fa, fb)); y <= min(Ho - 1, Lb + 31 + max(fa, fb)); ++y) {
+        const int32_t o = y - fc - Lb;                            // the lane whose line holds (x, y)
+        const uint32_t w = __shfl_sync(FULL, word, o & 31);
+        const bool ok = xok && (uint32_t)o < 32u && u.l0 + o < u.H;
+        const uint32_t b = (w >> lane) & 1u;
+        if (!packed) {
+            if (ok) __stcs(Mv + (int64_t)y * Wo + x, (uint8_t)b);
+        } else {
+            const uint32_t bits = __ballot_sync(FULL, ok && b);
+            if (lane == 0 && bits) atomicOr(P + (int64_t)y * a.mf.Wb + k, bits);
         }
     }
 }

@@ -56,10 +56,16 @@ struct occ_ctx {
         SweepUnit *d_units = nullptr;
         int32_t kstart[5] = {0, 0, 0, 0, 0};
         int32_t fgroup = 1, smin = 1;
+        float *d_D = nullptr;             // its sheared D, one chunk of frames
+        uint32_t *d_W = nullptr;          // its candidate words
+        int64_t q0 = 0;                   // its region of the far-partner queue [q0, q0 + qcap)
+        int32_t qcap = 0;
+        cudaStream_t st = nullptr;        // families run concurrently, forked from the caller's stream
+        cudaEvent_t done = nullptr;
     };
     std::vector<ShearFam> shear;
-    float *d_shD = nullptr;               // sheared D of one family, one chunk of frames
-    uint32_t *d_shW = nullptr;            // its candidate words
+    cudaEvent_t sh_fork = nullptr;
+    int32_t main_qcap = 0;                // queue region of the main sweep [0, main_qcap)
     std::vector<LineUnit> units;          // k_line work (eligible groups, OCC_SWEEP=0)
     std::vector<TileDesc> all_tiles;      // k_tile work for every group (OCC_PATH_TILED)
     LineUnit *d_units = nullptr;
@@ -202,7 +208,7 @@ struct ProfScope {
         if (!on) return;
         auto &v = c->ev[kind];
         size_t &u = c->ev_used[kind];
-        cudaEventRecord(v[u + 1], s);
+        if (v.size() >= u + 2) cudaEventRecord(v[u + 1], s);     // (scopes of one kind never nest)
         u += 2;
         on = false;
     }
@@ -563,18 +569,43 @@ const char *occ_strerror(int code) {
 // device buffers of the sheared (knight) families: one sheared frame and its
 // words per chunk frame (sized for the largest family), unit lists
 bool alloc_shear(occ_ctx *c) {
+    c->main_qcap = c->gq_cap;
     if (c->shear.empty()) return true;
-    size_t dmax = 0, wmax = 0;
+    // queue regions in proportion to the views each sweep serves
+    int32_t vmain = 0;
+    {
+        std::vector<char> inmain(c->groups.size(), 0);
+        for (const SweepUnit &u : c->sunits) inmain[(size_t)u.group] = 1;
+        for (size_t g = 0; g < c->groups.size(); ++g) vmain += inmain[g] ? c->groups[g].nv : 0;
+    }
+    int32_t vtot = vmain;
+    std::vector<int32_t> vsh;
     for (auto &sf : c->shear) {
-        dmax = std::max(dmax, (size_t)sf.Hs * sf.Ws);
-        wmax = std::max(wmax, (size_t)sweep_words_per_frame(sf.Hs, sf.Ws));
+        std::vector<char> in(c->groups.size(), 0);
+        for (const SweepUnit &u : sf.units) in[(size_t)u.group] = 1;
+        int32_t v = 0;
+        for (size_t g = 0; g < c->groups.size(); ++g) v += in[g] ? c->groups[g].nv : 0;
+        vsh.push_back(std::max(1, v));
+        vtot += std::max(1, v);
+    }
+    c->main_qcap = (int32_t)((double)c->gq_cap * vmain / vtot);
+    int64_t q = c->main_qcap;
+    for (size_t k = 0; k < c->shear.size(); ++k) {
+        auto &sf = c->shear[k];
+        sf.q0 = q;
+        sf.qcap = (int32_t)((double)c->gq_cap * vsh[k] / vtot);
+        q += sf.qcap;
         if (cudaMalloc(&sf.d_units, sizeof(SweepUnit) * std::max<size_t>(1, sf.units.size())) != cudaSuccess ||
             (sf.units.size() && cudaMemcpy(sf.d_units, sf.units.data(), sizeof(SweepUnit) * sf.units.size(),
-                                           cudaMemcpyHostToDevice) != cudaSuccess))
+                                           cudaMemcpyHostToDevice) != cudaSuccess) ||
+            cudaMalloc(&sf.d_D, sizeof(float) * (size_t)c->chunk * sf.Hs * sf.Ws) != cudaSuccess ||
+            cudaMalloc(&sf.d_W, sizeof(uint32_t) * (size_t)c->chunk * (size_t)sweep_words_per_frame(sf.Hs, sf.Ws)) !=
+                cudaSuccess ||
+            cudaStreamCreateWithFlags(&sf.st, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sf.done, cudaEventDisableTiming) != cudaSuccess)
             return false;
     }
-    return cudaMalloc(&c->d_shD, sizeof(float) * (size_t)c->chunk * dmax) == cudaSuccess &&
-           cudaMalloc(&c->d_shW, sizeof(uint32_t) * (size_t)c->chunk * wmax) == cudaSuccess;
+    return cudaEventCreateWithFlags(&c->sh_fork, cudaEventDisableTiming) == cudaSuccess;
 }
 
 // Device side of a context whose views (and families) are set up: work
@@ -589,7 +620,7 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         // 51.3, 4 GiB (one launch) 52.4
         double shear_per = 0.0;
         for (const auto &sf : c->shear)
-            shear_per = std::max(shear_per, (double)sf.Hs * sf.Ws * 4.0 + 4.0 * (double)sweep_words_per_frame(sf.Hs, sf.Ws));
+            shear_per += (double)sf.Hs * sf.Ws * 4.0 + 4.0 * (double)sweep_words_per_frame(sf.Hs, sf.Ws);
         const double per = (double)H * W * (4.0 + c->code_bytes) +
                            (c->sunits.empty() && c->shear.empty() ? 0.0 : 4.0 * (double)sweep_words_per_frame(H, W)) +
                            shear_per;
@@ -611,7 +642,7 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
         ((!c->units.empty() || !c->sunits.empty() || !c->shear.empty()) &&
          (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = gq_capacity(c->chunk, H, W, n_views))) != cudaSuccess ||
-          cudaMalloc(&c->d_gq_count, sizeof(uint32_t)) != cudaSuccess)) ||
+          cudaMalloc(&c->d_gq_count, sizeof(uint32_t) * (1 + kMaxFamilies)) != cudaSuccess)) ||
         ((!c->sunits.empty() || !c->shear.empty()) &&
          (cudaMalloc(&c->d_sunits, sizeof(SweepUnit) * std::max<size_t>(1, c->sunits.size())) != cudaSuccess ||
           cudaMalloc(&c->d_words, sizeof(uint32_t) * (size_t)c->chunk * (size_t)sweep_words_per_frame(H, W)) != cudaSuccess)) ||
@@ -914,43 +945,52 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         return OCC_OK;
     }
     if (sweep) {
-        ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
 #ifdef OCC_CHECKS
         // poison the queue: a slot k_hard reads that this chunk did not write fails its checks
         CK(cudaMemsetAsync(c->d_gq, 0xFF, sizeof(HardEntry) * (size_t)c->gq_cap, s));
 #endif
+        // knight families: sheared copy + words (k_shear), the sweep over its
+        // rows / columns, the far-partner searches of its queue region; each
+        // family on its own stream (one family is about one wave of units:
+        // run alone, its tail would idle the GPU), joined back into s
+        if (!c->shear.empty()) CK(cudaEventRecord(c->sh_fork, s));
+        for (size_t q = 0; q < c->shear.size(); ++q) {
+            const auto &sf = c->shear[q];
+            cudaStream_t ss = sf.st;
+            CK(cudaStreamWaitEvent(ss, c->sh_fork, 0));
+            ProfScope ps2(c, OCC_KERNEL_LINE, ss);
+            const FamilyDesc &fd = c->fams[(size_t)sf.fam];
+            uint32_t *cnt = c->d_gq_count + 1 + q;
+            HardEntry *gq = c->d_gq + sf.q0;
+            CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), ss));
+            CK(launch_shear(Dc, c->H, c->W, n, sf.sd, sf.Hs, sf.Ws, fd.b0x, fd.b0y, c->params.e2_thresh, sf.d_D,
+                            sf.d_W, ss));
+            CK(launch_sweep(sf.d_D, sf.Hs, sf.Ws, n, sf.d_units, (int32_t)sf.units.size(), c->d_groups, c->d_views,
+                            c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, sf.d_W, gq, cnt, sf.qcap,
+                            sf.kstart, sf.fgroup, c->d_dbg, sf.smin, &sf.sd, ss));
+            ps2.end();
+            ProfScope ph2(c, OCC_KERNEL_HARD, ss);
+            CK(launch_hard(sf.d_D, Mc, c->mf, sf.Ws, (int64_t)sf.Hs * sf.Ws, n, c->V, c->d_views, c->params, gq, cnt,
+                           sf.qcap, c->d_stats + c0, c->nsm, ss, &sf.sd));
+            ph2.end();
+            CK(cudaEventRecord(sf.done, ss));
+            launches += 4;       // k_shear, k_sweep, k_sweep_small, k_hard
+        }
         if (!c->sunits.empty()) {
+            // (profile scopes of one kind must not nest: the knight scopes above are closed)
+            ProfScope pl(c, OCC_KERNEL_LINE, s);
             CK(launch_sweep(Dc, c->H, c->W, n, c->d_sunits, (int32_t)c->sunits.size(), c->d_groups, c->d_views, c->V,
                             c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_words, c->d_gq, c->d_gq_count,
-                            c->gq_cap, c->skstart, c->sfgroup, c->d_dbg, c->ssmin, nullptr, s));
+                            c->main_qcap, c->skstart, c->sfgroup, c->d_dbg, c->ssmin, nullptr, s));
             pl.end();
             ProfScope ph(c, OCC_KERNEL_HARD, s);
             CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
-                           c->gq_cap, c->d_stats + c0, c->nsm, s));
+                           c->main_qcap, c->d_stats + c0, c->nsm, s));
             launches += 3;       // k_sweep, k_sweep_small, k_hard
             ph.end();
-        } else {
-            pl.end();
         }
-        // knight families: sheared copy + words (k_shear), the sweep over its
-        // rows / columns, the far-partner searches of its queue
-        for (const auto &sf : c->shear) {
-            ProfScope ps2(c, OCC_KERNEL_LINE, s);
-            const FamilyDesc &fd = c->fams[(size_t)sf.fam];
-            CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
-            CK(launch_shear(Dc, c->H, c->W, n, sf.sd, sf.Hs, sf.Ws, fd.b0x, fd.b0y, c->params.e2_thresh, c->d_shD,
-                            c->d_shW, s));
-            CK(launch_sweep(c->d_shD, sf.Hs, sf.Ws, n, sf.d_units, (int32_t)sf.units.size(), c->d_groups, c->d_views,
-                            c->V, c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_shW, c->d_gq,
-                            c->d_gq_count, c->gq_cap, sf.kstart, sf.fgroup, c->d_dbg, sf.smin, &sf.sd, s));
-            ps2.end();
-            ProfScope ph2(c, OCC_KERNEL_HARD, s);
-            CK(launch_hard(c->d_shD, Mc, c->mf, sf.Ws, (int64_t)sf.Hs * sf.Ws, n, c->V, c->d_views, c->params, c->d_gq,
-                           c->d_gq_count, c->gq_cap, c->d_stats + c0, c->nsm, s, &sf.sd));
-            ph2.end();
-            launches += 4;       // k_shear, k_sweep, k_sweep_small, k_hard
-        }
+        for (const auto &sf : c->shear) CK(cudaStreamWaitEvent(s, sf.done, 0));
     } else if (!tiled_only && !c->units.empty()) {
         ProfScope pl(c, OCC_KERNEL_LINE, s);
         CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
@@ -1240,9 +1280,14 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_units);
     cudaFree(c->d_sunits);
     cudaFree(c->d_words);
-    for (auto &sf : c->shear) cudaFree(sf.d_units);
-    cudaFree(c->d_shD);
-    cudaFree(c->d_shW);
+    for (auto &sf : c->shear) {
+        cudaFree(sf.d_units);
+        cudaFree(sf.d_D);
+        cudaFree(sf.d_W);
+        if (sf.st) cudaStreamDestroy(sf.st);
+        if (sf.done) cudaEventDestroy(sf.done);
+    }
+    if (c->sh_fork) cudaEventDestroy(c->sh_fork);
     cudaFree(c->d_dbg);
     cudaFree(c->d_gq);
     cudaFree(c->d_gq_count);
