@@ -531,7 +531,9 @@ def c4_leg(peak, frames=2):
     pv = B * h * w * len(views)
     return {"frames": B, "views": len(views), "ms_per_call": ms, "value": pv / (ms / 1e3) / 1e6, "unit": "MPV/s",
             "hbm_frac": B * h * w * (4 + len(views)) / (ms / 1e3) / 1e9 / peak,
-            "kernels_ms": {k: v[0] / reps for k, v in kt.items() if v[1]}}
+            "kernels_ms": {k: v[0] / reps for k, v in kt.items() if v[1]},
+            "note": ("the knight families (2,+-1), (1,+-2) run through k_shear + k_sweep on concurrent "
+                     "streams; kernels_ms sums each kind's launch intervals, which overlap")}
 
 
 def main():

@@ -1153,7 +1153,6 @@ __global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
 // SHEAR: the entries of a knight family swept through its sheared copy
 // (k_shear): D, W, HW are the sheared frame's, the line step is 1 (rows) or
 // W (columns), and the mask pixel is un-sheared (ShearDesc, occ_internal.h)
-__device__ __forceinline__ int32_t h_fdiv(int32_t a, int32_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 template <bool SHEAR>
 __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict__ D, uint8_t *__restrict__ masks,
                                               MaskFmt mf, int32_t W, int64_t HW, int32_t frames, int32_t nviews,
@@ -1231,8 +1230,8 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
             uint8_t *Mv = masks + ((int64_t)f * nviews + v) * mf.vbytes;
             if constexpr (SHEAR) {
                 const int32_t q = he.pix / W, r = he.pix % W;
-                if (sh.kind == 0) mask_put(Mv, mf, sh.Wo, r, q + sh.lmin + h_fdiv(r * sh.num, sh.den), true);
-                else mask_put(Mv, mf, sh.Wo, r + sh.lmin + h_fdiv(q * sh.num, sh.den), q, true);
+                if (sh.kind == 0) mask_put(Mv, mf, sh.Wo, r, q + sh.lmin + ((r * sh.num) >> 1), true);
+                else mask_put(Mv, mf, sh.Wo, r + sh.lmin + ((q * sh.num) >> 1), q, true);
             } else {
                 mask_put(Mv, mf, W, he.pix % W, he.pix / W, true);
             }

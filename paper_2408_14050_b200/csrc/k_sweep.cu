@@ -533,9 +533,7 @@ __device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf
     }
 }
 
-__device__ __forceinline__ int32_t s_fdiv(int32_t a, int32_t b) {      // floor(a / b), b > 0
-    return a >= 0 ? a / b : -((-a + b - 1) / b);
-}
+// (the knight families have den = 2: floor(t num / 2) is an arithmetic shift)
 // masks of a sheared family (knight baselines): bit r of the lane's word is
 // line l0 + lane at tau = 32k + r; un-shear to the image pixel and write it
 // (uint8: every in-image byte of the unit's lines once; packed: set bits).
@@ -554,7 +552,7 @@ __device__ __noinline__ void s_store_sh(const SU &u, const SweepArgs &a, uint8_t
         for (int r = 0; r < 32; ++r) {
             const int32_t y = 32 * k + r;
             if (y < 0 || y >= Ho) continue;                       // warp-uniform
-            const int32_t x = xl + s_fdiv(y * a.sh_num, a.sh_den);
+            const int32_t x = xl + ((y * a.sh_num) >> 1);
             const bool ok = lok && (uint32_t)x < (uint32_t)Wo;
             const uint32_t b = (word >> r) & 1u;
             if (!packed) {
@@ -563,7 +561,7 @@ __device__ __noinline__ void s_store_sh(const SU &u, const SweepArgs &a, uint8_t
                 const uint32_t run = __ballot_sync(FULL, ok && b);    // bit j <-> x = x(lane 0) + j
                 const int32_t x0 = __shfl_sync(FULL, x, 0);               // lanes are consecutive x
                 if (lane == 0 && run) {
-                    const int32_t xs = x0, w0 = s_fdiv(xs, 32), sh = xs - 32 * w0;
+                    const int32_t xs = x0, w0 = xs >> 5, sh = xs - 32 * w0;
                     const uint32_t lo = run << sh, hi = sh ? (run >> (32 - sh)) : 0u;
                     if (lo && w0 >= 0 && w0 < a.mf.Wb) atomicOr(P + (int64_t)y * a.mf.Wb + w0, lo);
                     if (hi && w0 + 1 >= 0 && w0 + 1 < a.mf.Wb) atomicOr(P + (int64_t)y * a.mf.Wb + w0 + 1, hi);
@@ -574,8 +572,8 @@ __device__ __noinline__ void s_store_sh(const SU &u, const SweepArgs &a, uint8_t
     }
     // x-major: pixel (tau, l + f(tau)); lane c writes column x = 32k + c
     const int32_t x = 32 * k + lane;
-    const int32_t fc = s_fdiv(x * a.sh_num, a.sh_den);
-    const int32_t fa = s_fdiv(32 * k * a.sh_num, a.sh_den), fb = s_fdiv((32 * k + 31) * a.sh_num, a.sh_den);
+    const int32_t fc = (x * a.sh_num) >> 1;
+    const int32_t fa = (32 * k * a.sh_num) >> 1, fb = ((32 * k + 31) * a.sh_num) >> 1;
     const int32_t Lb = u.l0 + a.sh_lmin;  // image line of lane 0
     const bool xok = x < Wo;
     for (int32_t y = max(0, Lb + min(fa, fb)); y <= min(Ho - 1, Lb + 31 + max(fa, fb)); ++y) {
@@ -1314,8 +1312,8 @@ __global__ void __launch_bounds__(128) k_shear(ShearArgs a) {
         const int32_t row = 32 * m + r;
         const bool ins = wok && col < a.Ws && row < a.Hs;
         int32_t x, y;
-        if (a.xmajor) { x = col; y = row + a.lmin + s_fdiv(col * a.num, a.den); }
-        else { y = row; x = col + a.lmin + s_fdiv(row * a.num, a.den); }
+        if (a.xmajor) { x = col; y = row + a.lmin + ((col * a.num) >> 1); }
+        else { y = row; x = col + a.lmin + ((row * a.num) >> 1); }
         const bool in = ins && (uint32_t)x < (uint32_t)a.W && (uint32_t)y < (uint32_t)a.H;
         const float v = in ? __ldg(Df + (int64_t)y * a.W + x) : NaN;
         if (ins) Dsf[(int64_t)row * a.Ws + col] = v;

@@ -228,6 +228,7 @@ bool line_eligible(const occ_ctx *c, const GroupDesc &g) {
 bool shear_eligible(const occ_ctx *c, const GroupDesc &g) {
     const FamilyDesc &fd = c->fams[g.fam];
     if (fd.kind < 4 || fd.kind > 7 || g.nv < 1 || g.nv > 2) return false;
+    if (fd.den != 2) return false;        // (the sheared kernels shift by 1 for floor(t num / 2))
     return views_line_ok(c, g);
 }
 bool views_line_ok(const occ_ctx *c, const GroupDesc &g) {
