@@ -526,8 +526,8 @@ __device__ __noinline__ void flush_queue(const int DIR, const Ctx &c, const int3
             const int32_t src = w & 31, jm = (w >> 5) & 0x1FFFF;
             HardEntry he;
             he.pix = (int32_t)(line_base(c.kind, c.l0, src, c.W) + (int64_t)tau * c.S);
-            he.meta = (uint32_t)jm | ((uint32_t)c.f << 17) | ((uint32_t)vid << 25);
-            he.guess = 0;
+            he.meta = (uint32_t)jm | ((uint32_t)vid << 25);
+            he.guess = c.f << 17;
             he.vq = 0.0f;
             c.gq[base + (uint32_t)e] = he;
         }
@@ -1166,7 +1166,8 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const uint32_t e = n - 1u - t;
         const HardEntry he = gq[e];
-        const int32_t f = (int32_t)((he.meta >> 17) & 255u), v = (int32_t)(he.meta >> 25);
+        const int32_t f = (int32_t)((uint32_t)he.guess >> 17), v = (int32_t)(he.meta >> 25);
+        const int32_t guess = he.guess & 0x1FFFF;
         OCC_CHECK(f < frames && v < nviews && he.pix >= 0 && (int64_t)he.pix < HW);
         const ViewDesc &vdv = views[v];
         const int32_t s = vdv.s;
@@ -1184,7 +1185,7 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
         const double jv = floor(__dadd_rn(__dmul_rn((double)s, (double)__fsub_rn(vmax, vp)), (double)p.t_dist));
         const int32_t jm = (int32_t)fmin((double)(he.meta & 0x1FFFFu), jv);
         bool hit = false;
-        if (he.guess >= 3 && jm >= 3) {
+        if (guess >= 3 && jm >= 3) {
             // the sweep's probe at he.guess read he.vq and missed: a slanted
             // occluder puts the partner near the fixed point j = s (vq - v_p)
             const double jf = rint(__dmul_rn((double)s, (double)__fsub_rn(he.vq, vp)));

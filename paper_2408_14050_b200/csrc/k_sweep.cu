@@ -793,8 +793,8 @@ __device__ __forceinline__ void s_resolve(const SweepArgs &a, const SU &u, const
                     if (slotq < (uint32_t)a.gq_cap) {
                         HardEntry he;
                         he.pix = (int32_t)(d.B + (int64_t)d.i * u.S);
-                        he.meta = (uint32_t)d.J | ((uint32_t)u.f << 17) | ((uint32_t)vid << 25);
-                        he.guess = d.j1;
+                        he.meta = (uint32_t)d.J | ((uint32_t)vid << 25);
+                        he.guess = d.j1 | (u.f << 17);
                         he.vq = vq;
                         a.gq[slotq] = he;
                     } else {

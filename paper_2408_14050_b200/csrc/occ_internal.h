@@ -161,8 +161,8 @@ struct LineUnit {
 // An exhaustive far-partner search deferred to k_hard (16 bytes): survivor at
 // pixel index pix of frame f (of the chunk), view v; partners at
 // pix + j * sg(v) * stride(kind(v)), j = 3 .. jm (dcov clipped to the image).
-// meta = jm | f << 17 | v << 25 (jm <= 2 * (65536 / 2) < 2^17, f < 256,
-// v < 64).
+// meta = jm | v << 25 (jm <= 2 * (65536 / 2) < 2^17, v < 128);
+// guess = j | f << 17 (j < 2^17 the sweep's failed probe offset or 0, f < 2^15).
 // A knight family served by k_sweep through a sheared copy of D (k_shear):
 // kind = the sweep kind its lines become (0 rows: x-major, 1 columns:
 // y-major); image line l = sheared line + lmin; f(t) = floor(t num / den).
@@ -172,10 +172,10 @@ struct ShearDesc {
 struct HardEntry {
     int32_t pix;
     uint32_t meta;
-    int32_t guess;      // offset of the sweep's failed probe (0: none)
+    int32_t guess;      // offset of the sweep's failed probe (0: none) | frame << 17
     float vq;           // the value it read (k_hard starts at its fixed point s (vq - v_p))
 };
-constexpr int kMaxChunkFrames = 255;     // f field of HardEntry
+constexpr int kMaxChunkFrames = 4096;    // frames per chunk (HardEntry's f: 15 bits)
 // Candidate words precomputed per chunk by k_cand (one entry per family;
 // families without line units have nlb = nk = 0): blocks of 32 lines x 32
 // positions, [frame][base_slot + lb * nk + (k - kmin)][view 2][lane 32] uint32.
