@@ -409,8 +409,9 @@ void build_tiles(occ_ctx *c) {
             const int32_t f0 = fdv(0), f1 = fdv(PM - 1);
             sd.lmin = -std::max(f0, f1);
             const int32_t nl = QM - 1 - std::min(f0, f1) - sd.lmin + 1;     // lines
+            // rows padded to 32 floats (NaN): TMA boxes need 16-byte row strides
             sf.Hs = fd.xmajor ? nl : H;
-            sf.Ws = fd.xmajor ? W : nl;
+            sf.Ws = ((fd.xmajor ? W : nl) + 31) & ~31;
             // units: 32-line blocks x seg positions over the block's in-image extent
             for (int32_t gi : gs) {
                 for (int32_t l0 = 0; l0 < nl; l0 += 32) {
