@@ -45,6 +45,13 @@ struct occ_ctx {
     std::vector<SweepUnit> sunits;        // k_sweep work (eligible groups; the default line path)
     SweepUnit *d_sunits = nullptr;
     uint32_t *d_words = nullptr;          // k_words -> k_sweep candidate words, one chunk of frames
+    // consecutive chunks on two streams (the second chunk's sweep fills the
+    // first chunk's k_hard and tail): a second words buffer, the main queue
+    // region split in two halves with their own counters
+    uint32_t *d_words2 = nullptr;
+    cudaStream_t s_alt = nullptr;
+    cudaEvent_t ev_alt_fork = nullptr, ev_alt_join = nullptr;
+    cudaEvent_t ev_swept[2] = {nullptr, nullptr};   // chunk's sweep done: the next chunk may start
     int32_t skstart[5] = {0, 0, 0, 0, 0}; // sunits of kind k at [skstart[k], skstart[k + 1])
     int32_t sfgroup = 1;                  // k_sweep work order: frames per group
     int32_t ssmin = 1;                    // smallest s of the k_sweep groups (k_sweep_small's frame filter)
@@ -644,10 +651,13 @@ int create_tail(occ_ctx *c, int32_t H, int32_t W, int32_t n_views, int32_t max_b
         cudaMalloc(&c->d_codes, (size_t)c->chunk * H * W * c->code_bytes) != cudaSuccess ||
         ((!c->units.empty() || !c->sunits.empty() || !c->shear.empty()) &&
          (cudaMalloc(&c->d_gq, sizeof(HardEntry) * (size_t)(c->gq_cap = gq_capacity(c->chunk, H, W, n_views))) != cudaSuccess ||
-          cudaMalloc(&c->d_gq_count, sizeof(uint32_t) * (1 + kMaxFamilies)) != cudaSuccess)) ||
+          cudaMalloc(&c->d_gq_count, sizeof(uint32_t) * (2 + kMaxFamilies)) != cudaSuccess)) ||
         ((!c->sunits.empty() || !c->shear.empty()) &&
          (cudaMalloc(&c->d_sunits, sizeof(SweepUnit) * std::max<size_t>(1, c->sunits.size())) != cudaSuccess ||
-          cudaMalloc(&c->d_words, sizeof(uint32_t) * (size_t)c->chunk * (size_t)sweep_words_per_frame(H, W)) != cudaSuccess)) ||
+          cudaMalloc(&c->d_words, sizeof(uint32_t) * (size_t)c->chunk * (size_t)sweep_words_per_frame(H, W)) != cudaSuccess ||
+          (max_batch > c->chunk &&
+           cudaMalloc(&c->d_words2, sizeof(uint32_t) * (size_t)c->chunk * (size_t)sweep_words_per_frame(H, W)) !=
+               cudaSuccess))) ||
         !alloc_shear(c)) {
         cudaGetLastError();
         occ_destroy(c);
@@ -910,7 +920,14 @@ int32_t smax_of(const occ_ctx *c) {
 }
 
 // K0 + K1 for frames [c0, c0 + n) of a batch whose frames start at D / M (device).
-int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, cudaStream_t s, int &launches) {
+// slot: 0, or 1 for the odd chunks of an alternating call (second words
+// buffer, second half of the main queue region); -1: the whole region
+int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, cudaStream_t s, int &launches,
+                 int slot = -1, cudaEvent_t swept = nullptr) {
+    uint32_t *words = slot == 1 ? c->d_words2 : c->d_words;
+    const int32_t qcap = slot < 0 ? c->main_qcap : c->main_qcap / 2;
+    HardEntry *gqm = c->d_gq + (slot == 1 ? qcap : 0);
+    uint32_t *gqc = slot == 1 ? c->d_gq_count + 1 + kMaxFamilies : c->d_gq_count;
     const int64_t HW = (int64_t)c->H * c->W;
     const float *Dc = D + (int64_t)c0 * HW;
     uint8_t *Mc = M + (int64_t)c0 * c->V * c->mf.vbytes;
@@ -922,7 +939,7 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
     {
         ProfScope ps(c, OCC_KERNEL_STATS, s);
         if (sweep) {
-            CK(launch_words(Dc, c->H, c->W, n, c->params.e2_thresh, c->d_stats + c0, c->d_words, 1, s)); ++launches;
+            CK(launch_words(Dc, c->H, c->W, n, c->params.e2_thresh, c->d_stats + c0, words, 1, s)); ++launches;
             if (nt > 0) {    // k_tile's groups read the per-pixel codes
                 CK(launch_prologue(Dc, c->H, c->W, n, c->fams.data(), c->nfam, c->params.e2_thresh,
                                    c->d_stats + c0, c->d_codes, c->code_bytes, 0, s)); ++launches;
@@ -947,7 +964,7 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
         return OCC_OK;
     }
     if (sweep) {
-        CK(cudaMemsetAsync(c->d_gq_count, 0, sizeof(uint32_t), s));
+        CK(cudaMemsetAsync(gqc, 0, sizeof(uint32_t), s));
 #ifdef OCC_CHECKS
         // poison the queue: a slot k_hard reads that this chunk did not write fails its checks
         CK(cudaMemsetAsync(c->d_gq, 0xFF, sizeof(HardEntry) * (size_t)c->gq_cap, s));
@@ -983,12 +1000,13 @@ int detect_chunk(occ_ctx *c, const float *D, uint8_t *M, int32_t c0, int32_t n, 
             // (profile scopes of one kind must not nest: the knight scopes above are closed)
             ProfScope pl(c, OCC_KERNEL_LINE, s);
             CK(launch_sweep(Dc, c->H, c->W, n, c->d_sunits, (int32_t)c->sunits.size(), c->d_groups, c->d_views, c->V,
-                            c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, c->d_words, c->d_gq, c->d_gq_count,
-                            c->main_qcap, c->skstart, c->sfgroup, c->d_dbg, c->ssmin, nullptr, s));
+                            c->d_fams, c->d_stats + c0, c->params, Mc, c->mf, words, gqm, gqc,
+                            qcap, c->skstart, c->sfgroup, c->d_dbg, c->ssmin, nullptr, s));
+            if (swept) CK(cudaEventRecord(swept, s));
             pl.end();
             ProfScope ph(c, OCC_KERNEL_HARD, s);
-            CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, c->d_gq, c->d_gq_count,
-                           c->main_qcap, c->d_stats + c0, c->nsm, s));
+            CK(launch_hard(Dc, Mc, c->mf, c->W, HW, n, c->V, c->d_views, c->params, gqm, gqc,
+                           qcap, c->d_stats + c0, c->nsm, s));
             launches += 3;       // k_sweep, k_sweep_small, k_hard
             ph.end();
         }
@@ -1062,9 +1080,43 @@ int occ_detect(occ_ctx *c, const float *D, uint8_t *M, int32_t batch, void *stre
         // chunks of ~256 MiB of D + codes: enough warps per K1 launch to fill
         // the GPU (the long-tailed per-unit times average out); K1's re-reads
         // of D mostly hit L2, the rest is a small fraction of the HBM bandwidth
-        for (int32_t c0 = 0; c0 < batch; c0 += c->chunk) {
-            const int rc = detect_chunk(c, D, M, c0, std::min(c->chunk, batch - c0), s, launches);
+        // several chunks of a sweep-only call: odd chunks on a second stream
+        // (own words buffer and queue half), so one chunk's sweep overlaps
+        // the other's k_hard and tail; joined back into s
+#ifdef OCC_CHECKS
+        const bool alt_on = false;        // (the checks poison the whole queue per chunk)
+#else
+        // opt-in (OCC_ALT=1): C5 18.82 vs 18.90 ms per step (A/B on one B200),
+        // but the overlapping launches blur the per-kernel event times
+        static const bool alt_on = [] { const char *ev = getenv("OCC_ALT"); return ev && atoi(ev) != 0; }();
+#endif
+        const bool alt = alt_on && batch > c->chunk && c->d_words2 && c->tiles.empty() && c->path == OCC_PATH_AUTO &&
+                         c->neighbors == 0 && !c->angles && !c->sunits.empty();
+        if (alt) {
+            if (!c->s_alt) {
+                CK(cudaStreamCreateWithFlags(&c->s_alt, cudaStreamNonBlocking));
+                CK(cudaEventCreateWithFlags(&c->ev_alt_fork, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&c->ev_alt_join, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&c->ev_swept[0], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&c->ev_swept[1], cudaEventDisableTiming));
+            }
+            CK(cudaEventRecord(c->ev_alt_fork, s));
+            CK(cudaStreamWaitEvent(c->s_alt, c->ev_alt_fork, 0));
+        }
+        int32_t ci = 0;
+        for (int32_t c0 = 0; c0 < batch; c0 += c->chunk, ++ci) {
+            const bool odd = alt && (ci & 1);
+            cudaStream_t cs = odd ? c->s_alt : s;
+            // a chunk starts once the previous chunk's sweep is done (two sweeps
+            // at once would share L2): it overlaps that chunk's k_hard
+            if (alt && ci > 0) CK(cudaStreamWaitEvent(cs, c->ev_swept[(ci - 1) & 1], 0));
+            const int rc = detect_chunk(c, D, M, c0, std::min(c->chunk, batch - c0), cs, launches,
+                                        alt ? (ci & 1) : -1, alt ? c->ev_swept[ci & 1] : nullptr);
             if (rc != OCC_OK) return rc;
+        }
+        if (alt) {
+            CK(cudaEventRecord(c->ev_alt_join, c->s_alt));
+            CK(cudaStreamWaitEvent(s, c->ev_alt_join, 0));
         }
     }
     c->last_stream = s;
@@ -1282,6 +1334,11 @@ int occ_destroy(occ_ctx *c) {
     cudaFree(c->d_units);
     cudaFree(c->d_sunits);
     cudaFree(c->d_words);
+    cudaFree(c->d_words2);
+    if (c->s_alt) cudaStreamDestroy(c->s_alt);
+    if (c->ev_alt_fork) cudaEventDestroy(c->ev_alt_fork);
+    if (c->ev_alt_join) cudaEventDestroy(c->ev_alt_join);
+    for (cudaEvent_t e : c->ev_swept) if (e) cudaEventDestroy(e);
     for (auto &sf : c->shear) {
         cudaFree(sf.d_units);
         cudaFree(sf.d_D);
