@@ -2,7 +2,8 @@
 the line sweep on a C2 crop and a noisy C3 crop (uint8 and bit-packed masks,
 both views of every family), a forced far-partner queue overflow
 (OCC_GQ_CAP=37: straddling reservations, in-warp fallback, k_hard), the
-knight Eq. 2 overflow repro (k_tile) and the median fusion; every output is
+knight Eq. 2 overflow repro, a C4 crop with the 5x5 array (sheared knight
+families), crops at h ~ 5 and ~ 300, and the median fusion; every output is
 checked against the oracle.  Usage: compute-sanitizer --tool X python tools/sanitize_cases.py"""
 import os
 import sys
@@ -47,6 +48,12 @@ Dk[3:, :21] = -3e38
 Dk[2, 20] = 1e38
 Dk[0, 17] = Dk[0, 18] = Dk[1, 17] = 1.0
 run(Dk, scenes.VIEWS_5X5, "knight overflow repro", max_scan=150)
+# knight baselines through the sheared frames (both majors), small and large h
+run(scenes.make_scene(4)[1000:1160, 1500:1820], scenes.VIEWS_5X5, "C4 crop, 5x5 array (sheared knights)")
+D3 = scenes.make_scene(3)[300:460, 700:1020].astype(np.float64)
+R = float(D3.max() - D3.min())
+run(scenes.scale_disparity(D3, 5.0 / R), scenes.VIEWS_3X3, "C3 crop at h ~ 5 (k_sweep_small)")
+run(scenes.scale_disparity(D3, 300.0 / R), scenes.VIEWS_3X3, "C3 crop at h ~ 300")
 rng = scenes.SplitMix64(77)
 st = ((rng.uniform(8 * 4099) - 0.3) * 80).astype(np.float32).reshape(8, 4099)
 out = fuse_median(torch.from_numpy(st).cuda()).cpu().numpy()
