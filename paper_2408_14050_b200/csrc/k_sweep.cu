@@ -45,6 +45,12 @@ constexpr int kSlot = 1280;              // floats per staging slot (5 KB: keeps
 constexpr int kWordSlots = 12;            // words per K0 block and lane
 }  // namespace
 
+// merged diagonal words: K0 ORs both halves of every diagonal / anti-diagonal
+// word (atomics into a zeroed buffer) so the sweep loads one word instead of
+// two and an OR (C5 A/B on one B200: 18.68 vs 18.91 ms per step)
+#ifndef SWEEP_DMERGE
+#define SWEEP_DMERGE 1
+#endif
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t s_ge(int32_t a) { return a <= 0 ? FULL : (a >= 32 ? 0u : (FULL << a)); }
 __device__ __forceinline__ uint32_t s_le(int32_t b) { return b < 0 ? 0u : (b >= 31 ? FULL : ((2u << b) - 1u)); }
@@ -120,7 +126,7 @@ struct WordsArgs {
     int32_t H, W, nxb, nyb;
     float e2_thresh;
     FrameStats *st;
-    uint32_t *words;       // [frame][nyb][nxb][12][32]
+    uint32_t *words;       // [frame][nyb][nxb + 1][12][32] (one spare column: merged diagonal words)
     int32_t do_stats;
 };
 
@@ -199,10 +205,26 @@ __global__ void __launch_bounds__(128) k_words(WordsArgs a) {
             o[8] = t6 & gea;  o[9] = t7 & gea;
             o[10] = t6 & ~gea; o[11] = t7 & ~gea;
         }
-        uint32_t *dst = a.words + ((((int64_t)f * a.nyb + m) * a.nxb + kx) * kWordSlots) * 32 + lane;
+        uint32_t *dst = a.words + ((((int64_t)f * a.nyb + m) * (a.nxb + 1) + kx) * kWordSlots) * 32 + lane;
         if (wok) {
+#if SWEEP_DMERGE
+            // the diagonal words of record (m, kx) are lower(m, kx) | upper(m,
+            // kx - 1): OR both halves into the zeroed slots 4, 5 / 8, 9 (the
+            // upper halves into the next record), so the sweep loads one word
+#pragma unroll
+            for (int s = 0; s < 4; ++s) dst[s * 32] = o[s];
+            atomicOr(dst + 4 * 32, o[4]);
+            atomicOr(dst + 5 * 32, o[5]);
+            atomicOr(dst + 8 * 32, o[8]);
+            atomicOr(dst + 9 * 32, o[9]);
+            atomicOr(dst + (kWordSlots + 4) * 32, o[6]);
+            atomicOr(dst + (kWordSlots + 5) * 32, o[7]);
+            atomicOr(dst + (kWordSlots + 8) * 32, o[10]);
+            atomicOr(dst + (kWordSlots + 9) * 32, o[11]);
+#else
 #pragma unroll
             for (int s = 0; s < kWordSlots; ++s) dst[s * 32] = o[s];
+#endif
         }
     }
     if (!a.do_stats) return;
@@ -225,6 +247,10 @@ __global__ void __launch_bounds__(128) k_words(WordsArgs a) {
 cudaError_t launch_words(const float *D, int32_t H, int32_t W, int32_t frames, float e2_thresh, FrameStats *st,
                          uint32_t *words, int32_t do_stats, cudaStream_t s) {
     WordsArgs a{D, H, W, (W + 31) / 32, (H + 31) / 32, e2_thresh, st, words, do_stats};
+#if SWEEP_DMERGE
+    cudaError_t e = cudaMemsetAsync(words, 0, sizeof(uint32_t) * (size_t)frames * sweep_words_per_frame(H, W), s);
+    if (e != cudaSuccess) return e;
+#endif
     dim3 grid((unsigned)((a.nxb + 3) / 4), (unsigned)a.nyb, (unsigned)frames);
     k_words<<<grid, 128, 0, s>>>(a);
     return cudaGetLastError();
@@ -336,15 +362,20 @@ __device__ __forceinline__ int32_t s_stride(int kind, int32_t W) {
 __device__ __forceinline__ uint32_t s_word1(const SU &u, int32_t k, int v) {
     const uint32_t *Wl = u.Wf + u.lane + 32 * v;
     constexpr int St = kWordSlots * 32;
-    if (u.kind == 0) return (uint32_t)k < (uint32_t)u.nxb ? __ldg(Wl + (u.A * u.nxb + k) * St) : 0u;
-    if (u.kind == 1) return (uint32_t)k < (uint32_t)u.nyb ? __ldg(Wl + (k * u.nxb + u.A) * St + 64) : 0u;
+    const int32_t P = u.nxb + 1;              // record pitch
+    if (u.kind == 0) return (uint32_t)k < (uint32_t)u.nxb ? __ldg(Wl + (u.A * P + k) * St) : 0u;
+    if (u.kind == 1) return (uint32_t)k < (uint32_t)u.nyb ? __ldg(Wl + (k * P + u.A) * St + 64) : 0u;
     const int32_t m = u.kind == 2 ? u.A + k : u.A - k;
     if ((uint32_t)m >= (uint32_t)u.nyb) return 0u;
-    const uint32_t *p = Wl + (m * u.nxb + k) * St + (u.kind == 2 ? 4 * 32 : 8 * 32);
+    const uint32_t *p = Wl + (m * P + k) * St + (u.kind == 2 ? 4 * 32 : 8 * 32);
+#if SWEEP_DMERGE
+    return (uint32_t)k <= (uint32_t)u.nxb ? __ldg(p) : 0u;
+#else
     uint32_t w = 0u;
     if ((uint32_t)k < (uint32_t)u.nxb) w = __ldg(p);
     if ((uint32_t)(k - 1) < (uint32_t)u.nxb) w |= __ldg(p - St + 64);
     return w;
+#endif
 }
 
 #ifndef SWEEP_ROWCOPY
@@ -829,7 +860,7 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
     u.S = s_stride(kind, u.W);
     const int64_t HW = (int64_t)a.H * a.W;
     u.Df = a.D + (int64_t)f * HW;
-    u.Wf = a.words + (int64_t)f * a.nyb * a.nxb * kWordSlots * 32;
+    u.Wf = a.words + (int64_t)f * a.nyb * (a.nxb + 1) * kWordSlots * 32;
     float *stg = reinterpret_cast<float *>(smem);
     Rec *rec = reinterpret_cast<Rec *>(smem + kRecOff);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kBarOff);
@@ -1342,7 +1373,7 @@ __global__ void __launch_bounds__(128) k_shear(ShearArgs a) {
     __syncwarp();
     const uint2 q = rw[warp][lane];
     if (!wok) return;
-    uint32_t *dst = a.words + (((int64_t)f * a.nyb + m) * a.nxb + kx) * kWordSlots * 32 + lane;
+    uint32_t *dst = a.words + (((int64_t)f * a.nyb + m) * (a.nxb + 1) + kx) * kWordSlots * 32 + lane;
     if (a.xmajor) {          // kind 0: lane = line (row of the block), bit = position (column)
         dst[0] = q.x;
         dst[32] = q.y;

@@ -233,7 +233,7 @@ struct SweepUnit {
 #endif
 constexpr int kSweepSeg = SWEEP_SEG;
 inline int64_t sweep_words_per_frame(int32_t H, int32_t W) {
-    return (int64_t)((H + 31) / 32) * ((W + 31) / 32) * 12 * 32;
+    return (int64_t)((H + 31) / 32) * ((W + 31) / 32 + 1) * 12 * 32;   // (+1: spare record column)
 }
 cudaError_t launch_words(const float *D, int32_t H, int32_t W, int32_t frames, float e2_thresh, FrameStats *st,
                          uint32_t *words, int32_t do_stats, cudaStream_t s);
