@@ -1223,19 +1223,27 @@ __global__ void __launch_bounds__(32, SWEEP_MINB) k_sweep_small(const __grid_con
     __syncwarp();
     uint32_t phase[2] = {0u, 0u};
     uint32_t item = 0;
-    for (int32_t f = 0; f < a.frames; ++f) {
-        const FrameStats fs = a.st[f];
-        const float R = frame_range(fs);
-        if (fs.nonfinite || view_h(R, smin, a.p.max_scan) >= 17) continue;
-        // this warp's units of the frame: items item + i with (item + i) % grid == block
-        const uint32_t G = gridDim.x;
-        const uint32_t i0 = (blockIdx.x + G - item % G) % G;
-        item += (uint32_t)a.nunits;
-        for (uint32_t i = i0; i < (uint32_t)a.nunits; i += G) {
-            const SweepUnit un = a.units[i];
-            const GroupDesc gd = a.groups[un.group];
-            const int32_t h = view_h(R, a.views[gd.view[0]].s, a.p.max_scan);
-            if (h > 0 && h < 17) sweep_unit<true, SHEAR>(a, tm, un, gd, f, smem, phase);
+    const int lane = threadIdx.x & 31;
+    for (int32_t f32 = 0; f32 < a.frames; f32 += 32) {
+        // the lanes test 32 frames at once; only small-h frames are walked
+        bool small = false;
+        if (f32 + lane < a.frames) {
+            const FrameStats fl = a.st[f32 + lane];
+            small = !fl.nonfinite && view_h(frame_range(fl), smin, a.p.max_scan) < 17;
+        }
+        for (uint32_t sm = __ballot_sync(FULL, small); sm; sm &= sm - 1u) {
+            const int32_t f = f32 + __ffs(sm) - 1;
+            const float R = frame_range(a.st[f]);
+            // this warp's units of the frame: items item + i with (item + i) % grid == block
+            const uint32_t G = gridDim.x;
+            const uint32_t i0 = (blockIdx.x + G - item % G) % G;
+            item += (uint32_t)a.nunits;
+            for (uint32_t i = i0; i < (uint32_t)a.nunits; i += G) {
+                const SweepUnit un = a.units[i];
+                const GroupDesc gd = a.groups[un.group];
+                const int32_t h = view_h(R, a.views[gd.view[0]].s, a.p.max_scan);
+                if (h > 0 && h < 17) sweep_unit<true, SHEAR>(a, tm, un, gd, f, smem, phase);
+            }
         }
     }
 }

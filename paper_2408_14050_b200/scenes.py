@@ -170,10 +170,22 @@ def make_scene(cfg: int, seed: int = 0, frame: int = 0) -> np.ndarray:
         img = np.full((c.H, c.W), 2.0, dtype=np.float64)
         img[y0:y0 + 16, x0:x0 + 20] = 8.0
         return img.astype(np.float32)
+    return make_scene_scaled(cfg, 1.0, seed, frame)
+
+
+def make_scene_scaled(cfg: int, scale: float, seed: int = 0, frame: int = 0) -> np.ndarray:
+    """The config-``cfg`` scene (2..5) with the layered, noise-free disparities
+    mapped d -> 1 + scale*(d - 1) BEFORE the config's estimation noise is added
+    (the noise stays sigma pixels: a stereo matcher's error does not grow with
+    the disparity).  scale = 1 is make_scene bit for bit (d - 1 + 1 is exact).
+    bench.py's h sweep uses it to set Eq. 3's h (about 66*scale for C3)."""
+    c = CONFIGS[cfg]
     base = 3 if cfg == 5 else cfg       # C5 frames are C3 scenes from seed+frame
     rng = SplitMix64(base, seed + frame)
     img = _background(c.H, c.W)
     _paint_layers(img, rng, c)
+    if scale != 1.0:
+        img = 1.0 + float(scale) * (img - 1.0)
     if c.noise_sigma > 0:
         noise = SplitMix64(base, seed + frame, 0x4E4F495345).normal(c.H * c.W)
         img = img + c.noise_sigma * noise.reshape(c.H, c.W)
