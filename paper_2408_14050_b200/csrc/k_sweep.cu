@@ -1175,9 +1175,10 @@ constexpr int kSweepWarps = 1;
 // minimum CTAs per SM of the launch bounds: a code-generation knob (the
 // kernel keeps 96 registers either way; 18 gives the smaller stack frame):
 // C5 A/B on one B200, ms per 256 frames: 16 22.06, 17 20.18, 18 20.23,
-// 19 20.66, 20 20.88, 22 / 24 (80 registers, spills) 22.8
+// 19 20.66, 20 20.88, 22 / 24 (80 registers, spills) 22.8; after the merged
+// diagonal words: 17 18.48, 18 18.67, 19 18.47, 20 18.56, 21 (80 registers) 20.56
 #ifndef SWEEP_MINB
-#define SWEEP_MINB 18
+#define SWEEP_MINB 19
 #endif
 template <bool SHEAR>
 __global__ void __launch_bounds__(32 * kSweepWarps, SWEEP_MINB) k_sweep(const __grid_constant__ SweepArgs a,
