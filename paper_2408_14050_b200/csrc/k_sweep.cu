@@ -1168,8 +1168,9 @@ __device__ __forceinline__ void sweep_unit(const SweepArgs &a, const SweepMaps &
 }
 
 // grid: CTAs of kSweepWarps warps, one unit per warp.  Work order: frame
-// groups of fgroup frames; inside a group all units of kind 0, then 1, 2, 3
-// (longest first), each over the group's frames: the warps in flight work
+// groups of fgroup frames; inside a group the units of one kind segment
+// after another (host order: diagonals, anti-diagonals, rows, columns;
+// longest first inside a segment), each over the group's frames: the warps in flight work
 // on a few frames, whose D and words stay in L2.
 constexpr int kSweepWarps = 1;
 // minimum CTAs per SM of the launch bounds: a code-generation knob (the

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "occ_internal.h"
@@ -377,14 +378,29 @@ void build_tiles(occ_ctx *c) {
         for (const SweepUnit &x : c->sunits) c->ssmin = std::min(c->ssmin, c->views[c->groups[x.group].view[0]].s);
         if (c->sunits.empty()) c->ssmin = 1;
         // by kind, longest first inside a kind (k_sweep's work order, k_sweep.cu)
-        auto kind_of = [&](const SweepUnit &x) { return c->fams[c->groups[x.group].fam].kind; };
+        // segment order of the kinds inside a frame group: diagonals (the
+        // longer units, ~1.7x a row unit's work) first, so a group's last
+        // wave is made of short units (C5 A/B on one B200, ms per step:
+        // 0123 18.46, 2301 18.33, 2310 18.35, 0132 18.52); OCC_SWEEP_KORDER
+        // overrides it (a permutation of "0123"; the kernel takes the
+        // segments in turn whatever kinds they hold)
+        static const std::string korder = [] {
+            const char *ev = getenv("OCC_SWEEP_KORDER");
+            std::string o = ev ? ev : "2301";
+            std::string t = o;
+            std::sort(t.begin(), t.end());
+            return t == "0123" ? o : std::string("2301");
+        }();
+        auto rank_of = [&](const SweepUnit &x) {
+            return (int)korder.find((char)('0' + c->fams[c->groups[x.group].fam].kind));
+        };
         std::stable_sort(c->sunits.begin(), c->sunits.end(), [&](const SweepUnit &x, const SweepUnit &y) {
-            if (kind_of(x) != kind_of(y)) return kind_of(x) < kind_of(y);
+            if (rank_of(x) != rank_of(y)) return rank_of(x) < rank_of(y);
             return x.t1 - x.t0 > y.t1 - y.t0;
         });
         for (int k = 0; k <= 4; ++k) {
             int32_t n = 0;
-            for (const SweepUnit &x : c->sunits) n += kind_of(x) < k ? 1 : 0;
+            for (const SweepUnit &x : c->sunits) n += rank_of(x) < k ? 1 : 0;
             c->skstart[k] = n;
         }
         // frames per group: every kind's share of a group about one resident
