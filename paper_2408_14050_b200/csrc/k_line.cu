@@ -1,3 +1,5 @@
+#include <algorithm>
+#include <cstdlib>
 // k_line.cu -- K2, the line-sweep kernel for the four line families of
 // |b| <= 1 camera arrays (rows, columns, diagonals, anti-diagonals): Eqs. 1-6
 // for a pair of views +-b of one family.
@@ -1244,11 +1246,22 @@ cudaError_t launch_hard(const float *D, uint8_t *masks, const MaskFmt &mf, int32
                         int32_t nviews, const ViewDesc *views,
                         const Params &p, const HardEntry *gq, const uint32_t *gq_count, int32_t gq_cap,
                         const FrameStats *st, int32_t nsm, cudaStream_t s, const ShearDesc *sh) {
+    // Grid: about two entries per thread for the expected queue (1.5 % of the
+    // chunk's pixel-views at C5), so the block scheduler balances the
+    // variable-length searches (a resident grid-striding 8 blocks per SM left
+    // a tail: C5 k_hard 3.21 -> 2.63 ms per step at 256 blocks per SM, A/B on
+    // one B200); at least 8 blocks per SM, at most 256 (OCC_HARD_GRID: fixed
+    // blocks per SM).  More entries than threads are grid-strided.
+    static const int bps = [] { const char *ev = getenv("OCC_HARD_GRID"); return ev ? std::max(1, atoi(ev)) : 0; }();
+    const int64_t pv = (int64_t)frames * HW * nviews;
+    const int64_t want = (int64_t)(0.015 * (double)pv) / 512 + 1;
+    const int64_t blocks = bps ? (int64_t)nsm * bps : std::min<int64_t>((int64_t)nsm * 256, std::max<int64_t>((int64_t)nsm * 8, want));
     if (sh)
-        k_hard<true><<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, frames, nviews, views, p, gq, gq_count, gq_cap, st, *sh);
+        k_hard<true><<<(unsigned)blocks, 256, 0, s>>>(D, masks, mf, W, HW, frames, nviews, views, p, gq, gq_count, gq_cap,
+                                                      st, *sh);
     else
-        k_hard<false><<<nsm * 8, 256, 0, s>>>(D, masks, mf, W, HW, frames, nviews, views, p, gq, gq_count, gq_cap, st,
-                                              ShearDesc{});
+        k_hard<false><<<(unsigned)blocks, 256, 0, s>>>(D, masks, mf, W, HW, frames, nviews, views, p, gq, gq_count, gq_cap,
+                                                       st, ShearDesc{});
     return cudaGetLastError();
 }
 
