@@ -54,3 +54,15 @@ def test_h_range_s2(torch_cuda, h_target):
     views = [(2, 0), (-2, 0), (0, 2), (2, 2), (1, 0)]
     g, st = run_gpu(torch_cuda, D, views)
     assert_same(g[0], oracle.detect(D, views), f"s=2 h target {h_target}")
+
+
+def test_h_range_ragged_gate(torch_cuda):
+    # long far searches (jm >= k_hard's HARD_GATE) skip batches by the
+    # 32 x 32 block maxima of K0: ragged frame edges (partial blocks), a
+    # second frame (the maxima's frame offset) and s = 2 views
+    D = np.stack([scaled_crop(300, 150, 400, 150, 301, 0), scaled_crop(450, 600, 1000, 150, 301, 4)])
+    views = scenes.VIEWS_3X3 + [(2, 2), (-2, 0)]
+    g, st = run_gpu(torch_cuda, D, views)
+    assert st == [0, 0]
+    for f in range(2):
+        assert_same(g[f], oracle.detect(D[f], views), f"frame {f}")
