@@ -1207,23 +1207,30 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
         for (int32_t j0 = 3; j0 <= jm && !hit; j0 += HARD_BATCH) {
             float vq[HARD_BATCH];
 #pragma unroll
-            for (int u = 0; u < HARD_BATCH; ++u) {
+            for (int u = 0; u < HARD_BATCH; ++u)
                 OCC_CHECK(j0 + u > jm || ((int64_t)he.pix + (int64_t)(j0 + u) * step >= 0 &&
                                           (int64_t)he.pix + (int64_t)(j0 + u) * step < HW));
-                vq[u] = (j0 + u <= jm) ? __ldg(Ds + (int64_t)(j0 + u) * step) : NaN;
+            // addresses by pointer steps; whole batches below jm unpredicated
+            const float *q = Ds + (int64_t)j0 * step;
+            if (j0 + HARD_BATCH - 1 <= jm) {
+#pragma unroll
+                for (int u = 0; u < HARD_BATCH; ++u) { vq[u] = __ldg(q); q += step; }
+            } else {
+#pragma unroll
+                for (int u = 0; u < HARD_BATCH; ++u) { vq[u] = (j0 + u <= jm) ? __ldg(q) : NaN; q += step; }
             }
             // branch-free fast test of the HARD_BATCH offsets (fp32 with the 2^-10
-            // band, as pair_far); offsets inside the band take the exact test
+            // band, as pair_far); offsets inside the band take the exact test.
+            // No offset below the band (mn >= tlo): some offset lies in the
+            // band iff the minimum does (fminf skips the NaNs beyond jm)
             float mn = INFINITY;
-            bool band = false;
 #pragma unroll
             for (int u = 0; u < HARD_BATCH; ++u) {
                 vq[u] = fabsf(__fmaf_rn(vk.fs, __fsub_rn(vq[u], vp), -(float)(j0 + u)));   // NaN beyond jm
                 mn = fminf(mn, vq[u]);
-                band |= vq[u] >= vk.tlo && vq[u] <= vk.thi;
             }
             hit = mn < vk.tlo;
-            if (!hit && band) {
+            if (!hit && mn <= vk.thi) {
                 for (int u = 0; u < HARD_BATCH && !hit; ++u)
                     if (vq[u] >= vk.tlo && vq[u] <= vk.thi)
                         hit = pair_exact_slow(__ldg(Ds + (int64_t)(j0 + u) * step), vp, j0 + u, s, p.t_dist, p.t_disp);
