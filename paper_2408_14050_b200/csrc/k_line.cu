@@ -1152,6 +1152,9 @@ __global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
 #ifndef HARD_MINB
 #define HARD_MINB 4
 #endif
+#ifndef HARD_PROBE_LEAN
+#define HARD_PROBE_LEAN 0
+#endif
 // SHEAR: the entries of a knight family swept through its sheared copy
 // (k_shear): D, W, HW are the sheared frame's, the line step is 1 (rows) or
 // W (columns), and the mask pixel is un-sheared (ShearDesc, occ_internal.h)
@@ -1193,6 +1196,31 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
             const double jf = rint(__dmul_rn((double)s, (double)__fsub_rn(he.vq, vp)));
             const int32_t j2 = (int32_t)fmin(fmax(jf, 3.0), (double)jm);
             float w[5];
+#if HARD_PROBE_LEAN
+            // as the scan batches: pointer steps, one minimum, the exact test
+            // only when the minimum lies in the 2^-10 band
+            const float *q = Ds + (int64_t)(j2 - 2) * step;
+            float mn = INFINITY;
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+                const int32_t j = j2 - 2 + u;
+                w[u] = (j >= 3 && j <= jm) ? __ldg(q) : NaN;
+                q += step;
+            }
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+                const float x = fabsf(__fmaf_rn(vk.fs, __fsub_rn(w[u], vp), -(float)(j2 - 2 + u)));   // NaN off range
+                mn = fminf(mn, x);
+            }
+            hit = mn < vk.tlo;
+            if (!hit && mn <= vk.thi) {
+#pragma unroll
+                for (int u = 0; u < 5; ++u) {
+                    const int32_t j = j2 - 2 + u;
+                    if (!hit && j >= 3 && j <= jm) hit = pair_far(w[u], vp, j, vk, p);
+                }
+            }
+#else
 #pragma unroll
             for (int u = 0; u < 5; ++u) {
                 const int32_t j = j2 - 2 + u;
@@ -1203,6 +1231,7 @@ __global__ void __launch_bounds__(256, HARD_MINB) k_hard(const float *__restrict
                 const int32_t j = j2 - 2 + u;
                 if (!hit && j >= 3 && j <= jm) hit = pair_far(w[u], vp, j, vk, p);
             }
+#endif
         }
         for (int32_t j0 = 3; j0 <= jm && !hit; j0 += HARD_BATCH) {
             float vq[HARD_BATCH];
