@@ -1153,7 +1153,7 @@ __global__ void __launch_bounds__(128, LINE_MINB) k_line(LineArgs a) {
 #define HARD_MINB 4
 #endif
 #ifndef HARD_PROBE_LEAN
-#define HARD_PROBE_LEAN 0
+#define HARD_PROBE_LEAN 1    // (C5 k_hard 2.46 -> 2.39 ms per step, A/B on one B200)
 #endif
 // SHEAR: the entries of a knight family swept through its sheared copy
 // (k_shear): D, W, HW are the sheared frame's, the line step is 1 (rows) or
