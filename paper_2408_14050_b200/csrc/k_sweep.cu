@@ -51,6 +51,9 @@ constexpr int kWordSlots = 12;            // words per K0 block and lane
 #ifndef SWEEP_DMERGE
 #define SWEEP_DMERGE 1
 #endif
+#ifndef SWEEP_STORE_LEAN
+#define SWEEP_STORE_LEAN 0
+#endif
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t s_ge(int32_t a) { return a <= 0 ? FULL : (a >= 32 ? 0u : (FULL << a)); }
 __device__ __forceinline__ uint32_t s_le(int32_t b) { return b < 0 ? 0u : (b >= 31 ? FULL : ((2u << b) - 1u)); }
@@ -554,8 +557,15 @@ __device__ __noinline__ void s_store(const SU &u, uint8_t *Mv, const MaskFmt &mf
     }
 #endif
     if (32 * k >= u.elo && 32 * k + 32 <= u.ehi) {
+#if SWEEP_STORE_LEAN
+        // pointer steps and a shifted word (no per-byte variable shift)
+        uint32_t w = word;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) { __stcs(dst, (uint8_t)(w & 1u)); w >>= 1; dst += S; }
+#else
 #pragma unroll 8
         for (int r = 0; r < 32; ++r) __stcs(dst + r * S, (uint8_t)((word >> r) & 1u));
+#endif
     } else {
         for (int r = 0; r < 32; ++r) {
             const int32_t tau = 32 * k + r;
