@@ -52,7 +52,7 @@ constexpr int kWordSlots = 12;            // words per K0 block and lane
 #define SWEEP_DMERGE 1
 #endif
 #ifndef SWEEP_STORE_LEAN
-#define SWEEP_STORE_LEAN 0
+#define SWEEP_STORE_LEAN 1
 #endif
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t s_ge(int32_t a) { return a <= 0 ? FULL : (a >= 32 ? 0u : (FULL << a)); }
